@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""PDF solver hot-path benchmark on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json metric, config 2): one 64x64 scene, 16 plane-wave
+incidences, 32 receivers, m_f = 8 (15x15 modes), 500 Adam iterations.
+A STEP is one full 500-iteration optimisation loop of that scene with its
+inputs (data, alpha0, operators) resident in HBM; L2 is flushed between
+steps.  value = whole-job iterations/s (N GPUs each run their own scene,
+weak scaling, no collective).  e2e = the same metric through the public
+API (BatchReconstructor.run on HOST data: H2D, bp_initialize, init_alpha,
+the loop, forward_net + loss_total + recover_contrast + CCO, D2H).
+`batched` adds the config-4 form: S scenes per GPU reconstructed together
+(scenes/s).  --impl reference times the CPU oracle port of the reference
+algorithm on the host cores on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "PDF solver iter/s (fwd+bwd) and scenes/s at 64x64, 16 inc; % of roofline"
+WORKLOAD = ("cfg2: 64x64 grid on [-1,1] lambda, 16 plane-wave incidences, 32 receivers at 3 lambda, "
+            "m_f=8 (15x15 modes), beta=6, CIE+bridge loss, 500 Adam iterations per reconstruction")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=500)
+    ap.add_argument("--batch", type=int, default=256, help="scenes for the batched (config 4) leg; 0 = skip")
+    ap.add_argument("--batch-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-iters", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class Dist:
+    def __init__(self, gpus):
+        self.rank, self.world, self.local = dist_env()
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.th = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def cpu_oracle_rate(iters: int, threads: int | None):
+    """Iterations/s of the oracle port of the reference loop (grad_loss + Adam) on host cores."""
+    from threadpoolctl import threadpool_limits
+    from oracle import pdf_oracle as O
+    from paper_2602_13805_b200.workloads import baseline_config, baseline_scene
+    from paper_2602_13805_b200 import build_array, build_grid, plane_wave_fields
+    cfg = baseline_config(2)
+    grid, arr = build_grid(cfg), build_array(cfg)
+    e_inc = plane_wave_fields(cfg, grid).views
+    ops = O.build_operators(cfg.wavenumber, cfg.doi_side, cfg.m1, cfg.m2, arr.rx_positions)
+    # measured data: a noise-free-enough synthetic stand-in from the oracle's own forward model
+    scene, rng, snr = baseline_scene(2)
+    from paper_2602_13805_b200.scenes import rasterize
+    chi = rasterize(scene, grid).values
+    jt = chi * e_inc   # Born-level current; the step cost does not depend on the data values
+    data = jt.reshape(cfg.n_tx, -1) @ ops.gs.T
+    ctx = O.Context(data, e_inc, ops, cfg.m_f, cfg.beta, (cfg.lambda1, cfg.lambda2, cfg.lambda3), cfg.tau_b)
+    chi0, r0 = O.bp_initialize(data, e_inc, ops, cfg.beta)
+    a0 = O.init_alpha(r0, data, e_inc, ops, cfg.m_f, cfg.beta)
+    params = O.init_net(4 * cfg.m_f ** 2, np.random.default_rng(cfg.rng_seed))
+    theta = O.flat(params)
+    adam = O.Adam(m=np.zeros_like(theta), v=np.zeros_like(theta), lr=cfg.learn_rate)
+    with threadpool_limits(limits=threads):
+        g, _ = O.grad_loss(O.unflat(theta, params), a0, ctx)   # warm
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            g, _ = O.grad_loss(O.unflat(theta, params), a0, ctx)
+            theta = O.adam_update(adam, theta, g)
+        dt = time.perf_counter() - t0
+    return iters / dt, dt
+
+
+def cpu_baseline(iters: int):
+    ncores = os.cpu_count() or 1
+    best = None
+    for th in (1, ncores):
+        rate, dt = cpu_oracle_rate(iters, th)
+        if best is None or rate > best[0]:
+            best = (rate, dt, th)
+    return {"value": best[0], "unit": "iter/s", "cores": best[2], "kind": "port",
+            "sample": f"{iters} iterations of the cfg2 loop (grad_loss + Adam, oracle/pdf_oracle.py numpy port), "
+                      f"best of 1 and {ncores} BLAS threads, {best[1]:.2f} s"}
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    k = args.cpu_sample_iters
+    for _ in range(args.warmup):
+        cpu_oracle_rate(1, None)
+    rates, times = [], []
+    ncores = os.cpu_count() or 1
+    for _ in range(args.steps):
+        r, dt = cpu_oracle_rate(k, ncores)
+        r1, dt1 = cpu_oracle_rate(k, 1)
+        rates.append(max(r, r1))
+        times.append(min(dt, dt1))
+    v = float(np.median(rates))
+    line = {"metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(times)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_iters_per_step": k},
+            "cpu_baseline": {"value": v, "unit": "iter/s", "cores": ncores, "kind": "port",
+                             "sample": f"{k} iterations per step of the cfg2 loop, numpy oracle port "
+                                       f"(reference is pure Python; best of 1 / {ncores} BLAS threads)"},
+            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def algorithmic_work(dev, phase: str):
+    """Algorithmic bytes (HBM-bound kernels) or FP64 flops per launch."""
+    M, P, n, R, S = dev.M, 2 * dev.M, dev.n, dev.R, dev.S
+    K = 2 * dev.mf
+    rows, D0, H = dev.rows, dev.d0, dev.hidden
+    es = 8 if dev.rdt.itemsize == 8 else 4
+    cs = 2 * es
+    lg = np.log2(P * P)
+    if phase in ("view_fwd", "view_bwd"):
+        fft = 2 * 5 * P * P * lg + 6 * P * P                  # forward + inverse padded 2-D FFT, x K^
+        spec = 8 * (M * K * K + M * M * K)                     # corner-sparse DFT contraction
+        gs = 8 * M * M * R if phase == "view_fwd" else 0       # data GEMM row
+        return "fp64", S * n * (fft + spec + gs)
+    if phase == "pixel":
+        return "hbm", S * (4 * n * M * M * cs + R * M * M * cs)
+    layer = {"fwd_l1": (H, D0), "fwd_l2": (H, H), "fwd_l3": (D0, H),
+             "bwd_l1": (H, D0), "bwd_l2": (H, H), "bwd_l3": (D0, H)}.get(phase)
+    if layer is None:
+        return "hbm", S * 64
+    N_, K_ = layer
+    if phase.startswith("fwd"):
+        return "hbm", S * es * (N_ * K_ + rows * K_ + rows * N_)
+    return "hbm", S * es * (6 * N_ * K_ + rows * (K_ + 2 * N_))
+
+
+def run_ours(args, d: Dist):
+    import torch
+    from paper_2602_13805_b200 import plane_wave_fields, build_grid
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.workloads import baseline_config, baseline_scene, cfg4_scene, synthesize_gpu, SNR_5PCT
+    from paper_2602_13805_b200 import _native as N
+
+    torch.cuda.set_device(d.local)
+    k = args.iters
+    cfg = baseline_config(2, k_iters=k)
+    # each rank reconstructs its own scene: config-2 geometry, scene/noise seeds offset by rank
+    scene, rng, snr = baseline_scene(2)
+    if d.rank:
+        scene, rng = cfg4_scene(d.rank)[0], np.random.default_rng(1000 + d.rank)
+    data, chi_true = synthesize_gpu(cfg, [scene], [rng], snr)
+    e_inc = plane_wave_fields(cfg, build_grid(cfg)).views
+    rec = BatchReconstructor(cfg, 1, e_inc=e_inc, dtype=args.dtype)
+    dev = rec.dev
+    dev.set_data(data)
+    chi0, r0 = dev.bp_initialize()
+    alpha0 = dev.init_alpha(r0)
+    dev.net_setup(alpha0)
+    theta0 = torch.as_tensor(_theta0([cfg.rng_seed], rec.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
+    theta, m, v = theta0.clone(), torch.zeros_like(theta0), torch.zeros_like(theta0)
+    trace = torch.zeros(k, 1, 6, dtype=torch.float64, device=dev.device)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev.device)
+
+    def step():
+        theta.copy_(theta0)
+        m.zero_()
+        v.zero_()
+        dev.train(theta, m, v, 0, k, trace, use_graph=True)
+
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    dev.check_errors()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(d.local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            flush.fill_(1)      # L2 flush between steps (256 MiB write > 126 MB L2)
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    d.barrier()
+    ms_total = d.max(e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    value = d.world * k / (ms_step / 1e3)
+    dev.check_errors()
+    final_total = float(trace[-1, 0, 5].item())
+
+    # ---- per-kernel live timing (events between kernels of un-graphed iterations)
+    theta.copy_(theta0); m.zero_(); v.zero_()
+    phases = dev.profile_phases(theta, m, v, 0, 20)
+    dev.check_errors()
+    share = {p: t / sum(phases.values()) for p, t in phases.items()}
+    dom = max(phases, key=phases.get)
+    bound, work = algorithmic_work(dev, dom)
+    import ctypes as ct
+    g = ct.c_double()
+    N.check(N.lib().pdf_fp64_probe(ct.byref(g), ct.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    fp64_peak_tflops = g.value / 1e3
+    peaks = json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(HERE, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    launch_s = phases[dom] / 1e3
+    if bound == "hbm":
+        achieved = work / launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    else:
+        achieved = work / launch_s / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak_tflops, "peak_source": "pdf_fp64_probe DFMA kernel (measured live)"}
+    roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom], "traffic": None,
+                 "share_of_step": share[dom]})
+
+    # ---- e2e through the public API with host buffers (per step: H2D data, D2H results)
+    res = rec.run([data[0]], seeds=[cfg.rng_seed], chi_trues=[chi_true[0]])   # warm (theta0 cache)
+    for _ in range(2):
+        rec.run([data[0]], seeds=[cfg.rng_seed])
+    torch.cuda.synchronize()
+    d.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = rec.run([data[0]], seeds=[cfg.rng_seed], chi_trues=[chi_true[0]])
+    torch.cuda.synchronize()
+    e2e_s = d.max((time.perf_counter() - t0) / args.steps)
+    M = cfg.m1
+    h2d = data[0].nbytes
+    d2h = 3 * M * M * 16 + k * 6 * 8 + 6 * 8
+
+    # ---- batched (config 4 form): S scenes per GPU
+    batched = None
+    if args.batch:
+        S = max(1, args.batch // d.world)
+        cfg4 = baseline_config(4, k_iters=k)
+        idx = list(range(d.rank * S, (d.rank + 1) * S))
+        sc = [cfg4_scene(i) for i in idx]
+        datab, chib = synthesize_gpu(cfg4, [s for s, _ in sc], [r for _, r in sc], SNR_5PCT)
+        rb = BatchReconstructor(cfg4, S, e_inc=e_inc, dtype=args.dtype, theta_cache=False)
+        rb.run(list(datab), seeds=idx, k_iters=k)          # warm-up
+        torch.cuda.synchronize()
+        d.barrier()
+        tb0 = time.perf_counter()
+        for _ in range(args.batch_steps):
+            outb = rb.run(list(datab), seeds=idx, chi_trues=list(chib), k_iters=k)
+        torch.cuda.synchronize()
+        tb = d.max((time.perf_counter() - tb0) / args.batch_steps)
+        # device-resident batched loop only
+        devb = rb.dev
+        th0 = torch.as_tensor(_theta0(idx, rb.m0_eff), dtype=devb.rdt, device=devb.device)
+        thb, mb, vb = th0.clone(), torch.zeros_like(th0), torch.zeros_like(th0)
+        trb = torch.zeros(k, S, 6, dtype=torch.float64, device=devb.device)
+        devb.train(thb, mb, vb, 0, k, trb)
+        torch.cuda.synchronize()
+        eb0, eb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        thb.copy_(th0); mb.zero_(); vb.zero_()
+        eb0.record()
+        devb.train(thb, mb, vb, 0, k, trb)
+        eb1.record()
+        torch.cuda.synchronize()
+        tdev = d.max(eb0.elapsed_time(eb1) / 1e3)
+        thb.copy_(th0); mb.zero_(); vb.zero_()
+        phb = devb.profile_phases(thb, mb, vb, 0, 3)
+        devb.check_errors()
+        rels = [o.rel_error for o in outb]
+        batched = {"workload": f"cfg4: {S * d.world} scenes of 1-4 random ellipses (seed = scene index), "
+                               f"{S} per GPU, {k} iterations each",
+                   "scenes_per_s": d.world * S / tdev, "iter_per_s": d.world * S * k / tdev,
+                   "e2e_scenes_per_s": d.world * S / tb, "s_per_batch": tdev, "e2e_s_per_batch": tb,
+                   "median_rel_error": float(np.median(rels)), "phases_ms": phb,
+                   "scaling": "strong (256 scenes split over the GPUs)"}
+
+    cpu = None
+    if d.rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample_iters)
+
+    line = {"metric": METRIC, "value": value, "unit": "iter/s", "n_gpus": d.world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128/f64" if args.dtype == "f64" else "c64/f32",
+            "data": "synthetic (seeded BASELINE cfg2 scene, GPU MoM forward solve + 5% AWGN)",
+            "config": {"workload": WORKLOAD, "k_iters": k, "scenes_per_gpu": 1,
+                       "parallelism": f"scene-sharded x{d.world} (no collective)",
+                       "l2": "flushed between steps (256 MiB write)", "graph": "CUDA graph of 10 iterations",
+                       "final_loss_total": final_total},
+            "e2e": {"value": d.world * k / e2e_s, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "s_per_reconstruction": e2e_s,
+                    "api": "BatchReconstructor.run(host data) -> ReconstructionResult",
+                    "rel_error": res[0].rel_error},
+            "roofline": roof, "phases_ms": phases, "fp64_peak_tflops_measured": fp64_peak_tflops,
+            "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": args.steps * (1 + 10 * k), "batched": batched}
+    if d.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    d = Dist(args.gpus)
+    try:
+        if args.impl == "reference":
+            run_reference(args, d)
+        else:
+            run_ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

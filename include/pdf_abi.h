@@ -1,0 +1,150 @@
+/*
+ * pdf_abi.h -- C ABI of the B200 (sm_100a) PDF inverse-scattering hot path.
+ *
+ * The reference (`pdfisp`, pure Python) has no FFI; its drop-in boundary for
+ * this path is a set of Python functions.  Each entry point below replaces
+ * one of them (citations relative to /root/reference/pkg/src/pdfisp/):
+ *
+ *   pdf_ctx_create      LossContext.__post_init__      losses.py:52-80
+ *                       (+ GreensOperators upload,      forward.py:69-94)
+ *   pdf_loss_grad       grad_alpha / pipeline_forward   losses.py:309-312,
+ *                       + pipeline_backward             losses.py:215-306
+ *   pdf_loss_value      loss_total / recover_contrast   losses.py:250-252, cie.py:83-99
+ *   pdf_net_setup       _feature_scales/_split_views    network.py:88-136
+ *   pdf_net_forward     alpha0 + forward_net            network.py:143-150
+ *   pdf_grad_loss       grad_loss                       network.py:183-223
+ *   pdf_adam_step       adam_step                       network.py:248-264
+ *   pdf_set_norms       LossContext c_inc / c_sca       losses.py:67-76
+ *   pdf_train           reconstruct hot loop            reconstruct.py:217-221
+ *   pdf_apply_gd        apply_gd / apply_gd_adjoint     forward.py:140-151
+ *   pdf_gs_forward      J @ gs_matrix.T                 losses.py:229, reconstruct.py:62
+ *   pdf_gs_adjoint      apply_gs_adjoint                forward.py:303-306
+ *   pdf_expand          expand                          spectral.py:68-79
+ *   pdf_truncate        truncate                        spectral.py:56-65
+ *   pdf_apply_cco       apply_cco                       filters.py:56-67
+ *   pdf_get_error       PoleError / FloatingPointError  cie.py:27-29, losses.py:239-243,
+ *                                                       network.py:221-222, 260-261
+ *
+ * Conventions: all array pointers are DEVICE pointers owned by the caller,
+ * complex numbers are interleaved (re, im) in the context's real type
+ * (complex128 for PDF_F64, complex64 for PDF_F32), arrays are C-contiguous
+ * with the reference's shapes, `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Every call is asynchronous on `stream` except
+ * pdf_ctx_create (synchronous upload of constants) and pdf_get_error
+ * (synchronises `stream`).  A context is not thread-safe; separate contexts
+ * may run concurrently.  Return value 0 = success, < 0 = error, message via
+ * pdf_last_error().
+ */
+#ifndef PDF_ABI_H
+#define PDF_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDF_ABI_VERSION 1
+
+enum pdf_dtype { PDF_F64 = 0, PDF_F32 = 1 };
+
+/* sticky device error bits (per scene) */
+enum pdf_error_bits {
+  PDF_ERR_POLE = 1,             /* PoleError: |beta chi + 1| < 1e-14            */
+  PDF_ERR_NONFINITE_STATE = 2,  /* FloatingPointError: nonfinite loss term(s)   */
+  PDF_ERR_NONFINITE_DATA = 4,
+  PDF_ERR_NONFINITE_BOUND = 8,
+  PDF_ERR_NONFINITE_TV = 16,
+  PDF_ERR_NONFINITE_BRIDGE = 32,
+  PDF_ERR_NONFINITE_GRAD = 64,  /* FloatingPointError: nonfinite parameter grad */
+  PDF_ERR_NONFINITE_PARAM = 128 /* FloatingPointError: nonfinite params after Adam */
+};
+
+enum pdf_status {
+  PDF_OK = 0,
+  PDF_EINVAL = -1,      /* bad argument / unsupported shape */
+  PDF_ECUDA = -2,       /* CUDA runtime error */
+  PDF_ENOMEM = -3       /* workspace too small */
+};
+
+typedef struct pdf_ctx pdf_ctx;
+
+typedef struct pdf_desc {
+  int32_t abi_version;   /* PDF_ABI_VERSION */
+  int32_t dtype;         /* enum pdf_dtype */
+  int32_t S;             /* scenes sharing one geometry (batched reconstruction) */
+  int32_t n;             /* incidences (views) */
+  int32_t m1, m2;        /* grid; m1 == m2, power of two, 16..128 */
+  int32_t R;             /* receivers */
+  int32_t mf;            /* corner-block edge, m0 = 4 mf^2 */
+  int32_t joint;         /* ImagingConfig.joint_views */
+  int32_t freeze_r;      /* ImagingConfig.freeze_r (r_fixed must be given) */
+  double beta, lambda1, lambda2, lambda3, tau_b;
+  double lr, adam_b1, adam_b2, adam_eps;
+  const void* e_inc;           /* [S or 1][n][m1][m2] complex */
+  int64_t e_inc_scene_stride;  /* elements between scenes; 0 = shared */
+  const void* gd_kernel_hat;   /* [2 m1][2 m2] complex, natural fft2 order */
+  const void* gs_matrix;       /* [R][m1 m2] complex */
+  const void* data;            /* [S][n][R] complex measured field */
+  const void* mask;            /* [S][n][R] real, or NULL */
+  const void* r_fixed;         /* [S][m1][m2] complex, or NULL */
+  const double* c_inc;         /* HOST [S]: ||E_inc||^2   (losses.py:72) */
+  const double* c_sca;         /* HOST [S]: ||mask d||^2  (losses.py:71) */
+  int32_t k_iters_max;         /* reserved */
+} pdf_desc;
+
+const char* pdf_last_error(void);
+int pdf_abi_version(void);
+
+size_t pdf_workspace_bytes(const pdf_desc* desc);
+int pdf_ctx_create(const pdf_desc* desc, void* workspace, size_t workspace_bytes, void* stream,
+                   pdf_ctx** out);
+int pdf_ctx_destroy(pdf_ctx* ctx);
+
+/* network geometry: rows, d0 (= input/output width), hidden, n_params per scene */
+int pdf_net_dims(const pdf_ctx* ctx, int32_t* rows, int32_t* d0, int32_t* hidden, int64_t* n_params);
+
+/* physics: alpha_hat [S][n][m0] -> g_alpha [S][n][m0] (NULL = skip), breakdown [S][6] f64
+ * in LossBreakdown.as_row order (state, data, bound, tv, bridge, total) */
+int pdf_loss_grad(pdf_ctx* ctx, const void* alpha_hat, void* g_alpha, double* breakdown, void* stream);
+/* loss only; chi_out [S][m1][m2] (NULL = skip) is recover_contrast at alpha_hat */
+int pdf_loss_value(pdf_ctx* ctx, const void* alpha_hat, double* breakdown, void* chi_out, void* stream);
+
+/* network (parameters theta [S][n_params] in the reference flat order) */
+int pdf_net_setup(pdf_ctx* ctx, const void* alpha0, void* stream);
+int pdf_net_forward(pdf_ctx* ctx, const void* theta, void* alpha_hat, void* stream);
+int pdf_grad_loss(pdf_ctx* ctx, const void* theta, void* grad, double* breakdown, void* stream);
+int pdf_adam_step(pdf_ctx* ctx, void* theta, void* m, void* v, const void* grad, int64_t count, int32_t t,
+                  void* stream);
+/* replace the per-scene normalisers after the caller rewrote data / e_inc in place (new batch) */
+int pdf_set_norms(pdf_ctx* ctx, const double* c_inc_host, const double* c_sca_host, void* stream);
+/* k fused iterations {grad_loss -> trace row -> Adam} starting from Adam step t0;
+ * trace [k][S][6] f64.  use_graph != 0 replays a captured CUDA graph. */
+int pdf_train(pdf_ctx* ctx, void* theta, void* m, void* v, int32_t t0, int32_t k_iters, double* trace,
+              int32_t use_graph, void* stream);
+
+/* operator primitives over `count` images / row vectors */
+int pdf_apply_gd(pdf_ctx* ctx, const void* x, void* y, int32_t count, int32_t adjoint, void* stream);
+int pdf_gs_forward(pdf_ctx* ctx, const void* img, void* rows, int32_t count, void* stream);
+int pdf_gs_adjoint(pdf_ctx* ctx, const void* rows, void* img, int32_t count, void* stream);
+int pdf_expand(pdf_ctx* ctx, const void* alpha, void* img, int32_t count, void* stream);
+int pdf_truncate(pdf_ctx* ctx, const void* img, void* alpha, int32_t count, void* stream);
+int pdf_apply_cco(pdf_ctx* ctx, const void* chi, void* out, int32_t count, double tau, double eta_max,
+                  double delta, int32_t radius, double eps_gf, void* stream);
+
+/* measurement hooks: `iters` un-graphed fused iterations with an event between each of the
+ * PDF_NPHASES kernels (fwd_l1 fwd_l2 fwd_l3 view_fwd pixel view_bwd finalize bwd_l3 bwd_l2 bwd_l1);
+ * ms[PDF_NPHASES] = mean milliseconds per launch.  pdf_fp64_probe: DFMA-bound kernel, GFLOP/s. */
+#define PDF_NPHASES 10
+int pdf_profile_train(pdf_ctx* ctx, void* theta, void* m, void* v, int32_t t0, int32_t iters, float* ms,
+                      void* stream);
+int pdf_fp64_probe(double* gflops, void* stream);
+
+/* copies the per-scene sticky error words to host (synchronises stream), then clears them */
+int pdf_get_error(pdf_ctx* ctx, int32_t* err_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDF_ABI_H */

@@ -1,0 +1,33 @@
+"""B200-native (sm_100a) PDF inverse-scattering hot path.
+
+Drop-in for the reference package's solver API on the per-iteration path
+(physics loss forward + hand adjoint, corrective network, Adam), see DESIGN.md.
+The setup modules (config, geometry, scenes, operators) import without a GPU;
+the solver entry points load ``libpdfb200.so`` on first use and fail loudly
+if it is missing.
+"""
+from .config import C0, CcoParams, ConfigError, ImagingConfig, config_from_dict, config_to_dict
+from .geometry import AntennaArray, ComplexGrid, GridGeometry, build_array, build_grid, perturb_array
+from .operators import (FieldSet, GeometryError, GreensOperators, NoConvergenceError, ScatteredData,
+                        SimulationResult, add_awgn, build_greens, incident_fields, plane_wave_fields,
+                        simulate, solve_total_field, synthesize_scattered)
+from .scenes import Scene, SceneError, Shape, builtin_scene, ellipse, rasterize
+
+__version__ = "0.1.0"
+
+_API = ("LossBreakdown", "LossContext", "PipelineState", "SpectralBasis", "NetworkParams", "AdamState",
+        "ReconstructionResult", "BatchReconstructor", "pipeline_forward", "pipeline_backward", "grad_alpha",
+        "loss_total", "init_network", "forward_net", "flatten_params", "unflatten_params", "grad_loss",
+        "adam_step", "bp_initialize", "init_alpha", "recover_contrast", "apply_cco", "reconstruct",
+        "relative_error", "count_components", "PoleError", "ZeroDataError")
+
+
+def __getattr__(name):
+    # the GPU API imports torch lazily so the setup modules stay light
+    if name in _API:
+        from . import api
+        return getattr(api, name)
+    if name == "DeviceProblem":
+        from .engine import DeviceProblem
+        return DeviceProblem
+    raise AttributeError(name)

@@ -1,0 +1,542 @@
+"""Reference-shaped solver API, GPU underneath.
+
+Same names, argument meaning and error behaviour as the reference's hot-path
+functions (citations relative to /root/reference/pkg/src/pdfisp/):
+
+  LossContext, LossBreakdown          losses.py:36-80
+  pipeline_forward / pipeline_backward losses.py:215-306
+  grad_alpha, loss_total              losses.py:250-252, 309-312
+  NetworkParams, init_network         network.py:53-71
+  forward_net, flatten/unflatten      network.py:143-176
+  grad_loss                           network.py:183-223
+  AdamState, adam_step                network.py:230-264
+  bp_initialize, init_alpha           reconstruct.py:52-153
+  recover_contrast                    cie.py:83-99
+  apply_cco                           filters.py:56-67
+  reconstruct, ReconstructionResult   reconstruct.py:32-236
+
+Host arrays in, host arrays out (numpy complex128 / float64), like the
+reference.  Every numerical step runs in libpdfb200.so on the GPU.
+"""
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+from scipy import ndimage
+
+from .config import CcoParams, ImagingConfig
+from .engine import DeviceProblem
+from .errors import PoleError, ZeroDataError  # noqa: F401  (re-exported)
+from .geometry import AntennaArray, ComplexGrid, build_array, build_grid
+from .operators import GreensOperators, ScatteredData, build_greens, incident_fields
+
+EPS_TV = 1e-12
+SCALE_MIX, SCALE_FLOOR, OUTPUT_GAIN = 0.7, 0.1, 8.0
+
+
+# ---------------------------------------------------------------------------- basis
+@dataclass(frozen=True)
+class SpectralBasis:
+    """Corner-block index sets, TL/TR/BL/BR row-major (spectral.py:21-53)."""
+    m1: int
+    m2: int
+    m_f: int
+    rows: np.ndarray = field(init=False)
+    cols: np.ndarray = field(init=False)
+
+    def __post_init__(self):
+        f = self.m_f
+        if f < 1 or 2 * f > min(self.m1, self.m2):
+            raise ValueError("corner blocks must not overlap: need 2*m_f <= min(m1, m2)")
+        rsets = (np.arange(f), np.arange(self.m1 - f, self.m1))
+        csets = (np.arange(f), np.arange(self.m2 - f, self.m2))
+        r = np.concatenate([np.repeat(a, f) for a in rsets for _ in csets])
+        c = np.concatenate([np.tile(b, f) for _ in rsets for b in csets])
+        object.__setattr__(self, "rows", r)
+        object.__setattr__(self, "cols", c)
+
+    @property
+    def m0(self) -> int:
+        return 4 * self.m_f * self.m_f
+
+    @property
+    def n_cells(self) -> int:
+        return self.m1 * self.m2
+
+
+# ---------------------------------------------------------------------------- losses
+@dataclass(frozen=True)
+class LossBreakdown:
+    total: float
+    state: float
+    data: float
+    bound: float
+    tv: float
+    bridge: float
+    weights: tuple
+
+    def as_row(self) -> tuple:
+        return (self.state, self.data, self.bound, self.tv, self.bridge, self.total)
+
+    @classmethod
+    def from_row(cls, row, weights) -> "LossBreakdown":
+        st, da, bo, tv, br, tot = (float(x) for x in row)
+        return cls(total=tot, state=st, data=da, bound=bo, tv=tv, bridge=br, weights=tuple(weights))
+
+
+@dataclass
+class LossContext:
+    """Everything a loss evaluation needs besides the coefficients (losses.py:52-80).
+
+    The first GPU call uploads operators and data into a cached DeviceProblem."""
+    data: ScatteredData
+    e_inc: np.ndarray
+    ops: GreensOperators
+    basis: SpectralBasis
+    beta: float
+    lambdas: tuple
+    tau_b: float
+    r_fixed: np.ndarray | None = None
+    c_sca: float = 0.0
+    c_inc: float = 0.0
+
+    def __post_init__(self):
+        mat = self.data.matrix if self.data.mask is None else self.data.matrix * self.data.mask
+        self.c_sca = float(np.vdot(mat, mat).real)
+        self.c_inc = float(np.vdot(self.e_inc, self.e_inc).real)
+        if self.c_sca <= 0:
+            raise ZeroDataError("measured scattered power is zero")
+        if self.c_inc <= 0:
+            raise ZeroDataError("incident power is zero")
+        self._dev = {}
+
+    @property
+    def n_views(self) -> int:
+        return self.e_inc.shape[0]
+
+    def device(self, joint: bool = False) -> DeviceProblem:
+        key = bool(joint)
+        if key not in self._dev:
+            self._dev[key] = DeviceProblem(
+                self.ops, self.e_inc, self.data.matrix, mf=self.basis.m_f, beta=self.beta,
+                lambdas=self.lambdas, tau_b=self.tau_b, mask=self.data.mask, r_fixed=self.r_fixed,
+                joint=joint)
+        return self._dev[key]
+
+
+@dataclass
+class PipelineState:
+    """Intermediates of one composite-loss evaluation (losses.py:202-212).
+
+    The GPU keeps J, E, chi ... in device workspace; the host record carries
+    the coefficients, the breakdown and the recovered contrast."""
+    alpha_hat: np.ndarray
+    chi: np.ndarray
+    breakdown: LossBreakdown
+
+
+def _cdev(x, dev: DeviceProblem):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dev.cdt, device=dev.device)
+
+
+def pipeline_forward(alpha_hat: np.ndarray, ctx: LossContext) -> PipelineState:
+    alpha_hat = np.atleast_2d(np.asarray(alpha_hat, dtype=np.complex128))
+    dev = ctx.device()
+    bd, chi = dev.loss_value(_cdev(alpha_hat[None], dev), want_chi=True)
+    dev.check_errors()
+    return PipelineState(alpha_hat=alpha_hat, chi=chi[0].cpu().numpy(),
+                         breakdown=LossBreakdown.from_row(bd[0].cpu().numpy(), ctx.lambdas))
+
+
+def pipeline_backward(state: PipelineState, ctx: LossContext) -> np.ndarray:
+    """g_alpha at state.alpha_hat (the fused kernels recompute the forward)."""
+    g, _ = grad_alpha(state.alpha_hat, ctx)
+    return g
+
+
+def grad_alpha(alpha: np.ndarray, ctx: LossContext) -> tuple[np.ndarray, LossBreakdown]:
+    alpha = np.atleast_2d(np.asarray(alpha, dtype=np.complex128))
+    if alpha.shape != (ctx.n_views, ctx.basis.m0):
+        raise ValueError("need one coefficient vector per incidence view")
+    dev = ctx.device()
+    g, bd = dev.loss_grad(_cdev(alpha[None], dev))
+    dev.check_errors()
+    return g[0].cpu().numpy(), LossBreakdown.from_row(bd[0].cpu().numpy(), ctx.lambdas)
+
+
+def loss_total(alpha: np.ndarray, ctx: LossContext) -> LossBreakdown:
+    return pipeline_forward(alpha, ctx).breakdown
+
+
+# ---------------------------------------------------------------------------- network
+@dataclass
+class NetworkParams:
+    weights: list
+    biases: list
+
+    @property
+    def in_dim(self) -> int:
+        return self.weights[0].shape[1]
+
+    def n_params(self) -> int:
+        return sum(w.size for w in self.weights) + sum(b.size for b in self.biases)
+
+
+def init_network(m0: int, rng: np.random.Generator) -> NetworkParams:
+    """Same draws as the reference (network.py:53-71): N(0, 1/fan_in), zero output layer."""
+    if m0 < 1:
+        raise ValueError("m0 must be >= 1")
+    dims = (2 * m0, 4 * m0, 4 * m0, 2 * m0)
+    ws, bs = [], []
+    for li, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+        ws.append(np.zeros((fo, fi)) if li == 2 else rng.normal(0.0, np.sqrt(1.0 / fi), (fo, fi)))
+        bs.append(np.zeros(fo))
+    return NetworkParams(weights=ws, biases=bs)
+
+
+def flatten_params(params: NetworkParams) -> np.ndarray:
+    return np.concatenate([a.ravel() for w, b in zip(params.weights, params.biases) for a in (w, b)])
+
+
+def unflatten_params(flat: np.ndarray, like: NetworkParams) -> NetworkParams:
+    ws, bs, k = [], [], 0
+    for w, b in zip(like.weights, like.biases):
+        ws.append(flat[k:k + w.size].reshape(w.shape).copy())
+        k += w.size
+        bs.append(flat[k:k + b.size].copy())
+        k += b.size
+    if k != flat.size:
+        raise ValueError("flat parameter vector has the wrong length")
+    return NetworkParams(weights=ws, biases=bs)
+
+
+_NET_DEVS: dict = {}
+
+
+def _net_device(n: int, m_f: int, joint: bool) -> DeviceProblem:
+    """A geometry-free context just large enough to run the network kernels."""
+    key = (n, m_f, joint)
+    if key not in _NET_DEVS:
+        M = 16
+        while M < 2 * m_f:
+            M *= 2
+        cfg = ImagingConfig(m1=M, m2=M, m_f=m_f, n_tx=n, n_rx=1).validate()
+        grid, arr = build_grid(cfg), build_array(cfg)
+        ops = build_greens(cfg, arr, grid)
+        _NET_DEVS[key] = DeviceProblem(ops, np.ones((n, M, M), complex), np.ones((n, 1), complex), mf=m_f,
+                                       beta=cfg.beta, lambdas=(0, 0, 0), tau_b=0.5, joint=joint)
+    return _NET_DEVS[key]
+
+
+def _theta(params: NetworkParams, dev: DeviceProblem) -> torch.Tensor:
+    return torch.as_tensor(flatten_params(params), dtype=dev.rdt, device=dev.device)[None].contiguous()
+
+
+def forward_net(params: NetworkParams, alpha0: np.ndarray, joint: bool = False) -> np.ndarray:
+    """Corrective update delta-alpha (network.py:143-150), on the GPU."""
+    alpha0 = np.atleast_2d(np.asarray(alpha0, dtype=np.complex128))
+    n, m0 = alpha0.shape
+    width = 2 * (alpha0.size if joint else m0)
+    if params.in_dim != width:
+        raise ValueError(f"network expects input width {params.in_dim}, got {width}")
+    mf = int(round(np.sqrt(m0 / 4)))
+    if 4 * mf * mf != m0:
+        raise ValueError("coefficient length must be 4*m_f**2")
+    dev = _net_device(n, mf, joint)
+    a0 = _cdev(alpha0[None], dev)
+    dev.net_setup(a0)
+    out = dev.net_forward(_theta(params, dev))
+    return (out - a0)[0].cpu().numpy()
+
+
+def grad_loss(params: NetworkParams, alpha0: np.ndarray, ctx: LossContext,
+              joint: bool = False) -> tuple[np.ndarray, LossBreakdown]:
+    """Exact gradient over the flat parameters (network.py:183-223)."""
+    alpha0 = np.atleast_2d(np.asarray(alpha0, dtype=np.complex128))
+    width = 2 * (alpha0.size if joint else alpha0.shape[1])
+    if params.in_dim != width:
+        raise ValueError(f"network expects input width {params.in_dim}, got {width}")
+    dev = ctx.device(joint)
+    dev.net_setup(_cdev(alpha0[None], dev))
+    g, bd = dev.grad_loss(_theta(params, dev))
+    dev.check_errors()
+    return g[0].cpu().numpy().astype(np.float64), LossBreakdown.from_row(bd[0].cpu().numpy(), ctx.lambdas)
+
+
+@dataclass
+class AdamState:
+    m: np.ndarray
+    v: np.ndarray
+    step: int = 0
+    lr: float = 1e-2
+    b1: float = 0.9
+    b2: float = 0.999
+    eps: float = 1e-8
+
+    @classmethod
+    def for_params(cls, params: NetworkParams, lr: float = 1e-2) -> "AdamState":
+        n = params.n_params()
+        return cls(m=np.zeros(n), v=np.zeros(n), lr=lr)
+
+
+def adam_step(state: AdamState, params: NetworkParams, grad: np.ndarray) -> tuple[NetworkParams, AdamState]:
+    """One bias-corrected Adam update on the GPU (network.py:248-264)."""
+    flat = flatten_params(params)
+    if grad.shape != flat.shape:
+        raise ValueError("gradient length does not match parameter count")
+    if (state.b1, state.b2, state.eps) != (0.9, 0.999, 1e-8):
+        raise ValueError("only the reference's Adam constants are supported on the device")
+    dev = _adam_device(state.lr)
+    t = state.step + 1
+    to = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev.device).clone()  # noqa
+    p, m, v, g = to(flat), to(state.m), to(state.v), to(grad)
+    dev.adam_step(p, m, v, g, t)
+    dev.check_errors()
+    new = AdamState(m=m.cpu().numpy(), v=v.cpu().numpy(), step=t, lr=state.lr, b1=state.b1, b2=state.b2,
+                    eps=state.eps)
+    return unflatten_params(p.cpu().numpy(), params), new
+
+
+_ADAM_DEVS: dict = {}
+
+
+def _adam_device(lr: float) -> DeviceProblem:
+    if lr not in _ADAM_DEVS:
+        cfg = ImagingConfig(m1=16, m2=16, m_f=1, n_tx=1, n_rx=1, learn_rate=lr).validate()
+        ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
+        _ADAM_DEVS[lr] = DeviceProblem(ops, np.ones((1, 16, 16), complex), np.ones((1, 1), complex), mf=1,
+                                       beta=6.0, lambdas=(0, 0, 0), tau_b=0.5, lr=lr)
+    return _ADAM_DEVS[lr]
+
+
+# ---------------------------------------------------------------------------- pipeline
+@dataclass
+class ReconstructionResult:
+    chi_hat: ComplexGrid
+    chi_cco: ComplexGrid
+    chi0: ComplexGrid
+    trace: list
+    final_loss: LossBreakdown
+    wall_time: float
+    rel_error: float | None = None
+
+    @property
+    def eps_r(self) -> np.ndarray:
+        return self.chi_cco.values + 1.0
+
+
+def relative_error(eps_hat: np.ndarray, eps_true: np.ndarray) -> float:
+    return float(np.linalg.norm(np.real(eps_hat) - np.real(eps_true)) / np.linalg.norm(np.real(eps_true)))
+
+
+FOUR_CONN = np.array([[0, 1, 0], [1, 1, 1], [0, 1, 0]], dtype=bool)
+
+
+def count_components(eps_map: np.ndarray, threshold: float) -> int:
+    _, n = ndimage.label(np.real(eps_map) > threshold, structure=FOUR_CONN)
+    return int(n)
+
+
+def _theta0(seeds, m0_eff: int, workers: int = 8) -> np.ndarray:
+    """Reference-identical initial weights per scene (numpy PCG64 draws on the host)."""
+    def one(s):
+        return flatten_params(init_network(m0_eff, np.random.default_rng(int(s))))
+    if len(seeds) == 1:
+        return one(seeds[0])[None]
+    with ThreadPoolExecutor(max_workers=min(workers, len(seeds))) as ex:
+        return np.stack(list(ex.map(one, seeds)))
+
+
+class BatchReconstructor:
+    """Reconstruct S scenes that share one geometry, all resident on one GPU.
+
+    This is the B200 form of the reference's reconstruct() (reconstruct.py:186-236):
+    bp_initialize + init_alpha, then k fused {grad_loss, trace, Adam} iterations
+    replayed from a CUDA graph, then forward_net + loss_total + recover_contrast
+    + apply_cco.  Scenes are independent (config 4 shards them over GPUs).
+    """
+
+    def __init__(self, config: ImagingConfig, S: int, e_inc: np.ndarray | None = None,
+                 array: AntennaArray | None = None, mask=None, dtype: str = "f64", use_graph: bool = True,
+                 theta_cache: bool = True):
+        config.validate()
+        self.config = config
+        self.array = build_array(config) if array is None else array
+        self.grid = build_grid(config)
+        self.ops = build_greens(config, self.array, self.grid)
+        self.e_inc = incident_fields(config, self.array, self.grid).views if e_inc is None else np.asarray(e_inc)
+        self.basis = SpectralBasis(config.m1, config.m2, config.m_f)
+        self.S = S
+        self.use_graph = use_graph
+        # initial weights are a pure function of (seed, width) -- the reference
+        # redraws the same numbers from default_rng(config.rng_seed) on every
+        # call -- so they are memoised per seed tuple like the operators
+        self.theta_cache = theta_cache
+        self._theta0 = {}
+        self.mask = mask
+        self.lambdas = (config.lambda1, config.lambda2, config.lambda3)
+        placeholder = np.ones((S, self.e_inc.shape[0], self.array.n_rx), complex)
+        self.dev = DeviceProblem(self.ops, self.e_inc, placeholder, mf=config.m_f, beta=config.beta,
+                                 lambdas=self.lambdas, tau_b=config.tau_b, mask=mask, joint=config.joint_views,
+                                 lr=config.learn_rate, dtype=dtype)
+        self.m0_eff = self.basis.m0 * (self.e_inc.shape[0] if config.joint_views else 1)
+
+    def run(self, datas, seeds=None, chi_trues=None, k_iters: int | None = None) -> list:
+        cfg = self.config
+        t0 = time.perf_counter()
+        mats = np.stack([np.asarray(d.matrix if isinstance(d, ScatteredData) else d) for d in datas])
+        if mats.shape != (self.S, self.e_inc.shape[0], self.array.n_rx):
+            raise ValueError("data matrix does not match the antenna array")
+        seeds = [cfg.rng_seed] * self.S if seeds is None else list(seeds)
+        k = cfg.k_iters if k_iters is None else k_iters
+        dev = self.dev
+        dev.set_data(mats)
+        chi0, r0 = dev.bp_initialize()
+        if cfg.freeze_r:
+            raise NotImplementedError("freeze_r with BatchReconstructor: build DeviceProblem(r_fixed=...)")
+        alpha0 = dev.init_alpha(r0)
+        dev.net_setup(alpha0)
+        key = tuple(int(x) for x in seeds)
+        theta0 = self._theta0.get(key)
+        if theta0 is None:
+            theta0 = torch.as_tensor(_theta0(seeds, self.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
+            if self.theta_cache:
+                self._theta0 = {key: theta0}
+        theta = theta0.clone()
+        m = torch.zeros_like(theta)
+        v = torch.zeros_like(theta)
+        trace = torch.zeros(max(k, 1), self.S, 6, dtype=torch.float64, device=dev.device)
+        if k:
+            dev.train(theta, m, v, 0, k, trace, use_graph=self.use_graph)
+        ahat = dev.net_forward(theta)
+        bd, chi = dev.loss_value(ahat, want_chi=True)
+        chi_cco = dev.apply_cco(chi, cfg.cco) if cfg.use_cco else chi.clone()
+        dev.check_errors()
+        chi0_h, chi_h, cco_h = chi0.cpu().numpy(), chi.cpu().numpy(), chi_cco.cpu().numpy()
+        tr_h, bd_h = trace.cpu().numpy(), bd.cpu().numpy()
+        wall = time.perf_counter() - t0
+        out = []
+        cs = self.grid.cell_size
+        for s in range(self.S):
+            rel = None
+            if chi_trues is not None and chi_trues[s] is not None:
+                ct_ = chi_trues[s].values if isinstance(chi_trues[s], ComplexGrid) else chi_trues[s]
+                rel = relative_error(cco_h[s].real + 1.0, np.real(ct_) + 1.0)
+            out.append(ReconstructionResult(
+                chi_hat=ComplexGrid(chi_h[s], cs), chi_cco=ComplexGrid(cco_h[s], cs),
+                chi0=ComplexGrid(chi0_h[s], cs),
+                trace=[LossBreakdown.from_row(tr_h[i, s], self.lambdas) for i in range(k)],
+                final_loss=LossBreakdown.from_row(bd_h[s], self.lambdas), wall_time=wall, rel_error=rel))
+        return out
+
+
+def reconstruct(config: ImagingConfig, data: ScatteredData, array: AntennaArray | None = None,
+                chi_true: ComplexGrid | None = None, *, e_inc: np.ndarray | None = None,
+                dtype: str = "f64") -> ReconstructionResult:
+    """Full pipeline from measured data to a permittivity map (reconstruct.py:186-236).
+
+    ``e_inc`` overrides the reference's line-source illumination (e.g. plane
+    waves for the BASELINE configs); everything else follows the reference."""
+    config.validate()
+    t0 = time.perf_counter()
+    if config.freeze_r:
+        return _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0)
+    rec = BatchReconstructor(config, 1, e_inc=e_inc, array=array, mask=data.mask, dtype=dtype)
+    res = rec.run([data], chi_trues=[chi_true])[0]
+    res.wall_time = time.perf_counter() - t0
+    return res
+
+
+def _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0):
+    array = build_array(config) if array is None else array
+    grid = build_grid(config)
+    ops = build_greens(config, array, grid)
+    e_inc = incident_fields(config, array, grid).views if e_inc is None else np.asarray(e_inc)
+    lambdas = (config.lambda1, config.lambda2, config.lambda3)
+    probe = DeviceProblem(ops, e_inc, data.matrix, mf=config.m_f, beta=config.beta, lambdas=lambdas,
+                          tau_b=config.tau_b, mask=data.mask, lr=config.learn_rate, dtype=dtype)
+    chi0, r0 = probe.bp_initialize()
+    alpha0 = probe.init_alpha(r0)
+    dev = DeviceProblem(ops, e_inc, data.matrix, mf=config.m_f, beta=config.beta, lambdas=lambdas,
+                        tau_b=config.tau_b, mask=data.mask, r_fixed=r0[0].cpu().numpy(),
+                        joint=config.joint_views, lr=config.learn_rate, dtype=dtype)
+    dev.net_setup(alpha0)
+    m0_eff = 4 * config.m_f ** 2 * (e_inc.shape[0] if config.joint_views else 1)
+    theta = torch.as_tensor(_theta0([config.rng_seed], m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
+    m, v = torch.zeros_like(theta), torch.zeros_like(theta)
+    k = config.k_iters
+    trace = torch.zeros(max(k, 1), 1, 6, dtype=torch.float64, device=dev.device)
+    if k:
+        dev.train(theta, m, v, 0, k, trace)
+    ahat = dev.net_forward(theta)
+    bd, _ = dev.loss_value(ahat)
+    # recover_contrast is evaluated with the (non-frozen) LS map, as the reference does
+    _, chi = probe.loss_value(ahat, want_chi=True)
+    chi_cco = probe.apply_cco(chi, config.cco) if config.use_cco else chi.clone()
+    dev.check_errors()
+    lam = lambdas
+    cs = grid.cell_size
+    rel = None
+    cco_h = chi_cco[0].cpu().numpy()
+    if chi_true is not None:
+        rel = relative_error(cco_h.real + 1.0, chi_true.values.real + 1.0)
+    tr = trace.cpu().numpy()
+    return ReconstructionResult(chi_hat=ComplexGrid(chi[0].cpu().numpy(), cs), chi_cco=ComplexGrid(cco_h, cs),
+                                chi0=ComplexGrid(chi0[0].cpu().numpy(), cs),
+                                trace=[LossBreakdown.from_row(tr[i, 0], lam) for i in range(k)],
+                                final_loss=LossBreakdown.from_row(bd[0].cpu().numpy(), lam),
+                                wall_time=time.perf_counter() - t0, rel_error=rel)
+
+
+def bp_initialize(data: ScatteredData, e_inc, ops: GreensOperators, beta: float):
+    """Backprojection (reconstruct.py:52-71) on the GPU; returns host (chi0, r0)."""
+    views = e_inc.views if hasattr(e_inc, "views") else np.asarray(e_inc)
+    m_f = 1
+    dev = DeviceProblem(ops, views, data.matrix, mf=m_f, beta=beta, lambdas=(0, 0, 0), tau_b=0.5,
+                        mask=data.mask)
+    chi0, r0 = dev.bp_initialize()
+    return chi0[0].cpu().numpy(), r0[0].cpu().numpy()
+
+
+def init_alpha(r0, data: ScatteredData, e_inc, ops: GreensOperators, basis: SpectralBasis, beta: float):
+    views = e_inc.views if hasattr(e_inc, "views") else np.asarray(e_inc)
+    dev = DeviceProblem(ops, views, data.matrix, mf=basis.m_f, beta=beta, lambdas=(0, 0, 0), tau_b=0.5,
+                        mask=data.mask)
+    a0 = dev.init_alpha(torch.as_tensor(np.asarray(r0)[None], dtype=dev.cdt, device=dev.device))
+    return a0[0].cpu().numpy()
+
+
+def recover_contrast(alpha, e_inc, ops: GreensOperators, basis: SpectralBasis):
+    alpha = np.atleast_2d(np.asarray(alpha, dtype=np.complex128))
+    if alpha.shape[0] != e_inc.shape[0]:
+        raise ValueError("need one coefficient vector per incidence view")
+    dev = DeviceProblem(ops, e_inc, np.ones((e_inc.shape[0], ops.n_rx), complex), mf=basis.m_f, beta=6.0,
+                        lambdas=(0, 0, 0), tau_b=0.5)
+    _, chi = dev.loss_value(_cdev(alpha[None], dev), want_chi=True)
+    return chi[0].cpu().numpy()
+
+
+def apply_cco(chi: np.ndarray, params: CcoParams) -> np.ndarray:
+    chi = np.asarray(chi, dtype=np.complex128)
+    M = chi.shape[0]
+    if chi.shape != (M, M) or M not in (16, 32, 64, 128):
+        raise ValueError("apply_cco on the GPU needs a square power-of-two image (16..128)")
+    dev = _cco_device(M)
+    out = dev.apply_cco(_cdev(chi[None], dev), params)
+    return out[0].cpu().numpy()
+
+
+_CCO_DEVS: dict = {}
+
+
+def _cco_device(M: int) -> DeviceProblem:
+    if M not in _CCO_DEVS:
+        cfg = ImagingConfig(m1=M, m2=M, m_f=1, n_tx=1, n_rx=1).validate()
+        ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
+        _CCO_DEVS[M] = DeviceProblem(ops, np.ones((1, M, M), complex), np.ones((1, 1), complex), mf=1, beta=6.0,
+                                     lambdas=(0, 0, 0), tau_b=0.5)
+    return _CCO_DEVS[M]

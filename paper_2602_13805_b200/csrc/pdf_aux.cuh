@@ -1,0 +1,177 @@
+// Operator primitives and one-time kernels around the hot loop:
+// expand / truncate (spectral.py:56-79), G_S products (forward.py:303-306,
+// losses.py:229), the contrast-compensation epilogue (filters.py:16-67) and
+// the kernel-spectrum permutation used by the view FFT.
+#pragma once
+#include "pdf_common.cuh"
+
+namespace pdf {
+
+__device__ inline int bitrev5(int l) { return __brev((unsigned)l) >> 27; }
+
+// khat_p[pos_c * P + pos_r] = khat[f(pos_r)][f(pos_c)] / P^2, f(q*32+l) = q + E*bitrev5(l)
+template <typename T>
+__global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P) {
+  const int E = P / 32;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P * P) return;
+  const int posc = idx / P, posr = idx % P;
+  const int fr = (posr / 32) + E * bitrev5(posr % 32);
+  const int fc = (posc / 32) + E * bitrev5(posc % 32);
+  const T s = T(1) / (T(P) * T(P));
+  out[idx] = cscale<T>(khat[(size_t)fr * P + fc], s);
+}
+
+__global__ void set_ints_kernel(int* p, int a, int b) { p[0] = a; p[1] = b; }
+
+// J = expand(alpha): one thread per pixel, direct corner-sparse inverse DFT
+template <typename T>
+__global__ void expand_kernel(const C<T>* alpha, C<T>* img, const C<T>* twM, int M, int mf) {
+  const int K = 2 * mf, M0 = K * K;
+  const int v = blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M * M) return;
+  const int y = p / M, x = p % M;
+  const C<T>* al = alpha + (size_t)v * M0;
+  C<T> acc = czero<T>();
+  for (int u = 0; u < K; ++u) {
+    const int fr = u < mf ? u : M - K + u;
+    C<T> row = czero<T>();
+    for (int w = 0; w < K; ++w) {
+      const int fc = w < mf ? w : M - K + w;
+      const int slot = (((u / mf) * 2 + (w / mf)) * mf + (u % mf)) * mf + (w % mf);
+      row = cadd<T>(row, cmulc<T>(al[slot], twM[(fc * x) & (M - 1)]));
+    }
+    acc = cadd<T>(acc, cmulc<T>(row, twM[(fr * y) & (M - 1)]));
+  }
+  img[(size_t)v * M * M + p] = cscale<T>(acc, T(1) / (T(M) * T(M)));
+}
+
+// alpha = truncate(img): one block per (coefficient chunk, image); fixed-order sums
+template <typename T>
+__global__ void truncate_kernel(const C<T>* img, C<T>* alpha, const C<T>* twM, int M, int mf) {
+  const int K = 2 * mf, M0 = K * K;
+  const int v = blockIdx.y;
+  const int c = blockIdx.x;     // coefficient slot
+  if (c >= M0) return;
+  const int blk = c / (mf * mf), rem = c % (mf * mf);
+  const int u = (blk / 2) * mf + rem / mf, w = (blk % 2) * mf + rem % mf;
+  const int fr = u < mf ? u : M - K + u, fc = w < mf ? w : M - K + w;
+  const C<T>* im = img + (size_t)v * M * M;
+  C<T> acc = czero<T>();
+  for (int p = threadIdx.x; p < M * M; p += blockDim.x) {
+    const int y = p / M, x = p % M;
+    acc = cadd<T>(acc, cmul<T>(im[p], twM[(fr * y + fc * x) & (M - 1)]));
+  }
+  __shared__ C<T> red[32];
+  acc.x = warp_sum<T>(acc.x);
+  acc.y = warp_sum<T>(acc.y);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    C<T> s = czero<T>();
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = cadd<T>(s, red[i]);
+    alpha[(size_t)v * M0 + c] = s;
+  }
+}
+
+// rows[v][r] = sum_p img[v][p] gs[r][p]
+template <typename T>
+__global__ void gs_forward_kernel(const C<T>* img, C<T>* rows, const C<T>* gs, int npix, int R) {
+  const int r = blockIdx.x, v = blockIdx.y;
+  const C<T>* im = img + (size_t)v * npix;
+  const C<T>* g = gs + (size_t)r * npix;
+  C<T> acc = czero<T>();
+  for (int p = threadIdx.x; p < npix; p += blockDim.x) acc = cadd<T>(acc, cmul<T>(im[p], g[p]));
+  __shared__ C<T> red[32];
+  acc.x = warp_sum<T>(acc.x);
+  acc.y = warp_sum<T>(acc.y);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    C<T> s = czero<T>();
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = cadd<T>(s, red[i]);
+    rows[(size_t)v * R + r] = s;
+  }
+}
+
+// img[v][p] = sum_r rows[v][r] conj(gs[r][p])
+template <typename T>
+__global__ void gs_adjoint_kernel(const C<T>* rows, C<T>* img, const C<T>* gs, int npix, int R) {
+  const int v = blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  const C<T>* rw = rows + (size_t)v * R;
+  C<T> acc = czero<T>();
+  for (int r = 0; r < R; ++r) acc = cadd<T>(acc, cmulc<T>(rw[r], gs[(size_t)r * npix + p]));
+  img[(size_t)v * npix + p] = acc;
+}
+
+// ---- contrast compensation (filters.py:16-67) ----------------------------
+// box mean over (2r+1)^2 windows with edge replication
+template <typename T>
+__device__ inline T box_at(const T* img, int M, int y, int x, int r) {
+  T s = T(0);
+  for (int dy = -r; dy <= r; ++dy) {
+    const int yy = min(max(y + dy, 0), M - 1);
+    for (int dx = -r; dx <= r; ++dx) {
+      const int xx = min(max(x + dx, 0), M - 1);
+      s += img[yy * M + xx];
+    }
+  }
+  const int w = 2 * r + 1;
+  return s / T(w * w);
+}
+
+// pass 1: per channel (re, im) the self-guided filter coefficients a, b
+template <typename T>
+__global__ void cco_pass1_kernel(const C<T>* chi, T* ab, int M, int r, T eps_gf) {
+  const int v = blockIdx.y, ch = blockIdx.z;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M * M) return;
+  const int y = p / M, x = p % M;
+  const T* base = reinterpret_cast<const T*>(chi + (size_t)v * M * M) + ch;
+  // strided channel view: element q at base[2q]
+  T mi = 0, mii = 0;
+  const int w = 2 * r + 1;
+  for (int dy = -r; dy <= r; ++dy) {
+    const int yy = min(max(y + dy, 0), M - 1);
+    for (int dx = -r; dx <= r; ++dx) {
+      const int xx = min(max(x + dx, 0), M - 1);
+      const T g = base[2 * (yy * M + xx)];
+      mi += g;
+      mii += g * g;
+    }
+  }
+  mi /= T(w * w);
+  mii /= T(w * w);
+  // self-guided: p == I, so cov = var
+  const T var = mii - mi * mi;
+  const T a = var / (var + eps_gf);
+  const T b = mi - a * mi;
+  T* o = ab + (((size_t)v * 2 + ch) * 2) * M * M;
+  o[p] = a;
+  o[M * M + p] = b;
+}
+
+template <typename T>
+__global__ void cco_pass2_kernel(const C<T>* chi, const T* ab, C<T>* out, int M, int r, T tau, T eta_max,
+                                 T delta) {
+  const int v = blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= M * M) return;
+  const int y = p / M, x = p % M;
+  const C<T> c = chi[(size_t)v * M * M + p];
+  T sm[2];
+  for (int ch = 0; ch < 2; ++ch) {
+    const T* a = ab + (((size_t)v * 2 + ch) * 2) * M * M;
+    const T* b = a + M * M;
+    const T g = ch == 0 ? c.x : c.y;
+    sm[ch] = box_at<T>(a, M, y, x, r) * g + box_at<T>(b, M, y, x, r);
+  }
+  const T am = sqrt_<T>(cabs2<T>(c));
+  const T eta = eta_max * sigmoid_<T>((am - tau) / delta);
+  out[(size_t)v * M * M + p] = mk<T>((T(1) + eta) * sm[0] + eta * c.x, (T(1) + eta) * sm[1] + eta * c.y);
+}
+
+}  // namespace pdf

@@ -1,0 +1,227 @@
+// Common device helpers for the PDF solver hot path (sm_100a).
+//
+// Complex numbers are stored interleaved (re, im) as float2 / double2 so an
+// n x m1 x m2 field stack is one contiguous c64 / c128 array with the same
+// memory image as numpy's complex64 / complex128.
+#pragma once
+#include <cuda_runtime.h>
+#include <cooperative_groups.h>
+#include <stdint.h>
+
+namespace cg = cooperative_groups;
+
+namespace pdf {
+
+template <typename T> struct cx;
+template <> struct cx<float> { using t = float2; };
+template <> struct cx<double> { using t = double2; };
+template <typename T> using C = typename cx<T>::t;
+
+template <typename T> __host__ __device__ __forceinline__ C<T> mk(T a, T b) { C<T> r; r.x = a; r.y = b; return r; }
+template <typename T> __host__ inline C<T> mk_host(double a, double b) { C<T> r; r.x = (T)a; r.y = (T)b; return r; }
+template <typename T> __device__ __forceinline__ C<T> cadd(C<T> a, C<T> b) { return mk<T>(a.x + b.x, a.y + b.y); }
+template <typename T> __device__ __forceinline__ C<T> csub(C<T> a, C<T> b) { return mk<T>(a.x - b.x, a.y - b.y); }
+template <typename T> __device__ __forceinline__ C<T> cmul(C<T> a, C<T> b) {
+  return mk<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename T> __device__ __forceinline__ C<T> cmulc(C<T> a, C<T> b) {
+  return mk<T>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename T> __device__ __forceinline__ C<T> conj_(C<T> a) { return mk<T>(a.x, -a.y); }
+template <typename T> __device__ __forceinline__ C<T> cscale(C<T> a, T s) { return mk<T>(a.x * s, a.y * s); }
+template <typename T> __device__ __forceinline__ T cabs2(C<T> a) { return a.x * a.x + a.y * a.y; }
+template <typename T> __device__ __forceinline__ C<T> cdiv(C<T> a, C<T> b) {
+  // plain formula, as numpy's complex division (no Smith scaling needed at
+  // these magnitudes)
+  T d = b.x * b.x + b.y * b.y;
+  return mk<T>((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+template <typename T> __device__ __forceinline__ C<T> czero() { return mk<T>(T(0), T(0)); }
+
+template <typename T> __device__ __forceinline__ C<T> shfl_xor(C<T> v, int m) {
+  return mk<T>(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+
+template <typename T> __device__ __forceinline__ T sqrt_(T x);
+template <> __device__ __forceinline__ float sqrt_<float>(float x) { return sqrtf(x); }
+template <> __device__ __forceinline__ double sqrt_<double>(double x) { return sqrt(x); }
+template <typename T> __device__ __forceinline__ T exp_(T x);
+template <> __device__ __forceinline__ float exp_<float>(float x) { return expf(x); }
+template <> __device__ __forceinline__ double exp_<double>(double x) { return exp(x); }
+
+// numerically stable logistic, scipy.special.expit semantics
+template <typename T> __device__ __forceinline__ T sigmoid_(T z) {
+  if (z >= T(0)) { T e = exp_<T>(-z); return T(1) / (T(1) + e); }
+  T e = exp_<T>(z);
+  return e / (T(1) + e);
+}
+
+// ---------------------------------------------------------------------------
+// Warp FFT of length P = 32*E, one transform per warp.
+//
+// Element n = l + 32*k lives in lane l, register k.  The forward transform is
+// decimation-in-frequency: an E-point DFT over the registers (stride 32),
+// a twiddle exp(-2 pi i l q / P), then a 32-point DFT across the lanes with
+// five shuffle butterflies.  Lane l, register q then holds the spectrum at
+// frequency q + E * bitrev5(l).  The inverse consumes exactly that order
+// (decimation in time) and returns natural order, so a convolution never
+// permutes data: the pointwise kernel is stored in the same permuted order.
+// Both directions are unnormalised.
+//
+// tw[k] = exp(-2 pi i k / P), k < P, lives in shared memory.
+// ---------------------------------------------------------------------------
+
+// exp(-2 pi i j / N) for compile-time N <= 16 (N a power of two)
+template <typename T, int N, int J>
+struct RootTab {
+  __device__ __forceinline__ static C<T> get() {
+    constexpr double c16[16] = {1.0, 0.92387953251128674, 0.70710678118654757, 0.38268343236508984,
+                                0.0, -0.38268343236508984, -0.70710678118654757, -0.92387953251128674,
+                                -1.0, -0.92387953251128674, -0.70710678118654757, -0.38268343236508984,
+                                0.0, 0.38268343236508984, 0.70710678118654757, 0.92387953251128674};
+    constexpr int idx = (J * (16 / N)) & 15;
+    constexpr int sidx = (idx + 12) & 15;  // sin(theta) = cos(theta - pi/2)
+    return mk<T>(T(c16[idx]), T(-c16[sidx]));
+  }
+};
+
+// multiply by exp(SIGN * 2 pi i J / N) with exact handling of the trivial roots
+template <typename T, int N, int J, int SIGN>
+__device__ __forceinline__ C<T> twiddle_ct(C<T> v) {
+  constexpr int j = ((J % N) + N) % N;
+  if constexpr (j == 0) {
+    return v;
+  } else if constexpr (4 * j == N) {       // exp(-i pi/2) = -i  (SIGN=-1)
+    return SIGN < 0 ? mk<T>(v.y, -v.x) : mk<T>(-v.y, v.x);
+  } else if constexpr (2 * j == N) {
+    return mk<T>(-v.x, -v.y);
+  } else if constexpr (4 * j == 3 * N) {
+    return SIGN < 0 ? mk<T>(-v.y, v.x) : mk<T>(v.y, -v.x);
+  } else {
+    C<T> w = RootTab<T, N, j>::get();     // exp(-2 pi i j/N)
+    if (SIGN > 0) w.y = -w.y;
+    return cmul<T>(v, w);
+  }
+}
+
+template <int B, int V> struct BitRev {
+  static constexpr int value = (B <= 1) ? 0 : (((V & 1) << (B - 1)) | BitRev<B - 1, (V >> 1)>::value);
+};
+template <int V> struct BitRev<0, V> { static constexpr int value = 0; };
+template <int V> struct BitRev<1, V> { static constexpr int value = V & 1; };
+
+template <int E> struct Log2 { static constexpr int value = 1 + Log2<E / 2>::value; };
+template <> struct Log2<1> { static constexpr int value = 0; };
+
+// in-register DIF butterflies for one stage (span = LEN/2) over all blocks
+template <typename T, int E, int LEN, int SIGN, int START, int J>
+struct RegStage {
+  __device__ __forceinline__ static void run(C<T> (&a)[E]) {
+    if constexpr (START < E) {
+      if constexpr (J < LEN / 2) {
+        C<T> u = a[START + J], v = a[START + J + LEN / 2];
+        a[START + J] = cadd<T>(u, v);
+        a[START + J + LEN / 2] = twiddle_ct<T, LEN, J, SIGN>(csub<T>(u, v));
+        RegStage<T, E, LEN, SIGN, START, J + 1>::run(a);
+      } else {
+        RegStage<T, E, LEN, SIGN, START + LEN, 0>::run(a);
+      }
+    }
+  }
+};
+
+template <typename T, int E, int LEN, int SIGN>
+struct RegDif {
+  __device__ __forceinline__ static void run(C<T> (&a)[E]) {
+    if constexpr (LEN >= 2) {
+      RegStage<T, E, LEN, SIGN, 0, 0>::run(a);
+      RegDif<T, E, LEN / 2, SIGN>::run(a);
+    }
+  }
+};
+
+template <typename T, int E, int I>
+struct RegPermute {
+  __device__ __forceinline__ static void run(const C<T> (&a)[E], C<T> (&o)[E]) {
+    if constexpr (I < E) {
+      o[BitRev<Log2<E>::value, I>::value] = a[I];
+      RegPermute<T, E, I + 1>::run(a, o);
+    }
+  }
+};
+
+// natural-order E-point DFT over registers: x[q] <- sum_k x[k] exp(SIGN 2 pi i k q / E)
+template <typename T, int E, int SIGN>
+__device__ __forceinline__ void reg_dft(C<T> (&x)[E]) {
+  if constexpr (E > 1) {
+    RegDif<T, E, E, SIGN>::run(x);
+    C<T> o[E];
+    RegPermute<T, E, 0>::run(x, o);
+#pragma unroll
+    for (int i = 0; i < E; ++i) x[i] = o[i];
+  }
+}
+
+template <typename T> __device__ __forceinline__ C<T> tw_get(const C<T>* tw, int k, bool inv) {
+  C<T> w = tw[k];
+  if (inv) w.y = -w.y;
+  return w;
+}
+
+template <typename T, int E>
+__device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
+  constexpr int P = 32 * E;
+  reg_dft<T, E, -1>(x);
+#pragma unroll
+  for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], tw[(lane * q) & (P - 1)]);
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) {
+    const bool upper = (lane & h) != 0;
+    const C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      C<T> o = shfl_xor<T>(x[q], h);
+      x[q] = upper ? cmul<T>(csub<T>(o, x[q]), w) : cadd<T>(x[q], o);
+    }
+  }
+}
+
+template <typename T, int E>
+__device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
+  constexpr int P = 32 * E;
+#pragma unroll
+  for (int h = 1; h <= 16; h <<= 1) {
+    const bool upper = (lane & h) != 0;
+    const C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      C<T> o = shfl_xor<T>(x[q], h);
+      x[q] = upper ? csub<T>(o, cmul<T>(x[q], w)) : cadd<T>(x[q], cmul<T>(o, w));
+    }
+  }
+#pragma unroll
+  for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], tw[(lane * q) & (P - 1)]);
+  reg_dft<T, E, +1>(x);
+}
+
+// deterministic fixed-order warp sum
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// error word bits (sticky, per scene) -- mirrored in include/pdf_abi.h
+enum : int {
+  ERR_POLE = 1,
+  ERR_NONFINITE_STATE = 2,
+  ERR_NONFINITE_DATA = 4,
+  ERR_NONFINITE_BOUND = 8,
+  ERR_NONFINITE_TV = 16,
+  ERR_NONFINITE_BRIDGE = 32,
+  ERR_NONFINITE_GRAD = 64,
+  ERR_NONFINITE_PARAM = 128,
+};
+
+}  // namespace pdf

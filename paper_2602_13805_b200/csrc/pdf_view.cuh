@@ -1,0 +1,340 @@
+// Per-incidence ("view") kernels: the zero-padded P x P FFT convolution that
+// applies the domain Green's operator G_D, fused with what sits either side
+// of it on the PDF hot path.
+//
+//   VIEW_FWD  : alpha -> J = expand(alpha) (spectral.py:68-79)
+//               E = E_inc + G_D J          (forward.py:140-146, losses.py:220)
+//               D = J G_S^T - d (masked), ||D||^2, g_rows (losses.py:229-232,285-287)
+//               ||E_i||^2 partials for eps_reg (cie.py:42-50)
+//   VIEW_BWD  : g_J = g_J_local + G_D^H g_E   (forward.py:149-151, losses.py:303)
+//               g_alpha = truncate(g_J)/(m1 m2) (spectral.py:56-65, losses.py:306)
+//               optionally scattered straight into the network's output
+//               gradient rows (network.py:575-582)
+//   VIEW_APPLY: y = G_D x or G_D^H x on dense images (init path, tests)
+//
+// One thread-block CLUSTER per view.  Rank c of CS owns spatial rows
+// [c*M/CS, (c+1)*M/CS) and spectral columns [c*P/CS, (c+1)*P/CS).  The
+// two 2-D transposes of the row-column FFT go through distributed shared
+// memory, so the padded P x P spectrum never touches HBM:
+//   A: row FFTs of my (nonzero) rows      -> DSMEM scatter by column owner
+//   B: per column  FFT, x K^, inverse FFT -> DSMEM scatter by row owner
+//   C: inverse row FFTs of my rows, crop to M columns
+#pragma once
+#include "pdf_common.cuh"
+
+namespace pdf {
+
+enum { VIEW_FWD = 0, VIEW_BWD = 1, VIEW_APPLY = 2 };
+
+template <typename T>
+struct ViewArgs {
+  int M, mf, R, n, CS;
+  const C<T>* khat;   // permuted / 1/P^2-scaled kernel spectrum, [P(col pos)][P(row pos)]
+  const C<T>* twP;    // exp(-2 pi i k / P), k < P
+  const C<T>* twM;    // exp(-2 pi i k / M), k < M
+  // FWD
+  const C<T>* alpha;  // [S*n][M0]
+  const C<T>* einc;   // [S or 1][n][M][M]
+  long long einc_scene_stride;   // elements; 0 = shared across scenes
+  const C<T>* gs;     // [R][M*M]
+  const C<T>* data;   // [S][n][R]
+  const T* mask;      // [S][n][R] or null
+  const double* c_sca;  // [S]
+  C<T>* J;            // [S*n][M][M]
+  C<T>* E;            // [S*n][M][M]
+  double* norms;      // [S*n][CS]
+  C<T>* grows;        // [S*n][R]
+  double* dloss;      // [S*n]
+  // BWD
+  const C<T>* gE;     // [S*n][M][M]
+  const C<T>* gJloc;  // [S*n][M][M]
+  C<T>* galpha;       // [S*n][M0] or null
+  T* gy;              // [S][rows][D0] or null
+  const T* cout;      // [S][D0] output gain per feature
+  int joint;
+  // APPLY
+  const C<T>* x;
+  C<T>* y;
+  int conj_in, conj_out;
+};
+
+template <typename T>
+struct ViewSmem {
+  C<T>* tw;     // P
+  C<T>* twm;    // M
+  C<T>* bufA;   // M * (P/CS)
+  C<T>* bufB;   // (M/CS) * P
+  C<T>* rows;   // (M/CS) * M
+  C<T>* small;  // M0 + (M/CS)*K : A (spectral grid) then V / U
+  // followed by xch: max(CS*R, M0) partial-sum exchange (read remotely)
+};
+
+template <typename T>
+__host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) {
+  const int P = 2 * M, K = 2 * mf, M0 = K * K;
+  const int rp = M / CS;
+  size_t a = (size_t)M0 + (size_t)rp * K;
+  size_t xch = (size_t)CS * R > (size_t)M0 ? (size_t)CS * R : (size_t)M0;
+  size_t n = (size_t)P + M + (size_t)M * (P / CS) + (size_t)rp * P + (size_t)rp * M + a + xch;
+  return n * sizeof(C<T>) + 64 * sizeof(double);
+}
+
+template <typename T>
+__device__ inline int corner_freq(int u, int mf, int M) { return u < mf ? u : M - 2 * mf + u; }
+// index in the reference coefficient vector of spectral grid entry (u, v)
+__device__ inline int corner_slot(int u, int v, int mf) {
+  return (((u / mf) * 2 + (v / mf)) * mf + (u % mf)) * mf + (v % mf);
+}
+
+template <typename T>
+__device__ inline double block_sum_d(double v, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum<double>(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];   // fixed order
+  return s;
+}
+
+template <typename T, int E, int MODE>
+__global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int P = 32 * E;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = a.CS;
+  const int rank = (int)cluster.block_rank();
+  const int M = a.M, mf = a.mf, K = 2 * mf, M0 = K * K;
+  const int rp = M / CS, cp = P / CS;
+  const int y0 = rank * rp;
+  const int v = blockIdx.y;                 // global view index (scene*n + view)
+  const int scene = v / a.n, view = v % a.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // element n = lane + 32k of a length-P line is inside the unpadded M = P/2
+  // window iff k < E/2 (E >= 2) or, for P = 32, lane < 16
+  constexpr int KH = E >= 2 ? E / 2 : 1;
+  const bool lane_ok = (E >= 2) || (lane < 16);
+
+  ViewSmem<T> s;
+  C<T>* p = reinterpret_cast<C<T>*>(smem_raw);
+  s.tw = p; p += P;
+  s.twm = p; p += M;
+  s.bufA = p; p += (size_t)M * cp;
+  s.bufB = p; p += (size_t)rp * P;
+  s.rows = p; p += (size_t)rp * M;
+  s.small = p; p += (size_t)M0 + (size_t)rp * K;
+  C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)M0 ? (size_t)CS * a.R : (size_t)M0);
+  double* red = reinterpret_cast<double*>(p);
+
+  for (int i = tid; i < P; i += blockDim.x) s.tw[i] = a.twP[i];
+  for (int i = tid; i < M; i += blockDim.x) s.twm[i] = a.twM[i];
+  const size_t img = (size_t)M * M;
+
+  // ---------------- stage 0: my input rows -> s.rows ----------------------
+  if constexpr (MODE == VIEW_FWD) {
+    const C<T>* al = a.alpha + (size_t)v * M0;
+    for (int i = tid; i < M0; i += blockDim.x) {
+      const int u = i / K, w = i % K;
+      s.small[i] = al[corner_slot(u, w, mf)];      // A[u][w]
+    }
+    __syncthreads();
+    // V[yl][w] = sum_u A[u][w] exp(+2 pi i kr_u y / M)  -> stored after A
+    C<T>* V = s.small + M0;
+    for (int i = tid; i < rp * K; i += blockDim.x) {
+      const int yl = i / K, w = i % K, y = y0 + yl;
+      C<T> acc = czero<T>();
+      for (int u = 0; u < K; ++u) {
+        const int f = corner_freq<T>(u, mf, M);
+        acc = cadd<T>(acc, cmulc<T>(s.small[u * K + w], s.twm[(f * y) & (M - 1)]));
+      }
+      V[i] = acc;
+    }
+    __syncthreads();
+    const T inv = T(1) / (T(M) * T(M));
+    for (int i = tid; i < rp * M; i += blockDim.x) {
+      const int yl = i / M, x = i % M;
+      C<T> acc = czero<T>();
+      for (int w = 0; w < K; ++w) {
+        const int f = corner_freq<T>(w, mf, M);
+        acc = cadd<T>(acc, cmulc<T>(V[yl * K + w], s.twm[(f * x) & (M - 1)]));
+      }
+      acc = cscale<T>(acc, inv);
+      s.rows[i] = acc;
+      a.J[(size_t)v * img + (size_t)(y0 + yl) * M + x] = acc;
+    }
+    __syncthreads();
+  } else if constexpr (MODE == VIEW_BWD) {
+    const C<T>* g = a.gE + (size_t)v * img + (size_t)y0 * M;
+    for (int i = tid; i < rp * M; i += blockDim.x) s.rows[i] = conj_<T>(g[i]);
+    __syncthreads();
+  } else {
+    const C<T>* g = a.x + (size_t)v * img + (size_t)y0 * M;
+    for (int i = tid; i < rp * M; i += blockDim.x) {
+      C<T> t = g[i];
+      s.rows[i] = a.conj_in ? conj_<T>(t) : t;
+    }
+    __syncthreads();
+  }
+
+  // ---------------- stage A: row FFTs, scatter to column owners ------------
+  for (int yl = warp; yl < rp; yl += nw) {
+    C<T> x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int col = lane + 32 * k;
+      x[k] = (k < KH && lane_ok) ? s.rows[yl * M + col] : czero<T>();
+    }
+    warp_fft_fwd<T, E>(x, s.tw, lane);
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int pos = q * 32 + lane;
+      const int dst = pos / cp, lc = pos - dst * cp;
+      C<T>* rb = cluster.map_shared_rank(s.bufA, dst);
+      rb[(size_t)(y0 + yl) * cp + lc] = x[q];
+    }
+  }
+
+  if constexpr (MODE == VIEW_FWD) {
+    // partial data residual over my pixels: sum_p J[p] G_S[r, p]
+    const size_t p0 = (size_t)y0 * M;
+    const int np = rp * M;
+    for (int r = warp; r < a.R; r += nw) {
+      const C<T>* g = a.gs + (size_t)r * img + p0;
+      C<T> acc = czero<T>();
+      for (int i = lane; i < np; i += 32) acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
+      acc.x = warp_sum<T>(acc.x);
+      acc.y = warp_sum<T>(acc.y);
+      if (lane == 0) {
+        C<T>* rx = cluster.map_shared_rank(xch, 0);
+        rx[rank * a.R + r] = acc;
+      }
+    }
+  }
+  cluster.sync();
+
+  if constexpr (MODE == VIEW_FWD) {
+    if (rank == 0) {
+      // D = sum of partials - d, masked; g_rows = 2 D mask / c_sca
+      double part = 0.0;
+      const double csca = a.c_sca[scene];
+      for (int r = tid; r < a.R; r += blockDim.x) {
+        C<T> acc = czero<T>();
+        for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * a.R + r]);
+        const size_t di = (size_t)v * a.R + r;
+        C<T> d = csub<T>(acc, a.data[di]);
+        T mk_ = a.mask ? a.mask[di] : T(1);
+        d = cscale<T>(d, mk_);
+        part += (double)cabs2<T>(d);
+        a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
+      }
+      double tot = block_sum_d<T>(part, red);
+      if (tid == 0) a.dloss[v] = tot;
+    }
+  }
+
+  // ---------------- stage B: columns: FFT, x K^, inverse FFT ---------------
+  for (int cc = warp; cc < cp; cc += nw) {
+    const int posc = rank * cp + cc;
+    C<T> x[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int row = lane + 32 * k;
+      x[k] = (k < KH && lane_ok) ? s.bufA[(size_t)row * cp + cc] : czero<T>();
+    }
+    warp_fft_fwd<T, E>(x, s.tw, lane);
+    const C<T>* kh = a.khat + (size_t)posc * P;
+#pragma unroll
+    for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kh[q * 32 + lane]);
+    warp_fft_inv<T, E>(x, s.tw, lane);
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      if (!lane_ok) break;
+      const int y = lane + 32 * k;
+      const int dst = y / rp, yl = y - dst * rp;
+      C<T>* rb = cluster.map_shared_rank(s.bufB, dst);
+      rb[(size_t)yl * P + posc] = x[k];
+    }
+  }
+  cluster.sync();
+
+  // ---------------- stage C: inverse row FFTs, crop ------------------------
+  double nrm = 0.0;
+  for (int yl = warp; yl < rp; yl += nw) {
+    C<T> x[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) x[q] = s.bufB[(size_t)yl * P + q * 32 + lane];
+    warp_fft_inv<T, E>(x, s.tw, lane);
+    const size_t rowoff = (size_t)v * img + (size_t)(y0 + yl) * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      if (!lane_ok) break;
+      const int col = lane + 32 * k;
+      if constexpr (MODE == VIEW_FWD) {
+        const C<T>* ei = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img +
+                         (size_t)(y0 + yl) * M + col;
+        C<T> e = cadd<T>(*ei, x[k]);
+        a.E[rowoff + col] = e;
+        nrm += (double)cabs2<T>(e);
+      } else if constexpr (MODE == VIEW_BWD) {
+        s.rows[yl * M + col] = cadd<T>(a.gJloc[rowoff + col], conj_<T>(x[k]));
+      } else {
+        a.y[rowoff + col] = a.conj_out ? conj_<T>(x[k]) : x[k];
+      }
+    }
+  }
+
+  if constexpr (MODE == VIEW_FWD) {
+    double tot = block_sum_d<T>(nrm, red);
+    if (tid == 0) a.norms[(size_t)v * CS + rank] = tot;
+  }
+
+  if constexpr (MODE == VIEW_BWD) {
+    __syncthreads();
+    // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)
+    C<T>* U = s.small + M0;
+    for (int i = tid; i < rp * K; i += blockDim.x) {
+      const int yl = i / K, w = i % K;
+      const int f = corner_freq<T>(w, mf, M);
+      C<T> acc = czero<T>();
+      for (int x = 0; x < M; ++x) acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
+      U[i] = acc;
+    }
+    __syncthreads();
+    // my partial G[u][w] = sum_yl exp(-2 pi i kr_u y / M) U[yl][w]
+    C<T>* mine = xch;
+    for (int i = tid; i < M0; i += blockDim.x) {
+      const int u = i / K, w = i % K;
+      const int f = corner_freq<T>(u, mf, M);
+      C<T> acc = czero<T>();
+      for (int yl = 0; yl < rp; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], s.twm[(f * (y0 + yl)) & (M - 1)]));
+      mine[i] = acc;
+    }
+    cluster.sync();
+    const T inv = T(1) / (T(M) * T(M));
+    for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {
+      C<T> acc = czero<T>();
+      for (int c = 0; c < CS; ++c) {
+        const C<T>* other = cluster.map_shared_rank(xch, c);
+        acc = cadd<T>(acc, other[i]);
+      }
+      acc = cscale<T>(acc, inv);
+      const int u = i / K, w = i % K;
+      const int slot = corner_slot(u, w, mf);
+      if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
+      if (a.gy) {
+        const int D0 = 2 * M0 * (a.joint ? a.n : 1);
+        const int rows = a.joint ? 1 : a.n;
+        const int re = a.joint ? view * M0 + slot : slot;
+        const int row = a.joint ? 0 : view;
+        T* gyrow = a.gy + ((size_t)scene * rows + row) * D0;
+        const T* co = a.cout + (size_t)scene * D0;
+        gyrow[re] = acc.x * co[re];
+        gyrow[re + D0 / 2] = acc.y * co[re + D0 / 2];
+      }
+    }
+    cluster.sync();
+  }
+}
+
+}  // namespace pdf

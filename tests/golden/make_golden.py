@@ -1,0 +1,235 @@
+"""Generate golden vectors by running the UNMODIFIED reference package.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [tiny cfg1 cfg2 cfg3 cfg4]
+
+Every array below comes from `pdfisp` itself (/root/reference/pkg/src), in
+float64 / complex128.  Plane-wave configs compose the reference's public
+functions in the order of reconstruct.py:194-236 with a plane-wave e_inc,
+exactly as SURVEY 8(c) prescribes.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+from pdfisp.config import C0, ImagingConfig  # noqa: E402
+from pdfisp.forward import (FieldSet, ScatteredData, add_awgn, apply_gd, apply_gd_adjoint,  # noqa: E402
+                            apply_gs_adjoint, build_greens, incident_fields, simulate,
+                            solve_total_field, synthesize_scattered)
+from pdfisp.filters import apply_cco  # noqa: E402
+from pdfisp.geometry import build_array, build_grid  # noqa: E402
+from pdfisp.losses import LossContext, grad_alpha  # noqa: E402
+from pdfisp import network  # noqa: E402
+from pdfisp.reconstruct import bp_initialize, init_alpha, reconstruct, relative_error  # noqa: E402
+from pdfisp.cie import recover_contrast  # noqa: E402
+from pdfisp.scenes import Scene, Shape, builtin_scene, rasterize  # noqa: E402
+from pdfisp.spectral import SpectralBasis, expand, truncate  # noqa: E402
+from pdfisp.losses import loss_total  # noqa: E402
+
+
+def plane_views(cfg, grid):
+    phi = 2.0 * np.pi * np.arange(cfg.n_tx) / cfg.n_tx
+    x, y = grid.centers[:, 0], grid.centers[:, 1]
+    v = np.exp(1j * cfg.wavenumber * (np.cos(phi)[:, None] * x + np.sin(phi)[:, None] * y))
+    return v.reshape(cfg.n_tx, cfg.m1, cfg.m2)
+
+
+def ellipse_poly(cx, cy, a, b, ang, eps, nv=256):
+    t = 2.0 * np.pi * np.arange(nv) / nv
+    ca, sa = np.cos(ang), np.sin(ang)
+    xs, ys = a * np.cos(t), b * np.sin(t)
+    return Shape(kind="polygon", eps_r=eps,
+                 vertices=tuple((float(cx + ca * u - sa * w), float(cy + sa * u + ca * w)) for u, w in zip(xs, ys)))
+
+
+def cfg4_scene(idx: int):
+    """1-4 non-overlapping ellipses, semi-axes U[0.15,0.5], chi U[0.5,3] (BASELINE cfg4)."""
+    rng = np.random.default_rng(idx)
+    k = int(rng.integers(1, 5))
+    shapes, placed = [], []
+    tries = 0
+    while len(shapes) < k and tries < 200:
+        tries += 1
+        a, b = rng.uniform(0.15, 0.5, 2)
+        cx, cy = rng.uniform(-1.0 + max(a, b), 1.0 - max(a, b), 2)
+        ang = rng.uniform(0.0, np.pi)
+        r = max(a, b)
+        if any(np.hypot(cx - px, cy - py) < r + pr for px, py, pr in placed):
+            continue
+        chi = rng.uniform(0.5, 3.0)
+        placed.append((cx, cy, r))
+        shapes.append(ellipse_poly(cx, cy, a, b, ang, 1.0 + chi))
+    return Scene(tuple(shapes)), rng
+
+
+def plane_problem(cfg, scene, snr_db, rng):
+    grid, arr = build_grid(cfg), build_array(cfg)
+    ops = build_greens(cfg, arr, grid)
+    views = plane_views(cfg, grid)
+    chi = rasterize(scene, grid)
+    e_tot = solve_total_field(chi, FieldSet(views, "incident"), ops,
+                              method="dense" if chi.values.size <= 1024 else "fft")
+    data = add_awgn(synthesize_scattered(chi, e_tot, ops), snr_db, rng)
+    return grid, arr, ops, views, chi, data
+
+
+def composed_reconstruct(cfg, data, views, ops, chi_true, k):
+    """reconstruct.py:194-236 with plane-wave e_inc."""
+    basis = SpectralBasis(cfg.m1, cfg.m2, cfg.m_f)
+    fs = FieldSet(views, "incident")
+    chi0, r0 = bp_initialize(data, fs, ops, cfg.beta)
+    alpha0 = init_alpha(r0, data, fs, ops, basis, cfg.beta)
+    net = network.init_network(basis.m0, np.random.default_rng(cfg.rng_seed))
+    adam = network.AdamState.for_params(net, lr=cfg.learn_rate)
+    ctx = LossContext(data=data, e_inc=views, ops=ops, basis=basis, beta=cfg.beta,
+                      lambdas=(cfg.lambda1, cfg.lambda2, cfg.lambda3), tau_b=cfg.tau_b)
+    trace = []
+    for _ in range(k):
+        g, bd = network.grad_loss(net, alpha0, ctx)
+        trace.append(bd.as_row())
+        net, adam = network.adam_step(adam, net, g)
+    ahat = alpha0 + network.forward_net(net, alpha0)
+    final = loss_total(ahat, ctx).as_row()
+    chi_hat = recover_contrast(ahat, views, ops, basis)
+    chi_cco = apply_cco(chi_hat, cfg.cco)
+    rel = relative_error(chi_cco.real + 1.0, chi_true.values.real + 1.0)
+    return dict(chi0=chi0, r0=r0, alpha0=alpha0, trace=np.array(trace), final=np.array(final),
+                chi_hat=chi_hat, chi_cco=chi_cco, rel_error=rel, ctx=ctx)
+
+
+def save(name, **arrs):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrs)
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB)", flush=True)
+
+
+def make_tiny():
+    """reference tests/conftest.py:43-57 setup: 16x16, m_f=3, 8 tx / 8 rx, austria eps 2."""
+    cfg = ImagingConfig(m1=16, m2=16, m_f=3, n_tx=8, n_rx=8, k_iters=30).validate()
+    grid, arr = build_grid(cfg), build_array(cfg)
+    ops = build_greens(cfg, arr, grid)
+    einc = incident_fields(cfg, arr, grid)
+    basis = SpectralBasis(16, 16, 3)
+    sim = simulate(cfg, builtin_scene("austria", 2.0, scale=0.9))
+    ctx = LossContext(data=sim.data, e_inc=einc.views, ops=ops, basis=basis, beta=6.0,
+                      lambdas=(1e-3, 1e-5, 1e-5), tau_b=0.5)
+    rng = np.random.default_rng(7)
+    n, m0 = 8, basis.m0
+    alpha = 0.1 * (rng.standard_normal((n, m0)) + 1j * rng.standard_normal((n, m0)))
+    g, bd = grad_alpha(alpha, ctx)
+    chi0, r0 = bp_initialize(sim.data, einc, ops, 6.0)
+    alpha0 = init_alpha(r0, sim.data, einc, ops, basis, 6.0)
+    g0, bd0 = grad_alpha(alpha0, ctx)
+    ctx_fr = LossContext(data=sim.data, e_inc=einc.views, ops=ops, basis=basis, beta=6.0,
+                         lambdas=(1e-3, 1e-5, 1e-5), tau_b=0.5, r_fixed=r0)
+    g_fr, bd_fr = grad_alpha(alpha, ctx_fr)
+    mask = (np.random.default_rng(11).random((n, 8)) > 0.3).astype(float)
+    dmask = ScatteredData(matrix=sim.data.matrix * mask, mask=mask)
+    ctx_mk = LossContext(data=dmask, e_inc=einc.views, ops=ops, basis=basis, beta=6.0,
+                         lambdas=(1e-3, 1e-5, 1e-5), tau_b=0.5)
+    g_mk, bd_mk = grad_alpha(alpha, ctx_mk)
+    # network gradient at perturbed parameters (reference tests/test_network.py:73-94)
+    net = network.init_network(m0, np.random.default_rng(6))
+    flat = network.flatten_params(net)
+    flat = flat + 0.05 * np.random.default_rng(6).standard_normal(flat.size)
+    net = network.unflatten_params(flat, net)
+    gflat, bdn = network.grad_loss(net, alpha0, ctx)
+    dalpha = network.forward_net(net, alpha0)
+    # Adam sequence (reference tests/test_network.py:111-123)
+    rs = np.random.default_rng(9)
+    p_adam = network.init_network(16, rs)
+    st = network.AdamState.for_params(p_adam, lr=1e-2)
+    flat_a0 = network.flatten_params(p_adam)
+    grads = [rs.standard_normal(flat_a0.size) for _ in range(5)]
+    p = p_adam
+    for gg in grads:
+        p, st = network.adam_step(st, p, gg)
+    # primitives
+    rr = np.random.default_rng(12)
+    x = rr.standard_normal((3, 16, 16)) + 1j * rr.standard_normal((3, 16, 16))
+    rows = rr.standard_normal((3, 8)) + 1j * rr.standard_normal((3, 8))
+    # 30-iteration reference reconstruct (line sources, the reference's own entry point)
+    res = reconstruct(cfg, sim.data, chi_true=sim.chi_true)
+    save("tiny", data=sim.data.matrix, chi_true=sim.chi_true.values, e_inc=einc.views, khat=ops.gd_kernel_hat,
+         gs=ops.gs_matrix, alpha=alpha, g_alpha=g, bd=np.array(bd.as_row()), chi0=chi0, r0=r0, alpha0=alpha0,
+         g_alpha0=g0, bd0=np.array(bd0.as_row()), g_frozen=g_fr, bd_frozen=np.array(bd_fr.as_row()),
+         mask=mask, g_mask=g_mk, bd_mask=np.array(bd_mk.as_row()), net_flat=flat, grad_flat=gflat,
+         bd_net=np.array(bdn.as_row()), dalpha=dalpha, adam_p0=flat_a0, adam_grads=np.array(grads),
+         adam_p5=network.flatten_params(p), adam_m5=st.m, adam_v5=st.v,
+         x=x, gd_x=apply_gd(ops, x), gdh_x=apply_gd_adjoint(ops, x), rows=rows, gsh_rows=apply_gs_adjoint(ops, rows),
+         exp_alpha=expand(basis, alpha), trunc_x=truncate(basis, x),
+         rec_trace=np.array([b.as_row() for b in res.trace]), rec_final=np.array(res.final_loss.as_row()),
+         rec_chi_hat=res.chi_hat.values, rec_chi_cco=res.chi_cco.values, rec_chi0=res.chi0.values,
+         rec_rel=np.array(res.rel_error))
+
+
+def plane_case(name, cfg, scene, snr_db, noise_seed, k, store_ops=False):
+    t0 = time.time()
+    grid, arr, ops, views, chi, data = plane_problem(cfg, scene, snr_db, np.random.default_rng(noise_seed))
+    out = composed_reconstruct(cfg, data, views, ops, chi, k)
+    ctx = out["ctx"]
+    g0, bd0 = grad_alpha(out["alpha0"], ctx)
+    net = network.init_network(ctx.basis.m0, np.random.default_rng(cfg.rng_seed))
+    flat = network.flatten_params(net)
+    flat = flat + 0.02 * np.random.default_rng(123).standard_normal(flat.size)
+    gflat, bdn = network.grad_loss(network.unflatten_params(flat, net), out["alpha0"], ctx)
+    idx = np.sort(np.random.default_rng(5).choice(flat.size, size=min(4096, flat.size), replace=False))
+    extra = dict(khat=ops.gd_kernel_hat, gs=ops.gs_matrix) if store_ops else {}
+    save(name, data=data.matrix, chi_true=chi.values, chi0=out["chi0"], alpha0=out["alpha0"],
+         g_alpha0=g0, bd0=np.array(bd0.as_row()), grad_idx=idx, grad_sub=gflat[idx],
+         grad_norms=np.array([np.linalg.norm(gflat), np.abs(gflat).max()]), bd_net=np.array(bdn.as_row()),
+         trace=out["trace"], final=out["final"], chi_hat=out["chi_hat"], chi_cco=out["chi_cco"],
+         rel_error=np.array(out["rel_error"]), einc_checksum=np.array([views.sum(), np.abs(views).sum()]),
+         gs_checksum=np.array([ops.gs_matrix.sum(), np.abs(ops.gs_matrix).sum()]),
+         khat_checksum=np.array([ops.gd_kernel_hat.sum(), np.abs(ops.gd_kernel_hat).sum()]), **extra)
+    print(f"{name}: rel_error {out['rel_error']:.6f}  ({time.time() - t0:.1f}s)", flush=True)
+
+
+def make_cfg1():
+    cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=32, m2=32, n_tx=16, n_rx=32, ring_radius=3.0, m_f=5,
+                        k_iters=200, rng_seed=0).validate()
+    scene = Scene((Shape(kind="disk", eps_r=2.0, center=(0.0, 0.0), radius=0.4),))
+    plane_case("cfg1", cfg, scene, 20 * np.log10(100 / 5), 0, 200, store_ops=True)
+
+
+def make_cfg2():
+    cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
+                        k_iters=500, rng_seed=1).validate()
+    scene = Scene((Shape(kind="disk", eps_r=3.0, center=(-0.35, 0.0), radius=0.3),
+                   Shape(kind="disk", eps_r=3.0, center=(0.35, 0.0), radius=0.3)))
+    plane_case("cfg2", cfg, scene, 20 * np.log10(100 / 5), 1, 500)
+
+
+def make_cfg3():
+    cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=36, n_rx=36, ring_radius=3.0, m_f=8,
+                        k_iters=500, rng_seed=2).validate()
+    scene = Scene((Shape(kind="annulus", eps_r=4.0 + 0.5j, center=(0.0, 0.0), r_inner=0.3, r_outer=0.5),
+                   Shape(kind="disk", eps_r=2.5, center=(0.6, 0.6), radius=0.15)))
+    plane_case("cfg3", cfg, scene, 20.0, 2, 500)
+
+
+def make_cfg4(n_scenes=2, k=500):
+    for idx in range(n_scenes):
+        cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
+                            k_iters=k, rng_seed=idx).validate()
+        scene, rng = cfg4_scene(idx)
+        grid, arr, ops, views, chi, data = plane_problem(cfg, scene, 20 * np.log10(100 / 5), rng)
+        out = composed_reconstruct(cfg, data, views, ops, chi, k)
+        save(f"cfg4_s{idx}", data=data.matrix, chi_true=chi.values, alpha0=out["alpha0"], trace=out["trace"],
+             final=out["final"], chi_cco=out["chi_cco"], rel_error=np.array(out["rel_error"]))
+        print(f"cfg4 scene {idx}: rel_error {out['rel_error']:.6f}", flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["tiny", "cfg1", "cfg2", "cfg3", "cfg4"]
+    for w in which:
+        globals()[f"make_{w}"]()
