@@ -17,6 +17,15 @@
 using namespace pdf;
 
 static thread_local std::string g_err;
+static int env_int(const char* name, int dflt);
+// programmatic dependent launch for the hot-loop kernels (PDF_PDL=0 disables)
+static const int g_pdl = env_int("PDF_PDL", 1);
+
+// cluster caps (tunable for experiments: PDF_NET_CLUSTER, PDF_VIEW_CLUSTER)
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -111,7 +120,8 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   c->E = c->P / 32;
   c->K = 2 * d->mf;
   c->M0 = c->K * c->K;
-  c->CS = 8;
+  c->CS = env_int("PDF_VIEW_CLUSTER", 8);
+  if (c->CS < 1 || c->CS > 16 || (M % c->CS) || ((2 * M) % c->CS)) return fail(PDF_EINVAL, "view cluster size");
   c->rows = d->joint ? 1 : d->n;
   c->D0 = 2 * c->M0 * (d->joint ? d->n : 1);
   c->H = 2 * c->D0;
@@ -148,13 +158,15 @@ static cudaError_t launch_cluster(F kern, dim3 grid, dim3 block, size_t smem, cu
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cluster.x;
   attr[0].val.clusterDim.y = cluster.y;
   attr[0].val.clusterDim.z = cluster.z;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
 }
 
@@ -163,6 +175,23 @@ static cudaError_t prep(K kern, size_t smem) {
   cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
+template <typename K>
+static cudaError_t plain_launch(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, void** args) {
+  cudaError_t e = cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
 }
 
 template <typename T, int MODE>
@@ -217,37 +246,42 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   p.c_inc = c->c_inc; p.gJ = (C<T>*)c->gJ; p.gE = (C<T>*)c->gE; p.part = c->part;
   p.chi_out = (C<T>*)chi_out; p.err = c->err;
   dim3 grid(c->M / c->TX, c->M, c->d.S);
-  pixel_kernel<T, GRAD><<<grid, 256, 0, st>>>(p);
-  cudaError_t e = cudaGetLastError();
+  const size_t smem = GRAD ? pixel_smem_bytes<T>(c->d.n, c->d.R) : 0;
+  constexpr int epc = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
+  if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
+  void* args[] = {&p};
+  cudaError_t e = plain_launch(pixel_kernel<T, GRAD>, grid, dim3(PIX_NW * 32), smem, st, args);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("pixel kernel: ") + cudaGetErrorString(e));
   return PDF_OK;
 }
 
+static FinalizeArgs fin_args(pdf_ctx* c, double* bd, double* trace) {
+  FinalizeArgs f = {};
+  f.n = c->d.n; f.ntiles = c->ntiles; f.S = c->d.S;
+  f.l1 = c->d.lambda1; f.l2 = c->d.lambda2; f.l3 = c->d.lambda3;
+  f.c_inc = c->c_inc; f.c_sca = c->c_sca; f.dloss = c->dloss; f.part = c->part;
+  f.bd = bd ? bd : c->bd; f.trace = trace; f.step = c->step; f.err = c->err;
+  return f;
+}
+
 template <typename T>
-static int phys_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st) {
+static int phys_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, double* bd = nullptr,
+                         double* trace = nullptr, bool fin = false) {
   ViewArgs<T> a = view_common<T>(c);
+  a.fin = fin_args(c, bd, trace);
+  a.do_fin = fin ? 1 : 0;
   a.gE = (const C<T>*)c->gE; a.gJloc = (const C<T>*)c->gJ;
   a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
   return launch_view<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st);
 }
 
 static int finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st) {
-  FinalizeArgs f = {};
-  f.n = c->d.n; f.ntiles = c->ntiles; f.S = c->d.S;
-  f.l1 = c->d.lambda1; f.l2 = c->d.lambda2; f.l3 = c->d.lambda3;
-  f.c_inc = c->c_inc; f.c_sca = c->c_sca; f.dloss = c->dloss; f.part = c->part;
-  f.bd = bd ? bd : c->bd; f.trace = trace; f.step = c->step; f.err = c->err;
+  FinalizeArgs f = fin_args(c, bd, trace);
   finalize_kernel<<<c->d.S, 128, 0, st>>>(f);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("finalize: ") + cudaGetErrorString(e));
   return PDF_OK;
-}
-
-static int clamp_cluster(int n, int per) {
-  int c = n / per;
-  if (c < 1) c = 1;
-  if (c > 16) c = 16;
-  return c;
 }
 
 template <typename T>
@@ -260,21 +294,22 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
   a.out = out; a.out_ss = (long long)c->rows * N; a.final_layer = final_layer;
   a.cout = (const T*)c->cout; a.alpha0 = (const C<T>*)c->alpha0; a.alpha_hat = (C<T>*)c->alpha_hat;
   a.n = c->d.n; a.M0 = c->M0; a.joint = c->d.joint; a.step = step;
-  const int CK = clamp_cluster(K, 64);
-  const int RP = 16 * c->RB;
-  const size_t smem = (size_t)(NET_TILE * (NET_KC + 1) + RP * (NET_KC + 1) + RP * NET_TILE) * sizeof(T);
-  dim3 grid((N + NET_TILE - 1) / NET_TILE, CK, c->d.S), block(NET_THREADS), cl(1, CK, 1);
+  a.w_early = woff != 0;   // W2, W3 were last written >= 2 launches earlier; W1 by the launch right before
+  if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
+  // one output row per warp while a single scene cannot fill the GPU, two otherwise
+  const int opw = (c->RB == 1 && (c->d.S * N) / (NET_THREADS / 32) >= 2 * 148 * 4) ? 2 : 1;
   void* args[] = {&a};
   cudaError_t e;
-  switch (c->RB) {
-#define FCASE(RR)                                                               \
-  case RR: {                                                                    \
-    auto k = net_fwd_kernel<T, RR>;                                             \
-    e = prep(k, smem);                                                          \
-    if (e == cudaSuccess) e = launch_cluster(k, grid, block, smem, st, cl, args); \
-    break;                                                                      \
+  switch (c->RB * 4 + opw) {
+#define FCASE(RR, OO)                                                                      \
+  case RR * 4 + OO: {                                                                      \
+    const size_t smem = fwd_smem_elems<T, RR>() * sizeof(T);                               \
+    const int per = (NET_THREADS / 32) * OO;                                               \
+    e = plain_launch(net_fwd_kernel<T, RR, OO>, dim3((N + per - 1) / per, c->d.S),          \
+                     dim3(NET_THREADS), smem, st, args);                                   \
+    break;                                                                                 \
   }
-    FCASE(1) FCASE(2) FCASE(3) FCASE(4) FCASE(5)
+    FCASE(1, 1) FCASE(1, 2) FCASE(2, 1) FCASE(2, 2) FCASE(3, 1) FCASE(4, 1) FCASE(5, 1)
 #undef FCASE
     default: return fail(PDF_EINVAL, "rows");
   }
@@ -290,24 +325,22 @@ static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T*
   a.gz = gz; a.gz_ss = (long long)c->rows * N;
   a.hin = hin; a.hin_ss = (long long)c->rows * K;
   a.theta = theta; a.th_ss = c->Np; a.w_off = woff; a.b_off = boff;
-  a.m = m; a.v = v; a.grad = grad; a.fused = fused; a.step = c->step;
+  a.m = m; a.v = v; a.grad = grad; a.step = c->step;
   a.lr = (T)c->d.lr; a.b1 = (T)c->d.adam_b1; a.b2 = (T)c->d.adam_b2; a.eps = (T)c->d.adam_eps;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
-  const int CN = clamp_cluster(N, 64);
-  const int RP = 16 * c->RB;
-  const size_t smem = (size_t)(RP * NET_TILE + NET_KC * NET_TILE + RP * (NET_KC + 1) + RP * NET_TILE) * sizeof(T);
-  dim3 grid((K + NET_TILE - 1) / NET_TILE, CN, c->d.S), block(NET_THREADS), cl(1, CN, 1);
+  if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
   void* args[] = {&a};
   cudaError_t e;
-  switch (c->RB) {
-#define BCASE(RR)                                                               \
-  case RR: {                                                                    \
-    auto k = net_bwd_kernel<T, RR>;                                             \
-    e = prep(k, smem);                                                          \
-    if (e == cudaSuccess) e = launch_cluster(k, grid, block, smem, st, cl, args); \
-    break;                                                                      \
+  const dim3 grid((K + BWD_COLS - 1) / BWD_COLS, c->d.S), block(NET_THREADS);
+  switch (c->RB * 2 + (fused ? 1 : 0)) {
+#define BCASE(RR, FF)                                                                      \
+  case RR * 2 + FF: {                                                                      \
+    const size_t smem = bwd_smem_elems<T, RR>() * sizeof(T);                               \
+    e = plain_launch(net_bwd_kernel<T, RR, (FF != 0)>, grid, block, smem, st, args);      \
+    break;                                                                                 \
   }
-    BCASE(1) BCASE(2) BCASE(3) BCASE(4) BCASE(5)
+    BCASE(1, 0) BCASE(1, 1) BCASE(2, 0) BCASE(2, 1) BCASE(3, 0) BCASE(3, 1) BCASE(4, 0) BCASE(4, 1)
+    BCASE(5, 0) BCASE(5, 1)
 #undef BCASE
     default: return fail(PDF_EINVAL, "rows");
   }
@@ -339,34 +372,37 @@ template <typename T>
 static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, double* bd, double* trace, int fused,
                      cudaStream_t st, cudaEvent_t* ev = nullptr) {
   // phase order (PDF_NPHASES = 10): fwd_l1 fwd_l2 fwd_l3 view_fwd pixel view_bwd finalize bwd_l3 bwd_l2 bwd_l1
+  // PDF_SKIP_PHASES (bitmask, measurement experiments only) drops kernels.
+  static const int skip = env_int("PDF_SKIP_PHASES", 0);
   int ph = 0;
-  auto mark = [&]() { if (ev) cudaEventRecord(ev[ph++], st); };
+  auto mark = [&]() { if (ev) cudaEventRecord(ev[ph], st); ++ph; };
+  auto run = [&]() { return !(skip >> ph & 1); };
   const Offs o = offsets(c);
   const T* thc = (const T*)theta;
   T* th = (T*)theta;
   mark();
-  TRY(net_fwd_layer<T>(c, (const T*)c->x0, c->D0, c->H, thc, o.w1, o.b1, (T*)c->h1, 0, fused ? c->step : nullptr, st));
+  if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->x0, c->D0, c->H, thc, o.w1, o.b1, (T*)c->h1, 0,
+                                  fused ? c->step : nullptr, st));
   mark();
-  TRY(net_fwd_layer<T>(c, (const T*)c->h1, c->H, c->H, thc, o.w2, o.b2, (T*)c->h2, 0, nullptr, st));
+  if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h1, c->H, c->H, thc, o.w2, o.b2, (T*)c->h2, 0, nullptr, st));
   mark();
-  TRY(net_fwd_layer<T>(c, (const T*)c->h2, c->H, c->D0, thc, o.w3, o.b3, nullptr, 1, nullptr, st));
+  if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h2, c->H, c->D0, thc, o.w3, o.b3, nullptr, 1, nullptr, st));
   mark();
-  TRY(phys_forward<T>(c, c->alpha_hat, st));
+  if (run()) TRY(phys_forward<T>(c, c->alpha_hat, st));
   mark();
-  TRY((phys_pixel<T, true>(c, nullptr, st)));
+  if (run()) TRY((phys_pixel<T, true>(c, nullptr, st)));
   mark();
-  TRY(phys_backward<T>(c, nullptr, c->gy, st));
+  if (run()) TRY(phys_backward<T>(c, nullptr, c->gy, st, bd, trace, true));
   mark();
-  TRY(finalize(c, bd, trace, st));
+  mark();   // finalize is fused into view_bwd (phase kept for a stable layout)
+  if (run()) TRY(net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, (T*)m, (T*)v,
+                                  (T*)grad, fused, (T*)c->gz2, st));
   mark();
-  TRY(net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, (T*)m, (T*)v, (T*)grad,
-                       fused, (T*)c->gz2, st));
+  if (run()) TRY(net_bwd_layer<T>(c, (const T*)c->gz2, (const T*)c->h1, c->H, c->H, th, o.w2, o.b2, (T*)m, (T*)v,
+                                  (T*)grad, fused, (T*)c->gz1, st));
   mark();
-  TRY(net_bwd_layer<T>(c, (const T*)c->gz2, (const T*)c->h1, c->H, c->H, th, o.w2, o.b2, (T*)m, (T*)v, (T*)grad,
-                       fused, (T*)c->gz1, st));
-  mark();
-  TRY(net_bwd_layer<T>(c, (const T*)c->gz1, (const T*)c->x0, c->D0, c->H, th, o.w1, o.b1, (T*)m, (T*)v, (T*)grad,
-                       fused, nullptr, st));
+  if (run()) TRY(net_bwd_layer<T>(c, (const T*)c->gz1, (const T*)c->x0, c->D0, c->H, th, o.w1, o.b1, (T*)m, (T*)v,
+                                  (T*)grad, fused, nullptr, st));
   mark();
   return PDF_OK;
 }
@@ -441,8 +477,7 @@ template <typename T>
 static int loss_grad_impl(pdf_ctx* c, const void* alpha, void* galpha, double* bd, cudaStream_t st) {
   TRY(phys_forward<T>(c, alpha, st));
   TRY((phys_pixel<T, true>(c, nullptr, st)));
-  TRY(phys_backward<T>(c, galpha ? galpha : c->galpha, nullptr, st));
-  return finalize(c, bd, nullptr, st);
+  return phys_backward<T>(c, galpha ? galpha : c->galpha, nullptr, st, bd, nullptr, true);
 }
 
 extern "C" int pdf_loss_grad(pdf_ctx* c, const void* alpha, void* galpha, double* bd, void* stream) {
@@ -508,7 +543,7 @@ extern "C" int pdf_grad_loss(pdf_ctx* c, const void* theta, void* grad, double* 
 template <typename T>
 static int adam_impl(pdf_ctx* c, void* theta, void* m, void* v, const void* g, long long cnt, int t,
                      cudaStream_t st) {
-  const double bc1 = 1.0 - pow(c->d.adam_b1, (double)t), bc2 = 1.0 - pow(c->d.adam_b2, (double)t);
+  const double bc1 = 1.0 / (1.0 - pow(c->d.adam_b1, (double)t)), bc2 = 1.0 / (1.0 - pow(c->d.adam_b2, (double)t));
   int blocks = (int)std::min<long long>((cnt + 255) / 256, 148LL * 16);
   adam_flat_kernel<T><<<blocks, 256, 0, st>>>((T*)theta, (T*)m, (T*)v, (const T*)g, cnt, (T)c->d.lr,
                                               (T)c->d.adam_b1, (T)c->d.adam_b2, (T)c->d.adam_eps, (T)bc1,

@@ -50,6 +50,24 @@ template <typename T> __device__ __forceinline__ T exp_(T x);
 template <> __device__ __forceinline__ float exp_<float>(float x) { return expf(x); }
 template <> __device__ __forceinline__ double exp_<double>(double x) { return exp(x); }
 
+// 16-byte asynchronous global -> shared copy (LDGSTS); zero-fills when !pred
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Programmatic dependent launch.  Kernels of the hot loop are launched with
+// programmatic stream serialization: code before pdl_wait() may overlap the
+// previous kernel, so it only touches data finalised two or more launches
+// earlier (weights, Adam moments, operators, constants); pdl_trigger() lets
+// the next kernel start its own prologue.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // numerically stable logistic, scipy.special.expit semantics
 template <typename T> __device__ __forceinline__ T sigmoid_(T z) {
   if (z >= T(0)) { T e = exp_<T>(-z); return T(1) / (T(1) + e); }

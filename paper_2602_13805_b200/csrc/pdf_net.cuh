@@ -5,24 +5,30 @@
 // w1, b1, w2, b2, w3, b3 with weights row-major (fan_out, fan_in), so
 // grad_loss / adam_step see the same flat vector the reference does.
 //
-// Forward layer  z = h W^T + b: CTA = 128 outputs x all rows for one K-slice;
-//   the CK CTAs of a cluster split K and reduce their partials through
-//   distributed shared memory in a fixed order (no float atomics).
-// Backward layer: CTA = 128 input columns x one slice of the outputs;
-//   it computes the partial g_h = g_z W from the OLD weights, the weight
-//   gradient g_W = g_z^T h tile by tile, and applies Adam in the same pass
-//   (the gradient never round-trips through HBM).  The CN CTAs of a
-//   cluster split the outputs and reduce g_h through DSMEM, then apply the
-//   tanh' of the layer input to produce the next g_z.
+// The layers are skinny (rows = incidences, 1..80) and wide (hundreds to
+// thousands of columns).  Both kernels stream every weight exactly once,
+// need no inter-CTA communication, and reduce in a fixed order:
+//
+// Forward  z = h W^T + b: a warp owns OPW output rows and its lanes split K
+//   (lane-contiguous 16-byte weight loads); the input rows arrive in
+//   double-buffered shared tiles (cp.async) and are reused by all OPW rows;
+//   the 32 lane partials are folded with a fixed shuffle tree.
+// Backward: a CTA owns 8 input columns k; its 256 threads are 8 columns x
+//   32 row subsets.  Each thread keeps h[:, k] and a partial g_h[:, k] and
+//   walks its rows n four at a time: W, m, v come straight from memory
+//   (64-byte row segments per warp), g_W[n,k] = sum_r g_z[r,n] h[r,k] and
+//   g_h[:,k] += g_z[:,n] W_old[n,k] use the same broadcast g_z values, Adam
+//   writes W, m, v back -- the weight gradient never round-trips through
+//   memory.  The 32 row-subset partials of g_h are summed in shared memory
+//   in a fixed order and multiplied by tanh'(h) to give the next g_z.
 #pragma once
 #include "pdf_common.cuh"
 
 namespace pdf {
 
-constexpr int NET_TILE = 128;   // outputs (fwd) / input columns (bwd) per CTA
-constexpr int NET_THREADS = 128;
-constexpr int NET_KC = 16;      // K (fwd) / N (bwd) chunk staged per step
 constexpr double OUTPUT_GAIN = 8.0;   // network.py:85
+constexpr int NET_THREADS = 256;
+template <typename T> struct Epc { static constexpr int v = 16 / sizeof(T); };   // elements per 16 B
 
 template <typename T>
 struct NetFwdArgs {
@@ -38,104 +44,139 @@ struct NetFwdArgs {
   C<T>* alpha_hat;                    // [S][n][M0]
   int n, M0, joint;
   int* step;                          // incremented once (train mode) or null
+  int w_early;                        // weights final two launches back: prefetch before pdl_wait
 };
 
-// rows padded to 16*RB; thread (rg, ng) of warp w owns rows rb*16+rg*4+{0..3}
-// and outputs w*32+ng*4+{0..3}
+template <typename T, int RB> struct FwdShape {
+  static constexpr int KCH = RB <= 2 ? 256 : 128;    // K per staged input chunk
+  static constexpr int P = KCH + Epc<T>::v;           // padded pitch
+  static constexpr int VL = KCH / 32;                 // elements per lane per chunk
+};
+
 template <typename T, int RB>
-__global__ void __launch_bounds__(NET_THREADS) net_fwd_kernel(NetFwdArgs<T> a) {
+__host__ __device__ constexpr size_t fwd_smem_elems() {
+  return (size_t)2 * 16 * RB * FwdShape<T, RB>::P;
+}
+
+template <typename T, int RB, int OPW>
+__global__ void __launch_bounds__(NET_THREADS, RB <= 2 ? 2 : 1) net_fwd_kernel(NetFwdArgs<T> a) {
+  using Sh = FwdShape<T, RB>;
+  constexpr int RP = 16 * RB, KCH = Sh::KCH, P = Sh::P, VL = Sh::VL, EPC = Epc<T>::v;
+  constexpr int SEG = KCH / EPC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CK = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  const int scene = blockIdx.z;
-  const int n0 = blockIdx.x * NET_TILE;
+  T* Xs = reinterpret_cast<T*>(smem_raw);            // 2 x [RP][P]
+  const int scene = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rg = lane >> 3, ng = lane & 7;
-  const int RP = 16 * RB;
   const int K = a.K, N = a.N, rows = a.rows;
+  const int nbase = (blockIdx.x * (NET_THREADS / 32) + warp) * OPW;
+  // (step counter is bumped after pdl_wait: the previous backward kernels read it)
+  const T* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  const T* __restrict__ X = a.in + scene * a.in_ss;
 
-  if (a.step && tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && scene == 0) atomicAdd(a.step, 1);
-
-  T* Ws = reinterpret_cast<T*>(smem_raw);            // [TILE][KC+1]
-  T* Xs = Ws + NET_TILE * (NET_KC + 1);              // [RP][KC+1]
-  T* red = Xs + RP * (NET_KC + 1);                   // [RP][TILE] partial output
-
-  const int ks = (K + CK - 1) / CK;
-  const int kb = rank * ks, ke = min(K, kb + ks);
-  const T* W = a.theta + scene * a.th_ss + a.w_off;
-  const T* X = a.in + scene * a.in_ss;
-
-  T acc[RB][4][4];
-#pragma unroll
-  for (int b = 0; b < RB; ++b)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[b][i][j] = T(0);
-
-  for (int k0 = kb; k0 < ke; k0 += NET_KC) {
-    __syncthreads();
-    for (int idx = tid; idx < NET_TILE * NET_KC; idx += NET_THREADS) {
-      const int nn = idx / NET_KC, kk = idx % NET_KC;
-      const int gn = n0 + nn, gk = k0 + kk;
-      Ws[nn * (NET_KC + 1) + kk] = (gn < N && gk < ke) ? W[(size_t)gn * K + gk] : T(0);
+  auto stage = [&](int k0, int s) {
+    T* dst = Xs + s * RP * P;
+    for (int i = tid; i < RP * SEG; i += NET_THREADS) {
+      const int r = i / SEG, sg = i % SEG, gk = k0 + sg * EPC;
+      const bool ok = r < rows && gk < K;
+      cp_async16(dst + r * P + sg * EPC, ok ? X + (size_t)r * K + gk : X, ok);
     }
-    for (int idx = tid; idx < RP * NET_KC; idx += NET_THREADS) {
-      const int r = idx / NET_KC, kk = idx % NET_KC;
-      const int gk = k0 + kk;
-      Xs[r * (NET_KC + 1) + kk] = (r < rows && gk < ke) ? X[(size_t)r * K + gk] : T(0);
+    cp_async_commit();
+  };
+
+  T acc[OPW][RP];
+#pragma unroll
+  for (int o = 0; o < OPW; ++o)
+#pragma unroll
+    for (int r = 0; r < RP; ++r) acc[o][r] = T(0);
+
+  // this warp's weights for a chunk: lane covers k0 + lane + 32 j (coalesced
+  // global rows, conflict-free shared reads); the next chunk's weights are
+  // loaded while the current one is consumed
+  auto load_w = [&](int k0, T (&w)[OPW][VL]) {
+#pragma unroll
+    for (int o = 0; o < OPW; ++o) {
+      const int n = nbase + o;
+#pragma unroll
+      for (int j = 0; j < VL; ++j) {
+        const int kk = k0 + lane + 32 * j;
+        w[o][j] = (n < N && kk < K) ? W[(size_t)n * K + kk] : T(0);
+      }
+    }
+  };
+  constexpr bool PF = OPW == 1;      // register prefetch of the next chunk (keeps 2 CTAs/SM otherwise)
+  T w[OPW][VL], wn[PF ? OPW : 1][PF ? VL : 1];
+  if (a.w_early) load_w(0, w);
+  pdl_wait();
+  if (!a.w_early) load_w(0, w);
+  if (a.step && tid == 0 && blockIdx.x == 0 && scene == 0) atomicAdd(a.step, 1);
+  stage(0, 0);
+  int s = 0;
+  for (int k0 = 0; k0 < K; k0 += KCH, s ^= 1) {
+    if constexpr (PF) { if (k0 + KCH < K) load_w(k0 + KCH, wn); }
+    if (k0 + KCH < K) {
+      stage(k0 + KCH, s ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < NET_KC; ++kk) {
-      T wv[4];
+    const T* xs = Xs + s * RP * P + lane;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) wv[j] = Ws[(warp * 32 + ng * 4 + j) * (NET_KC + 1) + kk];
+    for (int r = 0; r < RP; ++r) {
+      T xv[VL];
 #pragma unroll
-      for (int b = 0; b < RB; ++b) {
+      for (int j = 0; j < VL; ++j) xv[j] = xs[r * P + 32 * j];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const T xv = Xs[(b * 16 + rg * 4 + i) * (NET_KC + 1) + kk];
+      for (int o = 0; o < OPW; ++o) {
+        T t = T(0);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[b][i][j] += xv * wv[j];
-        }
+        for (int j = 0; j < VL; ++j) t += xv[j] * w[o][j];
+        acc[o][r] += t;
+      }
+    }
+    if constexpr (PF) {
+#pragma unroll
+      for (int o = 0; o < OPW; ++o)
+#pragma unroll
+        for (int j = 0; j < VL; ++j) w[o][j] = wn[o][j];
+    } else {
+      if (k0 + KCH < K) load_w(k0 + KCH, w);
+    }
+    __syncthreads();   // buffer s is restaged two chunks later
+  }
+  pdl_trigger();
+  // fixed-order lane reduction; lane r ends with output row r
+#pragma unroll
+  for (int o = 0; o < OPW; ++o)
+#pragma unroll
+    for (int r = 0; r < RP; ++r) acc[o][r] = warp_sum<T>(acc[o][r]);
+
+  const T* bias = a.theta + scene * a.th_ss + a.b_off;
+#pragma unroll
+  for (int o = 0; o < OPW; ++o) {
+    const int gn = nbase + o;
+    if (gn >= N) continue;
+#pragma unroll
+    for (int r = 0; r < RP; ++r) {
+      if (r != lane && !(RP > 32 && r - 32 == lane) && !(RP > 64 && r - 64 == lane)) continue;
+      if (r >= rows) continue;
+      const T z = acc[o][r] + bias[gn];
+      if (!a.final_layer) {
+        a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+      } else {
+        const T yv = z * a.cout[(size_t)scene * N + gn];
+        // [Re | Im] feature layout (network.py:123-136)
+        const int half = N / 2;
+        const int f = gn < half ? gn : gn - half;
+        int view, m;
+        if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
+        const size_t off = ((size_t)scene * a.n + view) * a.M0 + m;
+        T* dst = reinterpret_cast<T*>(a.alpha_hat + off);
+        const T* src = reinterpret_cast<const T*>(a.alpha0 + off);
+        if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
       }
     }
   }
-#pragma unroll
-  for (int b = 0; b < RB; ++b)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) red[(b * 16 + rg * 4 + i) * NET_TILE + warp * 32 + ng * 4 + j] = acc[b][i][j];
-  cluster.sync();
-
-  // reduce-scatter over the cluster, fixed rank order, then the epilogue
-  const T* bias = a.theta + scene * a.th_ss + a.b_off;
-  const int total = rows * NET_TILE;
-  for (int e = rank + CK * tid; e < total; e += CK * NET_THREADS) {
-    const int r = e / NET_TILE, nn = e % NET_TILE, gn = n0 + nn;
-    if (gn >= N) continue;
-    T s = T(0);
-    for (int c = 0; c < CK; ++c) s += cluster.map_shared_rank(red, c)[r * NET_TILE + nn];
-    const T z = s + bias[gn];
-    if (!a.final_layer) {
-      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
-    } else {
-      const T yv = z * a.cout[(size_t)scene * N + gn];
-      // [Re | Im] feature layout (network.py:123-136)
-      const int half = N / 2;
-      const int f = gn < half ? gn : gn - half;
-      int view, m;
-      if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
-      const size_t o = ((size_t)scene * a.n + view) * a.M0 + m;
-      T* dst = reinterpret_cast<T*>(a.alpha_hat + o);
-      const T* src = reinterpret_cast<const T*>(a.alpha0 + o);
-      if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
-    }
-  }
-  cluster.sync();
 }
 
 template <typename T>
@@ -147,185 +188,247 @@ struct NetBwdArgs {
   long long w_off, b_off;
   T* m; T* v;                         // Adam moments, same layout as theta
   T* grad;                            // [S][Np] gradient out (unfused mode) or null
-  int fused;                          // 1: apply Adam, 0: write grad
   const int* step;                    // Adam t (device)
   T lr, b1, b2, eps;
   T* gzprev; long long gzp_ss;        // [S][rows][K] or null (first layer)
   int* err;                           // [S]
 };
 
+// Adam in the reference's operation order (network.py:252-257).  The bias
+// corrections are applied as products with 1/(1-b^t) and the remaining
+// division and square root use hardware approximations refined by Newton
+// steps: agreement with the IEEE sequence to ~1 ulp, at a fraction of the
+// instruction count of the library routines (whose slow paths dominated).
+__device__ __forceinline__ double rcp_nr(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  double e = fma(-y, r, 1.0);   // the approximation is good to ~2^-23: two steps reach 2^-92
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double div_nr(double x, double y) {
+  const double r = rcp_nr(y);
+  const double q = x * r;
+  return fma(r, fma(-y, q, x), q);
+}
+__device__ __forceinline__ double sqrt_nr(double v) {
+  if (!(v > 0.0)) return v == 0.0 ? 0.0 : sqrt(v);   // 0, negative, NaN: exact IEEE semantics
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(v));
+  const double hv = 0.5 * v;
+  r = r * fma(-hv * r, r, 1.5);
+  r = r * fma(-hv * r, r, 1.5);
+  const double s = v * r;
+  return fma(0.5 * r, fma(-s, s, v), s);
+}
+__device__ __forceinline__ float div_nr(float x, float y) { return x / y; }
+__device__ __forceinline__ float sqrt_nr(float v) { return sqrtf(v); }
+
 template <typename T>
-__device__ __forceinline__ void adam_one(T& p, T& m, T& v, T g, T lr, T b1, T b2, T eps, T bc1, T bc2) {
+__device__ __forceinline__ void adam_one(T& p, T& m, T& v, T g, T lr, T b1, T b2, T eps, T ibc1, T ibc2) {
   m = b1 * m + (T(1) - b1) * g;
   v = b2 * v + (T(1) - b2) * g * g;
-  const T mh = m / bc1;
-  const T vh = v / bc2;
-  p = p - lr * mh / (sqrt_<T>(vh) + eps);
+  const T mh = m * ibc1;
+  const T vh = v * ibc2;
+  p = p - div_nr(lr * mh, sqrt_nr(vh) + eps);
 }
 
-// thread (warp w, lane): gh micro-tile rows rb*16 + (lane>>3)*4 + i, columns (lane&7)*4 + j + 32*w
+constexpr int BWD_COLS = 8;                          // input columns per CTA
+constexpr int BWD_SUB = NET_THREADS / BWD_COLS;      // row subsets per CTA (32)
+constexpr int BWD_UR = 4;                            // rows per thread per step (ILP)
+constexpr int BWD_NCH = BWD_SUB * BWD_UR;            // rows of g_z staged per step (128)
+
+template <typename T, int RB> struct BwdShape {
+  static constexpr bool HREG = RB <= 2;              // h / g_h partial in registers
+  static constexpr int GP = BWD_NCH + Epc<T>::v;      // padded pitch of the staged g_z rows
+};
+
 template <typename T, int RB>
-__global__ void __launch_bounds__(NET_THREADS) net_bwd_kernel(NetBwdArgs<T> a) {
+__host__ __device__ constexpr size_t bwd_smem_elems() {
+  constexpr int RP = 16 * RB;
+  return (size_t)2 * RP * BwdShape<T, RB>::GP + (size_t)BWD_SUB * 16 * BWD_COLS +
+         (BwdShape<T, RB>::HREG ? 0 : (size_t)2 * RP * NET_THREADS);
+}
+
+template <typename T, int RB, bool FUSED>
+__global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(NetBwdArgs<T> a) {
+  using Sh = BwdShape<T, RB>;
+  constexpr int RP = 16 * RB, EPC = Epc<T>::v, GP = Sh::GP;
+  constexpr bool HREG = Sh::HREG;
+  constexpr int SEG = BWD_NCH / EPC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int CN = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
-  const int scene = blockIdx.z;
-  const int k0 = blockIdx.x * NET_TILE;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rg = lane >> 3, cg_ = lane & 7;
-  const int RP = 16 * RB;
+  T* Gs = reinterpret_cast<T*>(smem_raw);            // 2 x [RP][GP]   g_z[r][n0 + i]
+  T* red = Gs + 2 * RP * GP;                         // [BWD_SUB][16][BWD_COLS] reduction scratch
+  T* Hs = red + BWD_SUB * 16 * BWD_COLS;             // [RP][NET_THREADS] when !HREG
+  T* GHs = Hs + RP * NET_THREADS;                    // [RP][NET_THREADS] when !HREG
+  __shared__ T bc_s[2];
+  const int scene = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int col = tid % BWD_COLS, sub = tid / BWD_COLS;
+  const int k = blockIdx.x * BWD_COLS + col;
   const int K = a.K, N = a.N, rows = a.rows;
+  const bool kok = k < K;
 
-  T* Hs = reinterpret_cast<T*>(smem_raw);       // [RP][TILE]
-  T* Ws = Hs + RP * NET_TILE;                   // [KC][TILE]
-  T* Gs = Ws + NET_KC * NET_TILE;               // [RP][KC+1]
-  T* red = Gs + RP * (NET_KC + 1);              // [RP][TILE]
+  const T* __restrict__ hin = a.hin + scene * a.hin_ss;
+  const T* __restrict__ gz = a.gz + scene * a.gz_ss;
+  T* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  T* __restrict__ mW = FUSED ? a.m + scene * a.th_ss + a.w_off : nullptr;
+  T* __restrict__ vW = FUSED ? a.v + scene * a.th_ss + a.w_off : nullptr;
+  T* __restrict__ gW = FUSED ? nullptr : a.grad + scene * a.th_ss + a.w_off;
 
-  const T* hin = a.hin + scene * a.hin_ss;
-  const T* gz = a.gz + scene * a.gz_ss;
-  T* th = a.theta + scene * a.th_ss;
-  T* W = th + a.w_off;
-  T* bia = th + a.b_off;
-  T* mW = a.m + scene * a.th_ss + a.w_off;
-  T* vW = a.v + scene * a.th_ss + a.w_off;
-  T* mb = a.m + scene * a.th_ss + a.b_off;
-  T* vb = a.v + scene * a.th_ss + a.b_off;
-  T* gW = a.grad ? a.grad + scene * a.th_ss + a.w_off : nullptr;
-  T* gB = a.grad ? a.grad + scene * a.th_ss + a.b_off : nullptr;
+  auto stage = [&](int n0, int s) {
+    T* dst = Gs + s * RP * GP;
+    for (int i = tid; i < RP * SEG; i += NET_THREADS) {
+      const int r = i / SEG, sg = i % SEG, gn = n0 + sg * EPC;
+      const bool ok = r < rows && gn < N;
+      cp_async16(dst + r * GP + sg * EPC, ok ? gz + (size_t)r * N + gn : gz, ok);
+    }
+    cp_async_commit();
+  };
 
-  T bc1 = T(1), bc2 = T(1);
-  if (a.fused) {
-    const int t = *a.step;
-    bc1 = T(1.0 - pow((double)a.b1, (double)t));
-    bc2 = T(1.0 - pow((double)a.b2, (double)t));
+  if (tid == 0) {
+    if (FUSED) {
+      const int t = *a.step;
+      bc_s[0] = T(1.0 / (1.0 - pow((double)a.b1, (double)t)));
+      bc_s[1] = T(1.0 / (1.0 - pow((double)a.b2, (double)t)));
+    } else {
+      bc_s[0] = bc_s[1] = T(1);
+    }
   }
-
-  for (int idx = tid; idx < RP * NET_TILE; idx += NET_THREADS) {
-    const int r = idx / NET_TILE, kk = idx % NET_TILE, gk = k0 + kk;
-    Hs[idx] = (r < rows && gk < K) ? hin[(size_t)r * K + gk] : T(0);
+  T h[HREG ? RP : 1], gh[HREG ? RP : 1];
+#pragma unroll(HREG ? RP : 4)
+  for (int r = 0; r < RP; ++r) {
+    const T hv = (kok && r < rows) ? hin[(size_t)r * K + k] : T(0);
+    if constexpr (HREG) { h[r] = hv; gh[r] = T(0); }
+    else { Hs[r * NET_THREADS + tid] = hv; GHs[r * NET_THREADS + tid] = T(0); }
   }
-
-  const int ns = (N + CN - 1) / CN;
-  const int nb = rank * ns, ne = min(N, nb + ns);
-
-  T acc[RB][4][4];
+  // this thread's rows of a step: n0 + sub + BWD_SUB*u.  W, m, v of the first
+  // step are final since the previous iteration, so they are loaded before
+  // pdl_wait; later steps are prefetched one step ahead (register double
+  // buffer where the register budget allows it).
+  constexpr bool DB = !HREG;
+  auto load_step = [&](int n0, T (&w_)[BWD_UR], T (&m_)[BWD_UR], T (&v_)[BWD_UR]) {
 #pragma unroll
-  for (int b = 0; b < RB; ++b)
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[b][i][j] = T(0);
-
+    for (int u = 0; u < BWD_UR; ++u) {
+      const int n = n0 + sub + BWD_SUB * u;
+      const bool ok = kok && n < N;
+      const size_t o = (size_t)n * K + k;
+      w_[u] = ok ? W[o] : T(0);
+      if constexpr (FUSED) {
+        m_[u] = ok ? mW[o] : T(0);
+        v_[u] = ok ? vW[o] : T(0);
+      }
+    }
+  };
   int errbits = 0;
-  for (int c0 = nb; c0 < ne; c0 += NET_KC) {
+  int s = 0;
+  T wv[BWD_UR], mv[BWD_UR], vv[BWD_UR];
+  load_step(0, wv, mv, vv);
+  pdl_wait();
+  stage(0, 0);
+  for (int n0 = 0; n0 < N; n0 += BWD_NCH, s ^= 1) {
+    T wn[DB ? BWD_UR : 1], mn[DB ? BWD_UR : 1], vn[DB ? BWD_UR : 1];
+    if constexpr (DB) {
+      if (n0 + BWD_NCH < N) load_step(n0 + BWD_NCH, wn, mn, vn);
+    }
+    if (n0 + BWD_NCH < N) {
+      stage(n0 + BWD_NCH, s ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    for (int idx = tid; idx < NET_KC * NET_TILE; idx += NET_THREADS) {
-      const int nn = idx / NET_TILE, kk = idx % NET_TILE;
-      const int gn = c0 + nn, gk = k0 + kk;
-      Ws[idx] = (gn < ne && gk < K) ? W[(size_t)gn * K + gk] : T(0);
-    }
-    for (int idx = tid; idx < RP * NET_KC; idx += NET_THREADS) {
-      const int r = idx / NET_KC, nn = idx % NET_KC, gn = c0 + nn;
-      Gs[r * (NET_KC + 1) + nn] = (r < rows && gn < ne) ? gz[(size_t)r * N + gn] : T(0);
-    }
-    __syncthreads();
-    // g_h partial with the old weights
-#pragma unroll 4
-    for (int nn = 0; nn < NET_KC; ++nn) {
-      T wv[4];
+    const T* G = Gs + s * RP * GP;
+    const T ibc1 = bc_s[0], ibc2 = bc_s[1];
+    T gw[BWD_UR];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) wv[j] = Ws[nn * NET_TILE + warp * 32 + cg_ * 4 + j];
+    for (int u = 0; u < BWD_UR; ++u) gw[u] = T(0);
+#pragma unroll(HREG ? RP : 4)
+    for (int r = 0; r < RP; ++r) {
+      const T hr = HREG ? h[r] : Hs[r * NET_THREADS + tid];
+      T ghs = T(0);
 #pragma unroll
-      for (int b = 0; b < RB; ++b)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const T gv = Gs[(b * 16 + rg * 4 + i) * (NET_KC + 1) + nn];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[b][i][j] += gv * wv[j];
-        }
-    }
-    // weight gradient + Adam for the chunk: thread owns n = c0 + warp*4 + i (i<4),
-    // k = k0 + lane + 32*j (j<4) so each warp touches contiguous rows of m, v, W
-    {
-      T g[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) g[i][j] = T(0);
-      for (int r = 0; r < rows; ++r) {
-        T hv[4], gv[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) hv[j] = Hs[r * NET_TILE + lane + 32 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) gv[i] = Gs[r * (NET_KC + 1) + warp * 4 + i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) g[i][j] += gv[i] * hv[j];
+      for (int u = 0; u < BWD_UR; ++u) {
+        const T g = G[r * GP + sub + BWD_SUB * u];
+        gw[u] += g * hr;
+        ghs += g * wv[u];
       }
+      if constexpr (HREG) gh[r] += ghs; else GHs[r * NET_THREADS + tid] += ghs;
+    }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int gn = c0 + warp * 4 + i;
-        if (gn >= ne) continue;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int gk = k0 + lane + 32 * j;
-          if (gk >= K) continue;
-          const size_t o = (size_t)gn * K + gk;
-          const T gg = g[i][j];
-          if (!isfinite(gg)) errbits |= ERR_NONFINITE_GRAD;
-          if (a.fused) {
-            T p = Ws[(warp * 4 + i) * NET_TILE + lane + 32 * j];
-            T mm = mW[o], vv = vW[o];
-            adam_one<T>(p, mm, vv, gg, a.lr, a.b1, a.b2, a.eps, bc1, bc2);
-            if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
-            W[o] = p; mW[o] = mm; vW[o] = vv;
-          } else {
-            gW[o] = gg;
-          }
-        }
-      }
-      // bias: owned by the first column tile
-      if (blockIdx.x == 0 && tid < NET_KC) {
-        const int gn = c0 + tid;
-        if (gn < ne) {
-          T gb = T(0);
-          for (int r = 0; r < rows; ++r) gb += Gs[r * (NET_KC + 1) + tid];
-          if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
-          if (a.fused) {
-            T p = bia[gn], mm = mb[gn], vv = vb[gn];
-            adam_one<T>(p, mm, vv, gb, a.lr, a.b1, a.b2, a.eps, bc1, bc2);
-            if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
-            bia[gn] = p; mb[gn] = mm; vb[gn] = vv;
-          } else {
-            gB[gn] = gb;
-          }
-        }
+    for (int u = 0; u < BWD_UR; ++u) {
+      const int n = n0 + sub + BWD_SUB * u;
+      if (!kok || n >= N) continue;
+      const size_t o = (size_t)n * K + k;
+      if (!isfinite(gw[u])) errbits |= ERR_NONFINITE_GRAD;
+      if constexpr (FUSED) {
+        T p = wv[u], mm = mv[u], vq = vv[u];
+        adam_one<T>(p, mm, vq, gw[u], a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
+        W[o] = p; mW[o] = mm; vW[o] = vq;
+      } else {
+        gW[o] = gw[u];
       }
     }
+    // bias (network.py:213,217): gb[n] = sum_r g_z[r, n], owned by the first column tile
+    if (blockIdx.x == 0 && tid < BWD_NCH && n0 + tid < N) {
+      T gb = T(0);
+      for (int r = 0; r < rows; ++r) gb += G[r * GP + tid];
+      const int gn = n0 + tid;
+      if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
+      if constexpr (FUSED) {
+        T* th = a.theta + scene * a.th_ss + a.b_off;
+        T* mb = a.m + scene * a.th_ss + a.b_off;
+        T* vb = a.v + scene * a.th_ss + a.b_off;
+        T p = th[gn], mm = mb[gn], vq = vb[gn];
+        adam_one<T>(p, mm, vq, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
+        th[gn] = p; mb[gn] = mm; vb[gn] = vq;
+      } else {
+        a.grad[scene * a.th_ss + a.b_off + gn] = gb;
+      }
+    }
+    if constexpr (DB) {
+#pragma unroll
+      for (int u = 0; u < BWD_UR; ++u) { wv[u] = wn[u]; mv[u] = mn[u]; vv[u] = vn[u]; }
+    } else {
+      if (n0 + BWD_NCH < N) load_step(n0 + BWD_NCH, wv, mv, vv);
+    }
+    __syncthreads();   // buffer s is restaged two steps later
   }
+  pdl_trigger();
   if (errbits) atomicOr(&a.err[scene], errbits);
 
   if (a.gzprev) {
+    // g_h[r][k] = sum over the 32 row subsets (fixed order), 16 rows at a time
 #pragma unroll
-    for (int b = 0; b < RB; ++b)
+    for (int rb = 0; rb < RP; rb += 16) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 16; ++j) {
+        const int r = rb + j;
+        T v_;
+        if constexpr (HREG) {
+          v_ = T(0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          red[(b * 16 + rg * 4 + i) * NET_TILE + warp * 32 + cg_ * 4 + j] = acc[b][i][j];
-    cluster.sync();
-    const int total = rows * NET_TILE;
-    for (int e = rank + CN * tid; e < total; e += CN * NET_THREADS) {
-      const int r = e / NET_TILE, kk = e % NET_TILE, gk = k0 + kk;
-      if (gk >= K) continue;
-      T s = T(0);
-      for (int c = 0; c < CN; ++c) s += cluster.map_shared_rank(red, c)[r * NET_TILE + kk];
-      const T h = Hs[r * NET_TILE + kk];
-      a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = s * (T(1) - h * h);
+          for (int q = 0; q < RP; ++q) if (q == r) v_ = gh[q];
+        } else {
+          v_ = GHs[r * NET_THREADS + tid];
+        }
+        red[(sub * 16 + j) * BWD_COLS + col] = v_;
+      }
+      __syncthreads();
+      if (tid < 16 * BWD_COLS) {
+        const int j = tid / BWD_COLS, c = tid % BWD_COLS, r = rb + j, gk = blockIdx.x * BWD_COLS + c;
+        T sum = T(0);
+        for (int q = 0; q < BWD_SUB; ++q) sum += red[(q * 16 + j) * BWD_COLS + c];
+        if (r < rows && gk < K) {
+          const T hv = hin[(size_t)r * K + gk];
+          a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = sum * (T(1) - hv * hv);
+        }
+      }
+      __syncthreads();
     }
-    cluster.sync();
   }
 }
 

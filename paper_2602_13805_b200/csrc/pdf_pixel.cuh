@@ -15,7 +15,10 @@
 // incidences i = w, w+NW, ...; lane = column inside the tile, so every global
 // access is a coalesced row segment.  The regulariser stencils need chi on a
 // one-pixel halo, which the CTA recomputes (rows y-1..y+1) instead of a
-// separate launch.  All cross-view sums are fixed-order (deterministic).
+// separate launch; the stencil terms of rows y-1 and y are computed once per
+// halo pixel by parallel threads.  The G_S columns of the tile and the
+// scene's g_rows are staged in shared memory with cp.async while the halo is
+// processed.  All cross-view sums are fixed-order (deterministic).
 #pragma once
 #include "pdf_common.cuh"
 
@@ -40,61 +43,66 @@ struct PixelArgs {
 };
 
 constexpr double EPS_TV = 1e-12;   // losses.py:29
+constexpr int PIX_TX = 32;         // max tile width
+constexpr int PIX_NW = 8;          // warps per CTA
 
 template <typename T>
-struct Nb {  // chi at a 3-row halo of the tile; NaN-free "outside" handled by flags
-  const C<T>* chi;
-  int W, x0, y, M;
-  __device__ C<T> at(int yy, int xx) const {
-    return chi[(yy - y + 1) * W + (xx - x0 + 1)];
-  }
-};
-
-template <typename T>
-__device__ inline void tv_terms(const Nb<T>& nb, int yy, int xx, C<T>& dx, C<T>& dy, T& s) {
-  const int M = nb.M;
-  const C<T> c = nb.at(yy, xx);
-  dx = (xx + 1 < M) ? csub<T>(nb.at(yy, xx + 1), c) : czero<T>();
-  dy = (yy + 1 < M) ? csub<T>(nb.at(yy + 1, xx), c) : czero<T>();
-  s = sqrt_<T>(cabs2<T>(dx) + cabs2<T>(dy) + T(EPS_TV));
+__host__ __device__ inline size_t pixel_smem_bytes(int n, int R) {
+  // gs tile [R][TX] + g_rows [n][R]
+  return ((size_t)R * PIX_TX + (size_t)n * R) * sizeof(C<T>);
 }
 
 template <typename T>
-__device__ inline T amag(C<T> z) { return sqrt_<T>(cabs2<T>(z)); }
-
-template <typename T>
-__device__ inline void bridge_terms(const Nb<T>& nb, int yy, int xx, T tau, T& sig, T& damp, T& gx, T& gy) {
-  const int M = nb.M;
-  const T a = amag<T>(nb.at(yy, xx));
-  gx = (xx + 1 < M) ? amag<T>(nb.at(yy, xx + 1)) - a : T(0);
-  gy = (yy + 1 < M) ? amag<T>(nb.at(yy + 1, xx)) - a : T(0);
-  sig = sigmoid_<T>((a - tau) / tau);
-  damp = exp_<T>(-(gx * gx + gy * gy));
-}
+__device__ __forceinline__ T amag(C<T> z) { return sqrt_<T>(cabs2<T>(z)); }
 
 template <typename T, bool GRAD>
-__global__ void __launch_bounds__(256) pixel_kernel(PixelArgs<T> a) {
-  constexpr int MAXTX = 32;
-  constexpr int MAXW = 8;
-  __shared__ C<T> pnum[MAXW][3 * (MAXTX + 2)];
-  __shared__ T pden[MAXW][3 * (MAXTX + 2)];
-  __shared__ C<T> chis[3 * (MAXTX + 2)];
-  __shared__ T dens[MAXTX];
-  __shared__ C<T> Rs[MAXTX], chain[MAXTX], greg[MAXTX], gnum[MAXTX];
-  __shared__ T gden[MAXTX];
-  __shared__ C<T> pgr[MAXW][MAXTX];
-  __shared__ double red[MAXW][4];
+__global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
+  constexpr int W = PIX_TX + 2;
+  __shared__ C<T> pnum[PIX_NW][3 * W];
+  __shared__ T pden[PIX_NW][3 * W];
+  __shared__ C<T> chis[3 * W];
+  // stencil terms for rows y-1 (index 0) and y (index 1) over columns x0-1 .. x0+TX
+  __shared__ C<T> twx[2][W], twy[2][W];       // tv weights dx/s, dy/s
+  __shared__ T ts[2][W];                      // tv value s
+  __shared__ T bsig[2][W], bdamp[2][W], bcx[2][W], bcy[2][W];
+  __shared__ T dens[PIX_TX];
+  __shared__ C<T> Rs[PIX_TX], chain[PIX_TX], greg[PIX_TX], gnum[PIX_TX];
+  __shared__ T gden[PIX_TX];
+  __shared__ C<T> pgr[PIX_NW][PIX_TX];
+  __shared__ double red[PIX_NW][4];
   __shared__ double eps_s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C<T>* gsS = reinterpret_cast<C<T>*>(smem_raw);     // [R][TX]
+  C<T>* grS = gsS + (size_t)a.R * PIX_TX;             // [n][R]
 
-  const int M = a.M, n = a.n;
-  const int TX = M < MAXTX ? M : MAXTX;
-  const int W = TX + 2;
-  const int NH = 3 * W;
+  const int M = a.M, n = a.n, R = a.R;
+  const int TX = M < PIX_TX ? M : PIX_TX;
+  const int NH = 3 * (TX + 2);
+  const int WW = TX + 2;
   const int tilesx = M / TX;
   const int x0 = blockIdx.x * TX, y = blockIdx.y, scene = blockIdx.z;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const size_t img = (size_t)M * M;
   const size_t vbase = (size_t)scene * n;
+
+  if constexpr (GRAD) {
+    // stage this tile's G_S columns and the scene's g_rows (consumed at the end)
+    constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
+    const int segs = TX / EPC;
+    for (int i = tid; i < R * segs; i += blockDim.x) {
+      const int r = i / segs, sg = i % segs;
+      cp_async16(gsS + r * PIX_TX + sg * EPC, a.gs + (size_t)r * img + (size_t)y * M + x0 + sg * EPC, true);
+    }
+    cp_async_commit();
+  }
+  pdl_wait();   // J, E, norms, g_rows come from the previous kernel
+  if constexpr (GRAD) {
+    constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
+    const int gseg = (n * R) / EPC;
+    for (int i = tid; i < gseg; i += blockDim.x)
+      cp_async16(grS + i * EPC, a.grows + vbase * R + i * EPC, true);
+    cp_async_commit();
+  }
 
   if (tid == 0) {
     double mx = 0.0;
@@ -108,7 +116,7 @@ __global__ void __launch_bounds__(256) pixel_kernel(PixelArgs<T> a) {
 
   // ---- per-warp partial num/den on the halo --------------------------------
   for (int h = lane; h < NH; h += 32) {
-    const int hy = y - 1 + h / W, hx = x0 - 1 + h % W;
+    const int hy = y - 1 + h / WW, hx = x0 - 1 + h % WW;
     C<T> num = czero<T>();
     T den = T(0);
     if (hy >= 0 && hy < M && hx >= 0 && hx < M) {
@@ -131,77 +139,82 @@ __global__ void __launch_bounds__(256) pixel_kernel(PixelArgs<T> a) {
     for (int w = 0; w < nw; ++w) { num = cadd<T>(num, pnum[w][h]); den += pden[w][h]; }
     den += eps;
     chis[h] = mk<T>(num.x / den, num.y / den);   // numpy complex/real division
-    if (h / W == 1 && (h % W) >= 1 && (h % W) <= TX) dens[h % W - 1] = den;
+    if (h / WW == 1 && (h % WW) >= 1 && (h % WW) <= TX) dens[h % WW - 1] = den;
   }
   __syncthreads();
 
-  // ---- per-pixel scalar work (warp 0) -------------------------------------
+  // ---- stencil terms at rows y-1, y (forward differences, losses.py:139-144)
+  const T tau = a.tau;
+  for (int q = tid; q < 2 * WW; q += blockDim.x) {
+    const int row = q / WW, cix = q % WW;           // row 0: y-1, row 1: y
+    const int yy = y - 1 + row, xx = x0 - 1 + cix;
+    C<T> wx = czero<T>(), wy = czero<T>();
+    T s = T(0), sig = T(0), damp = T(0), cx = T(0), cy = T(0);
+    if (yy >= 0 && yy < M && xx >= 0 && xx < M) {
+      const C<T> c = chis[row * WW + cix];
+      const C<T> dx = (xx + 1 < M) ? csub<T>(chis[row * WW + cix + 1], c) : czero<T>();
+      const C<T> dy = (yy + 1 < M) ? csub<T>(chis[(row + 1) * WW + cix], c) : czero<T>();
+      s = sqrt_<T>(cabs2<T>(dx) + cabs2<T>(dy) + T(EPS_TV));
+      wx = mk<T>(dx.x / s, dx.y / s);
+      wy = mk<T>(dy.x / s, dy.y / s);
+      const T am = amag<T>(c);
+      const T gx = (xx + 1 < M) ? amag<T>(chis[row * WW + cix + 1]) - am : T(0);
+      const T gy = (yy + 1 < M) ? amag<T>(chis[(row + 1) * WW + cix]) - am : T(0);
+      sig = sigmoid_<T>((am - tau) / tau);
+      damp = exp_<T>(-(gx * gx + gy * gy));
+      cx = T(-2) * sig * damp * gx;
+      cy = T(-2) * sig * damp * gy;
+    }
+    twx[row][cix] = wx; twy[row][cix] = wy; ts[row][cix] = s;
+    bsig[row][cix] = sig; bdamp[row][cix] = damp; bcx[row][cix] = cx; bcy[row][cix] = cy;
+  }
+  __syncthreads();
+
+  // ---- per-pixel scalar work ------------------------------------------------
   double vb = 0.0, vt = 0.0, vr = 0.0;
-  if (warp == 0 && lane < TX) {
-    const int x = x0 + lane;
-    Nb<T> nb{chis, W, x0, y, M};
-    const C<T> chi = nb.at(y, x);
-    const T tau = a.tau;
-    // values (losses.py:115-136)
+  if (tid < TX) {
+    const int x = x0 + tid, c1 = tid + 1;            // column index of x in the halo arrays
+    const C<T> chi = chis[WW + c1];
     const T neg = chi.x < T(0) ? chi.x : T(0);
     vb = (double)(neg * neg);
-    C<T> dx, dy; T s;
-    tv_terms<T>(nb, y, x, dx, dy, s);
-    vt = (double)s;
-    T sig, damp, gx, gy;
-    bridge_terms<T>(nb, y, x, tau, sig, damp, gx, gy);
-    vr = (double)(sig * damp);
+    vt = (double)ts[1][c1];
+    vr = (double)(bsig[1][c1] * bdamp[1][c1]);
     if (a.chi_out) a.chi_out[(size_t)scene * img + (size_t)y * M + x] = chi;
     if (GRAD) {
       C<T> g = czero<T>();
       if (a.l1 != T(0)) g = cadd<T>(g, mk<T>(a.l1 * (T(2) * neg), T(0)));
       if (a.l2 != T(0)) {
-        C<T> gt = mk<T>(-dx.x / s - dy.x / s, -dx.y / s - dy.y / s);
-        if (x >= 1) {
-          C<T> dx2, dy2; T s2;
-          tv_terms<T>(nb, y, x - 1, dx2, dy2, s2);
-          gt = cadd<T>(gt, mk<T>(dx2.x / s2, dx2.y / s2));
-        }
-        if (y >= 1) {
-          C<T> dx2, dy2; T s2;
-          tv_terms<T>(nb, y - 1, x, dx2, dy2, s2);
-          gt = cadd<T>(gt, mk<T>(dy2.x / s2, dy2.y / s2));
-        }
+        // g += wx(y, x-1) - wx(y, x) + wy(y-1, x) - wy(y, x)   (losses.py:156-165)
+        C<T> gt = mk<T>(-twx[1][c1].x - twy[1][c1].x, -twx[1][c1].y - twy[1][c1].y);
+        if (x >= 1) gt = cadd<T>(gt, twx[1][c1 - 1]);
+        if (y >= 1) gt = cadd<T>(gt, twy[0][c1]);
         g = cadd<T>(g, cscale<T>(gt, a.l2));
       }
       if (a.l3 != T(0)) {
-        T ga = sig * (T(1) - sig) / tau * damp;
-        ga -= T(-2) * sig * damp * gx;
-        ga -= T(-2) * sig * damp * gy;
-        if (x >= 1) {
-          T s2, d2, gx2, gy2;
-          bridge_terms<T>(nb, y, x - 1, tau, s2, d2, gx2, gy2);
-          ga += T(-2) * s2 * d2 * gx2;
-        }
-        if (y >= 1) {
-          T s2, d2, gx2, gy2;
-          bridge_terms<T>(nb, y - 1, x, tau, s2, d2, gx2, gy2);
-          ga += T(-2) * s2 * d2 * gy2;
-        }
+        // (losses.py:168-182)
+        const T sg = bsig[1][c1];
+        T ga = sg * (T(1) - sg) / tau * bdamp[1][c1];
+        ga -= bcx[1][c1];
+        ga -= bcy[1][c1];
+        if (x >= 1) ga += bcx[1][c1 - 1];
+        if (y >= 1) ga += bcy[0][c1];
         const T am = amag<T>(chi);
-        C<T> ph = am > T(0) ? mk<T>(chi.x / am, chi.y / am) : czero<T>();
+        const C<T> ph = am > T(0) ? mk<T>(chi.x / am, chi.y / am) : czero<T>();
         g = cadd<T>(g, cscale<T>(ph, a.l3 * ga));
       }
-      greg[lane] = g;
+      greg[tid] = g;
     }
-    C<T> R;
+    C<T> R_;
     if (a.rfixed) {
-      R = a.rfixed[(size_t)scene * img + (size_t)y * M + x];
-      chain[lane] = czero<T>();
+      R_ = a.rfixed[(size_t)scene * img + (size_t)y * M + x];
+      chain[tid] = czero<T>();
     } else {
       const C<T> q = mk<T>(a.beta * chi.x + T(1), a.beta * chi.y);
       if (sqrt_<T>(cabs2<T>(q)) < T(1e-14)) atomicOr(&a.err[scene], ERR_POLE);
-      R = cdiv<T>(mk<T>(a.beta * chi.x, a.beta * chi.y), q);
-      // conj(beta / q^2)
-      const C<T> q2 = cmul<T>(q, q);
-      chain[lane] = conj_<T>(cdiv<T>(mk<T>(a.beta, T(0)), q2));
+      R_ = cdiv<T>(mk<T>(a.beta * chi.x, a.beta * chi.y), q);
+      chain[tid] = conj_<T>(cdiv<T>(mk<T>(a.beta, T(0)), cmul<T>(q, q)));   // conj(beta / q^2)
     }
-    Rs[lane] = R;
+    Rs[tid] = R_;
   }
   __syncthreads();
 
@@ -210,37 +223,37 @@ __global__ void __launch_bounds__(256) pixel_kernel(PixelArgs<T> a) {
   const T gsc = T(2.0 / a.c_inc[scene]);
   double vs = 0.0;
   if (lane < TX) {
-    const int x = x0 + lane;
-    const size_t pix = (size_t)y * M + x;
-    const C<T> R = Rs[lane];
+    const size_t pix = (size_t)y * M + x0 + lane;
+    const C<T> R_ = Rs[lane];
     C<T> gr = czero<T>();
     for (int i = warp; i < n; i += nw) {
       const C<T> j = a.J[(vbase + i) * img + pix];
       const C<T> e = a.E[(vbase + i) * img + pix];
       const C<T> P = mk<T>(e.x + beta * j.x, e.y + beta * j.y);
-      const C<T> Sr = csub<T>(cmul<T>(R, P), mk<T>(beta * j.x, beta * j.y));
+      const C<T> Sr = csub<T>(cmul<T>(R_, P), mk<T>(beta * j.x, beta * j.y));
       vs += (double)cabs2<T>(Sr);
       if (GRAD) gr = cadd<T>(gr, cmulc<T>(cscale<T>(Sr, gsc), P));   // conj(P) g_S
     }
     if (GRAD) pgr[warp][lane] = gr;
   }
+  pdl_trigger();
   if (GRAD) {
     __syncthreads();
-    if (warp == 0 && lane < TX) {
+    if (tid < TX) {
       C<T> gr = czero<T>();
-      for (int w = 0; w < nw; ++w) gr = cadd<T>(gr, pgr[w][lane]);
-      const C<T> chi = chis[W + 1 + lane];
-      C<T> gchi = greg[lane];
-      if (!a.rfixed) gchi = cadd<T>(gchi, cmul<T>(chain[lane], gr));
-      const T den = dens[lane];
-      gnum[lane] = mk<T>(gchi.x / den, gchi.y / den);
-      gden[lane] = -(gchi.x * chi.x + gchi.y * chi.y) / den;   // -Re(conj(g_chi) chi)/den
+      for (int w = 0; w < nw; ++w) gr = cadd<T>(gr, pgr[w][tid]);
+      const C<T> chi = chis[WW + 1 + tid];
+      C<T> gchi = greg[tid];
+      if (!a.rfixed) gchi = cadd<T>(gchi, cmul<T>(chain[tid], gr));
+      const T den = dens[tid];
+      gnum[tid] = mk<T>(gchi.x / den, gchi.y / den);
+      gden[tid] = -(gchi.x * chi.x + gchi.y * chi.y) / den;   // -Re(conj(g_chi) chi)/den
     }
+    cp_async_wait<0>();
     __syncthreads();
     if (lane < TX) {
-      const int x = x0 + lane;
-      const size_t pix = (size_t)y * M + x;
-      const C<T> R = Rs[lane];
+      const size_t pix = (size_t)y * M + x0 + lane;
+      const C<T> R_ = Rs[lane];
       const C<T> gn = gnum[lane];
       const T gd = gden[lane];
       for (int i = warp; i < n; i += nw) {
@@ -248,15 +261,20 @@ __global__ void __launch_bounds__(256) pixel_kernel(PixelArgs<T> a) {
         const C<T> j = a.J[o];
         const C<T> e = a.E[o];
         const C<T> P = mk<T>(e.x + beta * j.x, e.y + beta * j.y);
-        const C<T> Sr = csub<T>(cmul<T>(R, P), mk<T>(beta * j.x, beta * j.y));
+        const C<T> Sr = csub<T>(cmul<T>(R_, P), mk<T>(beta * j.x, beta * j.y));
         const C<T> gS = cscale<T>(Sr, gsc);
-        const C<T> gP = cmul<T>(conj_<T>(R), gS);
+        const C<T> gP = cmul<T>(conj_<T>(R_), gS);
         C<T> gj = cscale<T>(csub<T>(gP, gS), beta);
-        // G_S^H g_rows at this pixel (forward.py:303-306)
-        const C<T>* gr = a.grows + (vbase + i) * a.R;
-        C<T> acc = czero<T>();
-        for (int r = 0; r < a.R; ++r) acc = cadd<T>(acc, cmulc<T>(gr[r], a.gs[(size_t)r * img + pix]));
-        gj = cadd<T>(gj, acc);
+        // G_S^H g_rows at this pixel (forward.py:303-306), shared-memory operands
+        const C<T>* gr = grS + (size_t)i * R;
+        C<T> acc0 = czero<T>(), acc1 = czero<T>();
+        int r = 0;
+        for (; r + 1 < R; r += 2) {
+          acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
+          acc1 = cadd<T>(acc1, cmulc<T>(gr[r + 1], gsS[(r + 1) * PIX_TX + lane]));
+        }
+        if (r < R) acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
+        gj = cadd<T>(gj, cadd<T>(acc0, acc1));
         gj = cadd<T>(gj, cmul<T>(e, gn));
         C<T> ge = cadd<T>(gP, cmul<T>(conj_<T>(gn), j));
         ge = cadd<T>(ge, cscale<T>(e, T(2) * gd));
@@ -295,20 +313,21 @@ struct FinalizeArgs {
   int* err;              // [S]
 };
 
-__global__ void finalize_kernel(FinalizeArgs a) {
-  const int scene = blockIdx.x;
-  __shared__ double red[32][4];
+// One CTA (>= 128 threads) reduces a scene's partials; the first 128 threads
+// take part in a fixed pattern, so the result does not depend on blockDim and
+// is bitwise identical wherever it runs (standalone or inside view_bwd).
+__device__ inline void finalize_block(const FinalizeArgs& a, int scene, double (*red)[4]) {
   const int tid = threadIdx.x;
   double s[4] = {0, 0, 0, 0};
-  for (int t = tid; t < a.ntiles; t += blockDim.x)
-    for (int k = 0; k < 4; ++k) s[k] += a.part[((size_t)scene * a.ntiles + t) * 4 + k];
-  // deterministic: fixed blockDim, fixed strides, fixed tree
+  if (tid < 128)
+    for (int t = tid; t < a.ntiles; t += 128)
+      for (int k = 0; k < 4; ++k) s[k] += a.part[((size_t)scene * a.ntiles + t) * 4 + k];
   for (int k = 0; k < 4; ++k) s[k] = warp_sum<double>(s[k]);
-  if ((tid & 31) == 0) for (int k = 0; k < 4; ++k) red[tid >> 5][k] = s[k];
+  if ((tid & 31) == 0 && tid < 128) for (int k = 0; k < 4; ++k) red[tid >> 5][k] = s[k];
   __syncthreads();
   if (tid == 0) {
     double st = 0, bo = 0, tv = 0, br = 0, da = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { st += red[w][0]; bo += red[w][1]; tv += red[w][2]; br += red[w][3]; }
+    for (int w = 0; w < 4; ++w) { st += red[w][0]; bo += red[w][1]; tv += red[w][2]; br += red[w][3]; }
     for (int i = 0; i < a.n; ++i) da += a.dloss[(size_t)scene * a.n + i];
     st /= a.c_inc[scene];
     da /= a.c_sca[scene];
@@ -330,6 +349,11 @@ __global__ void finalize_kernel(FinalizeArgs a) {
       atomicOr(&a.err[scene], bits);
     }
   }
+}
+
+__global__ void finalize_kernel(FinalizeArgs a) {
+  __shared__ double red[4][4];
+  finalize_block(a, blockIdx.x, red);
 }
 
 }  // namespace pdf

@@ -21,6 +21,7 @@
 //   C: inverse row FFTs of my rows, crop to M columns
 #pragma once
 #include "pdf_common.cuh"
+#include "pdf_pixel.cuh"
 
 namespace pdf {
 
@@ -52,6 +53,9 @@ struct ViewArgs {
   T* gy;              // [S][rows][D0] or null
   const T* cout;      // [S][D0] output gain per feature
   int joint;
+  // BWD: the scene's loss breakdown is finalised by (view 0, rank 0)
+  FinalizeArgs fin;
+  int do_fin;
   // APPLY
   const C<T>* x;
   C<T>* y;
@@ -130,6 +134,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   for (int i = tid; i < P; i += blockDim.x) s.tw[i] = a.twP[i];
   for (int i = tid; i < M; i += blockDim.x) s.twm[i] = a.twM[i];
   const size_t img = (size_t)M * M;
+  pdl_wait();   // everything below reads the previous kernel's outputs
 
   // ---------------- stage 0: my input rows -> s.rows ----------------------
   if constexpr (MODE == VIEW_FWD) {
@@ -284,6 +289,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
   }
 
+  pdl_trigger();
   if constexpr (MODE == VIEW_FWD) {
     double tot = block_sum_d<T>(nrm, red);
     if (tid == 0) a.norms[(size_t)v * CS + rank] = tot;
@@ -291,6 +297,10 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
 
   if constexpr (MODE == VIEW_BWD) {
     __syncthreads();
+    if (a.do_fin && view == 0 && rank == 0) {
+      finalize_block(a.fin, scene, reinterpret_cast<double(*)[4]>(red));
+      __syncthreads();
+    }
     // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)
     C<T>* U = s.small + M0;
     for (int i = tid; i < rp * K; i += blockDim.x) {
