@@ -1,0 +1,207 @@
+"""CPU tests: C-ABI library load + exported symbols, setup-code parity with the
+reference (golden vectors), host-side API logic, and the multi-rank path
+with a world_size-2 gloo group."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, Setup, cfg_baseline, cfg_tiny, golden, rel
+
+HEADER = os.path.join(ROOT, "include", "pdf_abi.h")
+
+
+# ------------------------------------------------------------------ ABI
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pdf_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2602_13805_b200 import build
+    return build.build()
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    names = _declared_functions()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    from paper_2602_13805_b200 import _native
+    assert set(names) == set(_native.EXPORTS)
+
+
+def test_abi_version_and_workspace_size_without_gpu(libpath):
+    from paper_2602_13805_b200 import _native as N
+    lib = ctypes.CDLL(libpath)
+    assert lib.pdf_abi_version() == N.ABI_VERSION
+    lib.pdf_workspace_bytes.restype = ctypes.c_size_t
+    lib.pdf_workspace_bytes.argtypes = [ctypes.POINTER(N.PdfDesc)]
+    d = N.PdfDesc()
+    d.abi_version, d.dtype, d.S, d.n, d.m1, d.m2, d.R, d.mf = 1, 0, 2, 16, 64, 64, 32, 8
+    d.e_inc = d.gd_kernel_hat = d.gs_matrix = d.data = 1
+    one = ctypes.c_double(1.0)
+    d.c_inc = d.c_sca = ctypes.pointer(one)
+    nbytes = lib.pdf_workspace_bytes(ctypes.byref(d))
+    # 4 field stacks of S*n*M*M complex128 dominate
+    assert nbytes > 4 * 2 * 16 * 64 * 64 * 16
+    d.m2 = 32   # non-square grid: rejected, not crashed
+    assert lib.pdf_workspace_bytes(ctypes.byref(d)) == 0
+    lib.pdf_last_error.restype = ctypes.c_char_p
+    assert b"square" in lib.pdf_last_error()
+
+
+def test_sm100a_sass_in_library(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+# ------------------------------------------------------------------ setup parity
+def test_operators_match_reference_tiny(tiny_setup, g_tiny):
+    assert rel(tiny_setup.ops.gd_kernel_hat, g_tiny["khat"]) < 1e-13
+    assert rel(tiny_setup.ops.gs_matrix, g_tiny["gs"]) < 1e-13
+    assert rel(tiny_setup.e_inc, g_tiny["e_inc"]) < 1e-14
+
+
+def test_operators_match_reference_cfg1(cfg1_setup, g_cfg1):
+    assert rel(cfg1_setup.ops.gd_kernel_hat, g_cfg1["khat"]) < 1e-13
+    assert rel(cfg1_setup.ops.gs_matrix, g_cfg1["gs"]) < 1e-13
+    ck = g_cfg1["einc_checksum"]
+    assert abs(cfg1_setup.e_inc.sum() - ck[0]) < 1e-9 and abs(np.abs(cfg1_setup.e_inc).sum() - ck[1]) < 1e-9
+
+
+def test_rasterised_scenes_match_reference():
+    from paper_2602_13805_b200 import build_grid, rasterize
+    from paper_2602_13805_b200.workloads import baseline_scene
+    for name, i in (("cfg1", 1), ("cfg2", 2), ("cfg3", 3)):
+        g = golden(name)
+        cfg = cfg_baseline(i)
+        chi = rasterize(baseline_scene(i)[0], build_grid(cfg)).values
+        assert np.array_equal(chi, g["chi_true"]), name
+
+
+def test_cfg4_random_ellipse_scenes_match_reference():
+    from paper_2602_13805_b200 import build_grid, rasterize
+    from paper_2602_13805_b200.workloads import baseline_config, cfg4_scene
+    grid = build_grid(baseline_config(4))
+    for idx in (0, 1):
+        g = golden(f"cfg4_s{idx}")
+        scene, _ = cfg4_scene(idx)
+        assert np.array_equal(rasterize(scene, grid).values, g["chi_true"])
+
+
+def test_host_simulate_matches_reference_data(g_tiny):
+    from paper_2602_13805_b200 import builtin_scene, simulate
+    sim = simulate(cfg_tiny(), builtin_scene("austria", 2.0, scale=0.9))
+    assert rel(sim.data.matrix, g_tiny["data"]) < 1e-10
+    assert np.array_equal(sim.chi_true.values, g_tiny["chi_true"])
+
+
+def test_config_json_round_trip(tmp_path):
+    from paper_2602_13805_b200.config import ConfigError, ImagingConfig, load_config, save_config
+    cfg = cfg_baseline(2)
+    save_config(tmp_path / "c.json", cfg)
+    assert load_config(tmp_path / "c.json") == cfg
+    with pytest.raises(ConfigError):
+        ImagingConfig(m_f=40).validate()
+    with pytest.raises(ConfigError):
+        ImagingConfig(ring_radius=0.5).validate()
+
+
+# ------------------------------------------------------------------ host API logic
+def test_spectral_basis_order_matches_oracle():
+    from oracle import pdf_oracle as O
+    from paper_2602_13805_b200.api import SpectralBasis
+    for m, f in ((16, 3), (64, 8), (32, 5)):
+        b = SpectralBasis(m, m, f)
+        r, c = O.corner_index(m, m, f)
+        assert np.array_equal(b.rows, r) and np.array_equal(b.cols, c)
+    with pytest.raises(ValueError):
+        SpectralBasis(8, 8, 5)
+
+
+def test_init_network_reproduces_reference_draws(g_tiny):
+    from paper_2602_13805_b200.api import flatten_params, init_network, unflatten_params
+    p = init_network(36, np.random.default_rng(6))
+    flat = flatten_params(p) + 0.05 * np.random.default_rng(6).standard_normal(flatten_params(p).size)
+    assert np.array_equal(flat, g_tiny["net_flat"])
+    back = unflatten_params(flat, p)
+    assert np.array_equal(flatten_params(back), flat)
+    with pytest.raises(ValueError):
+        unflatten_params(flat[:-1], p)
+
+
+def test_error_bits_map_to_reference_exceptions():
+    from paper_2602_13805_b200 import _native as N
+    from paper_2602_13805_b200.errors import PoleError, raise_for_bits
+    with pytest.raises(PoleError):
+        raise_for_bits([N.ERR_POLE | N.ERR_NONFINITE_STATE])
+    with pytest.raises(FloatingPointError, match=r"\['data', 'tv'\]"):
+        raise_for_bits([0, N.ERR_NONFINITE_DATA | N.ERR_NONFINITE_TV])
+    with pytest.raises(FloatingPointError, match="parameter gradient"):
+        raise_for_bits([N.ERR_NONFINITE_GRAD])
+    with pytest.raises(FloatingPointError, match="optimizer step"):
+        raise_for_bits([N.ERR_NONFINITE_PARAM])
+    raise_for_bits([0, 0])
+
+
+def test_loss_breakdown_row_layout():
+    from paper_2602_13805_b200.api import LossBreakdown
+    bd = LossBreakdown.from_row([1, 2, 3, 4, 5, 6], (1e-3, 1e-5, 1e-5))
+    assert bd.as_row() == (1, 2, 3, 4, 5, 6) and bd.total == 6 and bd.state == 1
+
+
+def test_zero_data_rejected_on_host(tiny_setup):
+    from paper_2602_13805_b200 import ScatteredData
+    from paper_2602_13805_b200.api import LossContext, SpectralBasis
+    from paper_2602_13805_b200.errors import ZeroDataError
+    with pytest.raises(ZeroDataError):
+        LossContext(data=ScatteredData(matrix=np.zeros((8, 8), complex)), e_inc=tiny_setup.e_inc,
+                    ops=tiny_setup.ops, basis=SpectralBasis(16, 16, 3), beta=6.0, lambdas=(1e-3, 1e-5, 1e-5),
+                    tau_b=0.5)
+
+
+# ------------------------------------------------------------------ multi-rank (gloo, world_size 2)
+def test_shard_range_partitions():
+    from paper_2602_13805_b200.shard import shard_range
+    for n in (0, 1, 7, 256):
+        for w in (1, 2, 3, 8):
+            got = [i for r in range(w) for i in shard_range(n, r, w)]
+            assert got == list(range(n))
+
+
+_WORKER = r'''
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch.distributed as dist
+from paper_2602_13805_b200.shard import shard_range, max_over_ranks, gather_rows
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+own = list(shard_range(10, r, w))
+rows = np.array([[i, i * i] for i in own], dtype=float)
+t = max_over_ranks(1.0 + r, dist)
+allr = gather_rows(rows, dist)
+if r == 0:
+    assert t == float(w), t
+    assert allr[:, 0].tolist() == list(range(10)), allr
+    print("OK", t)
+dist.destroy_process_group()
+'''
+
+
+def test_scene_sharding_with_gloo_world_size_2(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(_WORKER)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29531")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", str(script), ROOT]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "OK 2.0" in out.stdout
