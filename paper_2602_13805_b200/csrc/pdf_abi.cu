@@ -199,7 +199,9 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
   const size_t smem = view_smem_bytes<T>(c->M, c->d.mf, c->d.R, c->CS);
   void* args[] = {&a};
   cudaError_t e;
-  dim3 grid(c->CS, count), block(256), cl(c->CS, 1, 1);
+  static const int vt = env_int("PDF_VIEW_THREADS", 256);
+  const int nthr = c->E <= 4 ? vt : 256;
+  dim3 grid(c->CS, count), block(nthr), cl(c->CS, 1, 1);
   switch (c->E) {
 #define VCASE(EE)                                                   \
   case EE: {                                                        \
@@ -284,6 +286,15 @@ static int finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st) {
   return PDF_OK;
 }
 
+// cluster split for the network layers: enough CTAs for ~4 per SM (hot-L2
+// streaming needs bytes in flight), 1 when the batch alone fills the GPU
+static int net_split(long long base_ctas, int max_split) {
+  static const int cap = env_int("PDF_NET_CLUSTER", 2);
+  int c = 1;
+  while (c < cap && c < max_split && base_ctas * c < 4LL * 148) c *= 2;
+  return c;
+}
+
 template <typename T>
 static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, long long woff, long long boff,
                          T* out, int final_layer, int* step, cudaStream_t st) {
@@ -298,18 +309,24 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
   // one output row per warp while a single scene cannot fill the GPU, two otherwise
   const int opw = (c->RB == 1 && (c->d.S * N) / (NET_THREADS / 32) >= 2 * 148 * 4) ? 2 : 1;
+  const int kch = c->RB <= 2 ? FwdShape<T, 1>::KCH : FwdShape<T, 3>::KCH;
+  const int per = (NET_THREADS / 32) * opw;
+  const long long base = (long long)((N + per - 1) / per) * c->d.S;
+  const int CK = net_split(base, (K + kch - 1) / kch);
+  a.ks = ((K + CK - 1) / CK + kch - 1) / kch * kch;
   void* args[] = {&a};
   cudaError_t e;
+  const dim3 grid((N + per - 1) / per, CK, c->d.S), block(NET_THREADS), cl(1, CK, 1);
   switch (c->RB * 4 + opw) {
 #define FCASE(RR, OO)                                                                      \
   case RR * 4 + OO: {                                                                      \
-    const size_t smem = fwd_smem_elems<T, RR>() * sizeof(T);                               \
-    const int per = (NET_THREADS / 32) * OO;                                               \
-    e = plain_launch(net_fwd_kernel<T, RR, OO>, dim3((N + per - 1) / per, c->d.S),          \
-                     dim3(NET_THREADS), smem, st, args);                                   \
+    const size_t smem = fwd_smem_elems<T, RR>(OO) * sizeof(T);                             \
+    auto k = net_fwd_kernel<T, RR, OO>;                                                    \
+    e = prep(k, smem);                                                                     \
+    if (e == cudaSuccess) e = launch_cluster(k, grid, block, smem, st, cl, args);          \
     break;                                                                                 \
   }
-    FCASE(1, 1) FCASE(1, 2) FCASE(2, 1) FCASE(2, 2) FCASE(3, 1) FCASE(4, 1) FCASE(5, 1)
+    FCASE(1, 1) FCASE(1, 2) FCASE(2, 1) FCASE(3, 1) FCASE(4, 1) FCASE(5, 1)
 #undef FCASE
     default: return fail(PDF_EINVAL, "rows");
   }
@@ -329,14 +346,19 @@ static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T*
   a.lr = (T)c->d.lr; a.b1 = (T)c->d.adam_b1; a.b2 = (T)c->d.adam_b2; a.eps = (T)c->d.adam_eps;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
+  const long long base = (long long)((K + BWD_COLS - 1) / BWD_COLS) * c->d.S;
+  const int CN = net_split(base, (N + BWD_NCH - 1) / BWD_NCH);
+  a.ns = ((N + CN - 1) / CN + BWD_NCH - 1) / BWD_NCH * BWD_NCH;
   void* args[] = {&a};
   cudaError_t e;
-  const dim3 grid((K + BWD_COLS - 1) / BWD_COLS, c->d.S), block(NET_THREADS);
+  const dim3 grid((K + BWD_COLS - 1) / BWD_COLS, CN, c->d.S), block(NET_THREADS), cl(1, CN, 1);
   switch (c->RB * 2 + (fused ? 1 : 0)) {
 #define BCASE(RR, FF)                                                                      \
   case RR * 2 + FF: {                                                                      \
     const size_t smem = bwd_smem_elems<T, RR>() * sizeof(T);                               \
-    e = plain_launch(net_bwd_kernel<T, RR, (FF != 0)>, grid, block, smem, st, args);      \
+    auto k = net_bwd_kernel<T, RR, (FF != 0)>;                                             \
+    e = prep(k, smem);                                                                     \
+    if (e == cudaSuccess) e = launch_cluster(k, grid, block, smem, st, cl, args);          \
     break;                                                                                 \
   }
     BCASE(1, 0) BCASE(1, 1) BCASE(2, 0) BCASE(2, 1) BCASE(3, 0) BCASE(3, 1) BCASE(4, 0) BCASE(4, 1)

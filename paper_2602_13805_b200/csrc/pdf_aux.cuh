@@ -9,15 +9,15 @@ namespace pdf {
 
 __device__ inline int bitrev5(int l) { return __brev((unsigned)l) >> 27; }
 
-// khat_p[pos_c * P + pos_r] = khat[f(pos_r)][f(pos_c)] / P^2, f(q*32+l) = q + E*bitrev5(l)
+// khat_p[pos_c * P + pos_r] = khat[f(pos_r)][f(pos_c)] / P^2, f(q*32+l) = spectrum_slot_freq(l, q, E)
 template <typename T>
 __global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P) {
   const int E = P / 32;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= P * P) return;
   const int posc = idx / P, posr = idx % P;
-  const int fr = (posr / 32) + E * bitrev5(posr % 32);
-  const int fc = (posc / 32) + E * bitrev5(posc % 32);
+  const int fr = spectrum_slot_freq(posr % 32, posr / 32, E);
+  const int fc = spectrum_slot_freq(posc % 32, posc / 32, E);
   const T s = T(1) / (T(P) * T(P));
   out[idx] = cscale<T>(khat[(size_t)fr * P + fc], s);
 }

@@ -187,20 +187,45 @@ template <typename T> __device__ __forceinline__ C<T> tw_get(const C<T>* tw, int
   return w;
 }
 
+// Lane stages.  For E >= 2 each stage pairs lanes l, l^h and splits the
+// butterflies between them instead of having both lanes compute both halves:
+// the lower lane keeps register slots [0, E/2), the upper lane [E/2, E); each
+// lane ships the other half to its partner (one shuffle per pair), computes
+// its butterflies completely and stores sum -> slot j, (difference x twiddle)
+// -> slot j + E/2.  Every stage therefore swaps lane bit h with the top
+// register bit: after the five stages lane p, slot s holds the spectrum at
+//   f = R + E * bitrev5(L),  L = ((p & 15) << 1) | (s >> (e-1)),
+//                            R = ((p >> 4) << (e-1)) | (s & (E/2 - 1)),  E = 2^e
+// (host side: spectrum_slot_freq).  The inverse mirrors the stages exactly.
 template <typename T, int E>
 __device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
   constexpr int P = 32 * E;
   reg_dft<T, E, -1>(x);
 #pragma unroll
   for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], tw[(lane * q) & (P - 1)]);
+  if constexpr (E == 1) {
 #pragma unroll
-  for (int h = 16; h >= 1; h >>= 1) {
-    const bool upper = (lane & h) != 0;
-    const C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
+    for (int h = 16; h >= 1; h >>= 1) {
+      const bool upper = (lane & h) != 0;
+      const C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
+      C<T> o = shfl_xor<T>(x[0], h);
+      x[0] = upper ? cmul<T>(csub<T>(o, x[0]), w) : cadd<T>(x[0], o);
+    }
+  } else {
+    constexpr int H2 = E / 2;
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      C<T> o = shfl_xor<T>(x[q], h);
-      x[q] = upper ? cmul<T>(csub<T>(o, x[q]), w) : cadd<T>(x[q], o);
+    for (int h = 16; h >= 1; h >>= 1) {
+      const bool upper = (lane & h) != 0;
+      C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
+      if (upper) w = mk<T>(-w.x, -w.y);
+#pragma unroll
+      for (int j = 0; j < H2; ++j) {
+        const C<T> own = upper ? x[j + H2] : x[j];
+        const C<T> snd = upper ? x[j] : x[j + H2];
+        const C<T> rcv = shfl_xor<T>(snd, h);
+        x[j] = cadd<T>(own, rcv);
+        x[j + H2] = cmul<T>(csub<T>(own, rcv), w);
+      }
     }
   }
 }
@@ -208,19 +233,46 @@ __device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const C<T>* __restric
 template <typename T, int E>
 __device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
   constexpr int P = 32 * E;
+  if constexpr (E == 1) {
 #pragma unroll
-  for (int h = 1; h <= 16; h <<= 1) {
-    const bool upper = (lane & h) != 0;
-    const C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+    for (int h = 1; h <= 16; h <<= 1) {
+      const bool upper = (lane & h) != 0;
+      const C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+      C<T> o = shfl_xor<T>(x[0], h);
+      x[0] = upper ? csub<T>(o, cmul<T>(x[0], w)) : cadd<T>(x[0], cmul<T>(o, w));
+    }
+  } else {
+    constexpr int H2 = E / 2;
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      C<T> o = shfl_xor<T>(x[q], h);
-      x[q] = upper ? csub<T>(o, cmul<T>(x[q], w)) : cadd<T>(x[q], cmul<T>(o, w));
+    for (int h = 1; h <= 16; h <<= 1) {
+      const bool upper = (lane & h) != 0;
+      C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+      if (upper) w = mk<T>(-w.x, -w.y);
+#pragma unroll
+      for (int j = 0; j < H2; ++j) {
+        const C<T> t = cmul<T>(x[j + H2], w);
+        const C<T> own = cadd<T>(x[j], t);
+        const C<T> oth = csub<T>(x[j], t);
+        const C<T> rcv = shfl_xor<T>(oth, h);
+        x[j] = upper ? rcv : own;
+        x[j + H2] = upper ? own : rcv;
+      }
     }
   }
 #pragma unroll
   for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], tw[(lane * q) & (P - 1)]);
   reg_dft<T, E, +1>(x);
+}
+
+// frequency held by lane p, register slot s after warp_fft_fwd (see above)
+__host__ __device__ inline int spectrum_slot_freq(int p, int s, int E) {
+  auto br5 = [](int l) { int r = 0; for (int i = 0; i < 5; ++i) r |= ((l >> i) & 1) << (4 - i); return r; };
+  if (E == 1) return br5(p);
+  int e = 0;
+  while ((1 << e) < E) ++e;
+  const int L = ((p & 15) << 1) | (s >> (e - 1));
+  const int R = ((p >> 4) << (e - 1)) | (s & ((1 << (e - 1)) - 1));
+  return R + E * br5(L);
 }
 
 // deterministic fixed-order warp sum

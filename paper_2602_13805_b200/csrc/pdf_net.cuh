@@ -32,7 +32,7 @@ template <typename T> struct Epc { static constexpr int v = 16 / sizeof(T); };  
 
 template <typename T>
 struct NetFwdArgs {
-  int rows, K, N;
+  int rows, K, N, ks;                 // ks: K range per cluster rank (multiple of the chunk)
   const T* in; long long in_ss;       // [S][rows][K]
   const T* theta; long long th_ss;    // [S][Np]
   long long w_off, b_off;
@@ -54,21 +54,32 @@ template <typename T, int RB> struct FwdShape {
 };
 
 template <typename T, int RB>
-__host__ __device__ constexpr size_t fwd_smem_elems() {
-  return (size_t)2 * 16 * RB * FwdShape<T, RB>::P;
+__host__ __device__ constexpr size_t fwd_smem_elems(int opw) {
+  return (size_t)2 * 16 * RB * FwdShape<T, RB>::P + (size_t)(NET_THREADS / 32) * opw * 16 * RB;
 }
 
+// The K range is split across the CK CTAs of a cluster (CK = 1 when the
+// batch alone fills the GPU): a single scene then keeps ~4 CTAs per SM in
+// flight, which is what hot-L2 streaming needs (bytes in flight, not
+// launches, bound these skinny layers).  Partial row sums meet in DSMEM and
+// are added in rank order (deterministic).
 template <typename T, int RB, int OPW>
 __global__ void __launch_bounds__(NET_THREADS, RB <= 2 ? 2 : 1) net_fwd_kernel(NetFwdArgs<T> a) {
   using Sh = FwdShape<T, RB>;
   constexpr int RP = 16 * RB, KCH = Sh::KCH, P = Sh::P, VL = Sh::VL, EPC = Epc<T>::v;
   constexpr int SEG = KCH / EPC;
+  constexpr int NWP = NET_THREADS / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);            // 2 x [RP][P]
-  const int scene = blockIdx.y;
+  T* part = Xs + 2 * RP * P;                         // [NWP*OPW][RP] partial sums for the cluster
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CK = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int scene = blockIdx.z;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K, N = a.N, rows = a.rows;
-  const int nbase = (blockIdx.x * (NET_THREADS / 32) + warp) * OPW;
+  const int nbase = (blockIdx.x * NWP + warp) * OPW;
+  const int kb = rank * a.ks, ke = min(K, kb + a.ks);
   // (step counter is bumped after pdl_wait: the previous backward kernels read it)
   const T* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
   const T* __restrict__ X = a.in + scene * a.in_ss;
@@ -77,10 +88,23 @@ __global__ void __launch_bounds__(NET_THREADS, RB <= 2 ? 2 : 1) net_fwd_kernel(N
     T* dst = Xs + s * RP * P;
     for (int i = tid; i < RP * SEG; i += NET_THREADS) {
       const int r = i / SEG, sg = i % SEG, gk = k0 + sg * EPC;
-      const bool ok = r < rows && gk < K;
+      const bool ok = r < rows && gk < ke;
       cp_async16(dst + r * P + sg * EPC, ok ? X + (size_t)r * K + gk : X, ok);
     }
     cp_async_commit();
+  };
+  // this warp's weights for a chunk: lane covers k0 + lane + 32 j (coalesced
+  // global rows, conflict-free shared reads)
+  auto load_w = [&](int k0, T (&w)[OPW][VL]) {
+#pragma unroll
+    for (int o = 0; o < OPW; ++o) {
+      const int n = nbase + o;
+#pragma unroll
+      for (int j = 0; j < VL; ++j) {
+        const int kk = k0 + lane + 32 * j;
+        w[o][j] = (n < N && kk < ke) ? W[(size_t)n * K + kk] : T(0);
+      }
+    }
   };
 
   T acc[OPW][RP];
@@ -89,31 +113,17 @@ __global__ void __launch_bounds__(NET_THREADS, RB <= 2 ? 2 : 1) net_fwd_kernel(N
 #pragma unroll
     for (int r = 0; r < RP; ++r) acc[o][r] = T(0);
 
-  // this warp's weights for a chunk: lane covers k0 + lane + 32 j (coalesced
-  // global rows, conflict-free shared reads); the next chunk's weights are
-  // loaded while the current one is consumed
-  auto load_w = [&](int k0, T (&w)[OPW][VL]) {
-#pragma unroll
-    for (int o = 0; o < OPW; ++o) {
-      const int n = nbase + o;
-#pragma unroll
-      for (int j = 0; j < VL; ++j) {
-        const int kk = k0 + lane + 32 * j;
-        w[o][j] = (n < N && kk < K) ? W[(size_t)n * K + kk] : T(0);
-      }
-    }
-  };
   constexpr bool PF = OPW == 1;      // register prefetch of the next chunk (keeps 2 CTAs/SM otherwise)
   T w[OPW][VL], wn[PF ? OPW : 1][PF ? VL : 1];
-  if (a.w_early) load_w(0, w);
+  if (a.w_early && kb < ke) load_w(kb, w);
   pdl_wait();
-  if (!a.w_early) load_w(0, w);
-  if (a.step && tid == 0 && blockIdx.x == 0 && scene == 0) atomicAdd(a.step, 1);
-  stage(0, 0);
+  if (!a.w_early && kb < ke) load_w(kb, w);
+  if (a.step && tid == 0 && blockIdx.x == 0 && rank == 0 && scene == 0) atomicAdd(a.step, 1);
+  if (kb < ke) stage(kb, 0);
   int s = 0;
-  for (int k0 = 0; k0 < K; k0 += KCH, s ^= 1) {
-    if constexpr (PF) { if (k0 + KCH < K) load_w(k0 + KCH, wn); }
-    if (k0 + KCH < K) {
+  for (int k0 = kb; k0 < ke; k0 += KCH, s ^= 1) {
+    if constexpr (PF) { if (k0 + KCH < ke) load_w(k0 + KCH, wn); }
+    if (k0 + KCH < ke) {
       stage(k0 + KCH, s ^ 1);
       cp_async_wait<1>();
     } else {
@@ -140,48 +150,55 @@ __global__ void __launch_bounds__(NET_THREADS, RB <= 2 ? 2 : 1) net_fwd_kernel(N
 #pragma unroll
         for (int j = 0; j < VL; ++j) w[o][j] = wn[o][j];
     } else {
-      if (k0 + KCH < K) load_w(k0 + KCH, w);
+      if (k0 + KCH < ke) load_w(k0 + KCH, w);
     }
     __syncthreads();   // buffer s is restaged two chunks later
   }
   pdl_trigger();
-  // fixed-order lane reduction; lane r ends with output row r
+  // fixed-order lane reduction; every lane ends with all row sums
 #pragma unroll
   for (int o = 0; o < OPW; ++o)
 #pragma unroll
     for (int r = 0; r < RP; ++r) acc[o][r] = warp_sum<T>(acc[o][r]);
+  // lane r publishes row r (and r+32, r+64) of this warp's outputs
+#pragma unroll
+  for (int o = 0; o < OPW; ++o)
+#pragma unroll
+    for (int r = 0; r < RP; ++r)
+      if ((r & 31) == lane) part[(warp * OPW + o) * RP + r] = acc[o][r];
+  cluster.sync();
 
+  // reduce over the cluster ranks (fixed order) and apply the epilogue
   const T* bias = a.theta + scene * a.th_ss + a.b_off;
-#pragma unroll
-  for (int o = 0; o < OPW; ++o) {
-    const int gn = nbase + o;
-    if (gn >= N) continue;
-#pragma unroll
-    for (int r = 0; r < RP; ++r) {
-      if (r != lane && !(RP > 32 && r - 32 == lane) && !(RP > 64 && r - 64 == lane)) continue;
-      if (r >= rows) continue;
-      const T z = acc[o][r] + bias[gn];
-      if (!a.final_layer) {
-        a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
-      } else {
-        const T yv = z * a.cout[(size_t)scene * N + gn];
-        // [Re | Im] feature layout (network.py:123-136)
-        const int half = N / 2;
-        const int f = gn < half ? gn : gn - half;
-        int view, m;
-        if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
-        const size_t off = ((size_t)scene * a.n + view) * a.M0 + m;
-        T* dst = reinterpret_cast<T*>(a.alpha_hat + off);
-        const T* src = reinterpret_cast<const T*>(a.alpha0 + off);
-        if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
-      }
+  const int total = NWP * OPW * RP;
+  for (int e = rank * NET_THREADS + tid; e < total; e += CK * NET_THREADS) {
+    const int wo = e / RP, r = e % RP;
+    const int gn = blockIdx.x * NWP * OPW + wo;
+    if (gn >= N || r >= rows) continue;
+    T z = T(0);
+    for (int c = 0; c < CK; ++c) z += cluster.map_shared_rank(part, c)[e];
+    z += bias[gn];
+    if (!a.final_layer) {
+      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+    } else {
+      const T yv = z * a.cout[(size_t)scene * N + gn];
+      // [Re | Im] feature layout (network.py:123-136)
+      const int half = N / 2;
+      const int f = gn < half ? gn : gn - half;
+      int view, m;
+      if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
+      const size_t off = ((size_t)scene * a.n + view) * a.M0 + m;
+      T* dst = reinterpret_cast<T*>(a.alpha_hat + off);
+      const T* src = reinterpret_cast<const T*>(a.alpha0 + off);
+      if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
     }
   }
+  cluster.sync();
 }
 
 template <typename T>
 struct NetBwdArgs {
-  int rows, K, N;
+  int rows, K, N, ns;                 // ns: rows of W per cluster rank (multiple of 128)
   const T* gz; long long gz_ss;       // [S][rows][N]   gradient at this layer's pre-activation
   const T* hin; long long hin_ss;     // [S][rows][K]   this layer's input
   T* theta; long long th_ss;          // [S][Np] (updated in place when fused)
@@ -247,7 +264,7 @@ template <typename T, int RB> struct BwdShape {
 template <typename T, int RB>
 __host__ __device__ constexpr size_t bwd_smem_elems() {
   constexpr int RP = 16 * RB;
-  return (size_t)2 * RP * BwdShape<T, RB>::GP + (size_t)BWD_SUB * 16 * BWD_COLS +
+  return (size_t)2 * RP * BwdShape<T, RB>::GP + (size_t)BWD_SUB * 16 * BWD_COLS + (size_t)RP * BWD_COLS +
          (BwdShape<T, RB>::HREG ? 0 : (size_t)2 * RP * NET_THREADS);
 }
 
@@ -260,15 +277,20 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Gs = reinterpret_cast<T*>(smem_raw);            // 2 x [RP][GP]   g_z[r][n0 + i]
   T* red = Gs + 2 * RP * GP;                         // [BWD_SUB][16][BWD_COLS] reduction scratch
-  T* Hs = red + BWD_SUB * 16 * BWD_COLS;             // [RP][NET_THREADS] when !HREG
+  T* Hs = red + BWD_SUB * 16 * BWD_COLS + RP * BWD_COLS;   // [RP][NET_THREADS] when !HREG (after cpart)
   T* GHs = Hs + RP * NET_THREADS;                    // [RP][NET_THREADS] when !HREG
   __shared__ T bc_s[2];
-  const int scene = blockIdx.y;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CN = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int scene = blockIdx.z;
   const int tid = threadIdx.x;
   const int col = tid % BWD_COLS, sub = tid / BWD_COLS;
   const int k = blockIdx.x * BWD_COLS + col;
   const int K = a.K, N = a.N, rows = a.rows;
   const bool kok = k < K;
+  // this cluster rank's rows of W (CN = 1 when the batch alone fills the GPU)
+  const int nb = min(N, rank * a.ns), ne = min(N, nb + a.ns);
 
   const T* __restrict__ hin = a.hin + scene * a.hin_ss;
   const T* __restrict__ gz = a.gz + scene * a.gz_ss;
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
     T* dst = Gs + s * RP * GP;
     for (int i = tid; i < RP * SEG; i += NET_THREADS) {
       const int r = i / SEG, sg = i % SEG, gn = n0 + sg * EPC;
-      const bool ok = r < rows && gn < N;
+      const bool ok = r < rows && gn < ne;
       cp_async16(dst + r * GP + sg * EPC, ok ? gz + (size_t)r * N + gn : gz, ok);
     }
     cp_async_commit();
@@ -312,7 +334,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
 #pragma unroll
     for (int u = 0; u < BWD_UR; ++u) {
       const int n = n0 + sub + BWD_SUB * u;
-      const bool ok = kok && n < N;
+      const bool ok = kok && n < ne;
       const size_t o = (size_t)n * K + k;
       w_[u] = ok ? W[o] : T(0);
       if constexpr (FUSED) {
@@ -324,15 +346,15 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
   int errbits = 0;
   int s = 0;
   T wv[BWD_UR], mv[BWD_UR], vv[BWD_UR];
-  load_step(0, wv, mv, vv);
+  if (nb < ne) load_step(nb, wv, mv, vv);
   pdl_wait();
-  stage(0, 0);
-  for (int n0 = 0; n0 < N; n0 += BWD_NCH, s ^= 1) {
+  if (nb < ne) stage(nb, 0);
+  for (int n0 = nb; n0 < ne; n0 += BWD_NCH, s ^= 1) {
     T wn[DB ? BWD_UR : 1], mn[DB ? BWD_UR : 1], vn[DB ? BWD_UR : 1];
     if constexpr (DB) {
-      if (n0 + BWD_NCH < N) load_step(n0 + BWD_NCH, wn, mn, vn);
+      if (n0 + BWD_NCH < ne) load_step(n0 + BWD_NCH, wn, mn, vn);
     }
-    if (n0 + BWD_NCH < N) {
+    if (n0 + BWD_NCH < ne) {
       stage(n0 + BWD_NCH, s ^ 1);
       cp_async_wait<1>();
     } else {
@@ -359,7 +381,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
 #pragma unroll
     for (int u = 0; u < BWD_UR; ++u) {
       const int n = n0 + sub + BWD_SUB * u;
-      if (!kok || n >= N) continue;
+      if (!kok || n >= ne) continue;
       const size_t o = (size_t)n * K + k;
       if (!isfinite(gw[u])) errbits |= ERR_NONFINITE_GRAD;
       if constexpr (FUSED) {
@@ -372,7 +394,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
       }
     }
     // bias (network.py:213,217): gb[n] = sum_r g_z[r, n], owned by the first column tile
-    if (blockIdx.x == 0 && tid < BWD_NCH && n0 + tid < N) {
+    if (blockIdx.x == 0 && tid < BWD_NCH && n0 + tid < ne) {
       T gb = T(0);
       for (int r = 0; r < rows; ++r) gb += G[r * GP + tid];
       const int gn = n0 + tid;
@@ -393,7 +415,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
 #pragma unroll
       for (int u = 0; u < BWD_UR; ++u) { wv[u] = wn[u]; mv[u] = mn[u]; vv[u] = vn[u]; }
     } else {
-      if (n0 + BWD_NCH < N) load_step(n0 + BWD_NCH, wv, mv, vv);
+      if (n0 + BWD_NCH < ne) load_step(n0 + BWD_NCH, wv, mv, vv);
     }
     __syncthreads();   // buffer s is restaged two steps later
   }
@@ -401,7 +423,9 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
   if (errbits) atomicOr(&a.err[scene], errbits);
 
   if (a.gzprev) {
-    // g_h[r][k] = sum over the 32 row subsets (fixed order), 16 rows at a time
+    // g_h[r][k]: sum over the 32 row subsets (fixed order) into cpart, then over
+    // the cluster ranks (fixed order) through DSMEM
+    T* cpart = red + BWD_SUB * 16 * BWD_COLS;        // [RP][BWD_COLS]
 #pragma unroll
     for (int rb = 0; rb < RP; rb += 16) {
 #pragma unroll
@@ -419,16 +443,23 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
       }
       __syncthreads();
       if (tid < 16 * BWD_COLS) {
-        const int j = tid / BWD_COLS, c = tid % BWD_COLS, r = rb + j, gk = blockIdx.x * BWD_COLS + c;
+        const int j = tid / BWD_COLS, c = tid % BWD_COLS;
         T sum = T(0);
         for (int q = 0; q < BWD_SUB; ++q) sum += red[(q * 16 + j) * BWD_COLS + c];
-        if (r < rows && gk < K) {
-          const T hv = hin[(size_t)r * K + gk];
-          a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = sum * (T(1) - hv * hv);
-        }
+        cpart[(rb + j) * BWD_COLS + c] = sum;
       }
       __syncthreads();
     }
+    cluster.sync();
+    for (int e = rank * NET_THREADS + tid; e < rows * BWD_COLS; e += CN * NET_THREADS) {
+      const int r = e / BWD_COLS, c = e % BWD_COLS, gk = blockIdx.x * BWD_COLS + c;
+      if (gk >= K) continue;
+      T sum = T(0);
+      for (int q = 0; q < CN; ++q) sum += cluster.map_shared_rank(cpart, q)[e];
+      const T hv = hin[(size_t)r * K + gk];
+      a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = sum * (T(1) - hv * hv);
+    }
+    cluster.sync();
   }
 }
 

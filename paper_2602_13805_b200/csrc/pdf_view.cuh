@@ -103,7 +103,7 @@ __device__ inline double block_sum_d(double v, double* red) {
 }
 
 template <typename T, int E, int MODE>
-__global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
+__global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int P = 32 * E;
   cg::cluster_group cluster = cg::this_cluster();
@@ -207,7 +207,16 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     for (int r = warp; r < a.R; r += nw) {
       const C<T>* g = a.gs + (size_t)r * img + p0;
       C<T> acc = czero<T>();
-      for (int i = lane; i < np; i += 32) acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
+      C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
+      int i = lane;
+      for (; i + 96 < np; i += 128) {   // four independent chains, loads in flight together
+        acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
+        acc1 = cadd<T>(acc1, cmul<T>(s.rows[i + 32], g[i + 32]));
+        acc2 = cadd<T>(acc2, cmul<T>(s.rows[i + 64], g[i + 64]));
+        acc3 = cadd<T>(acc3, cmul<T>(s.rows[i + 96], g[i + 96]));
+      }
+      for (; i < np; i += 32) acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
+      acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
       acc.x = warp_sum<T>(acc.x);
       acc.y = warp_sum<T>(acc.y);
       if (lane == 0) {
@@ -247,10 +256,14 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       const int row = lane + 32 * k;
       x[k] = (k < KH && lane_ok) ? s.bufA[(size_t)row * cp + cc] : czero<T>();
     }
-    warp_fft_fwd<T, E>(x, s.tw, lane);
+    // the kernel spectrum column is fetched before the FFT so its latency hides
     const C<T>* kh = a.khat + (size_t)posc * P;
+    C<T> kv[E];
 #pragma unroll
-    for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kh[q * 32 + lane]);
+    for (int q = 0; q < E; ++q) kv[q] = kh[q * 32 + lane];
+    warp_fft_fwd<T, E>(x, s.tw, lane);
+#pragma unroll
+    for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kv[q]);
     warp_fft_inv<T, E>(x, s.tw, lane);
 #pragma unroll
     for (int k = 0; k < KH; ++k) {
@@ -307,7 +320,14 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       const int yl = i / K, w = i % K;
       const int f = corner_freq<T>(w, mf, M);
       C<T> acc = czero<T>();
-      for (int x = 0; x < M; ++x) acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
+      C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
+      for (int x = 0; x < M; x += 4) {   // M is a multiple of 4: four independent chains
+        acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
+        acc1 = cadd<T>(acc1, cmul<T>(s.rows[yl * M + x + 1], s.twm[(f * (x + 1)) & (M - 1)]));
+        acc2 = cadd<T>(acc2, cmul<T>(s.rows[yl * M + x + 2], s.twm[(f * (x + 2)) & (M - 1)]));
+        acc3 = cadd<T>(acc3, cmul<T>(s.rows[yl * M + x + 3], s.twm[(f * (x + 3)) & (M - 1)]));
+      }
+      acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
       U[i] = acc;
     }
     __syncthreads();
