@@ -29,6 +29,7 @@ static int env_int(const char* name, int dflt) {
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
+  if (code == PDF_ECUDA) (void)cudaGetLastError();   // do not leak a stale error into the next call
   return code;
 }
 
@@ -346,12 +347,15 @@ static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T*
   a.lr = (T)c->d.lr; a.b1 = (T)c->d.adam_b1; a.b2 = (T)c->d.adam_b2; a.eps = (T)c->d.adam_eps;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
-  const long long base = (long long)((K + BWD_COLS - 1) / BWD_COLS) * c->d.S;
-  const int CN = net_split(base, (N + BWD_NCH - 1) / BWD_NCH);
-  a.ns = ((N + CN - 1) / CN + BWD_NCH - 1) / BWD_NCH * BWD_NCH;
+  const int cols = c->RB >= 4 ? BwdShape<T, 4>::COLS : BwdShape<T, 1>::COLS;
+  const int nch = c->RB >= 4 ? BwdShape<T, 4>::NCH : BwdShape<T, 1>::NCH;
+  const int thr = c->RB >= 4 ? BwdShape<T, 4>::THR : BwdShape<T, 1>::THR;
+  const long long base = (long long)((K + cols - 1) / cols) * c->d.S;
+  const int CN = net_split(base, (N + nch - 1) / nch);
+  a.ns = ((N + CN - 1) / CN + BWD_NCH_MAX - 1) / BWD_NCH_MAX * BWD_NCH_MAX;
   void* args[] = {&a};
   cudaError_t e;
-  const dim3 grid((K + BWD_COLS - 1) / BWD_COLS, CN, c->d.S), block(NET_THREADS), cl(1, CN, 1);
+  const dim3 grid((K + cols - 1) / cols, CN, c->d.S), block(thr), cl(1, CN, 1);
   switch (c->RB * 2 + (fused ? 1 : 0)) {
 #define BCASE(RR, FF)                                                                      \
   case RR * 2 + FF: {                                                                      \

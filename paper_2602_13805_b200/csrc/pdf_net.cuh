@@ -251,42 +251,51 @@ __device__ __forceinline__ void adam_one(T& p, T& m, T& v, T g, T lr, T b1, T b2
   p = p - div_nr(lr * mh, sqrt_nr(vh) + eps);
 }
 
-constexpr int BWD_COLS = 8;                          // input columns per CTA
-constexpr int BWD_SUB = NET_THREADS / BWD_COLS;      // row subsets per CTA (32)
-constexpr int BWD_UR = 4;                            // rows per thread per step (ILP)
-constexpr int BWD_NCH = BWD_SUB * BWD_UR;            // rows of g_z staged per step (128)
-
+// Thread layout of the backward kernel by row count (RP = 16*RB rows):
+//   RB <= 2 : 8 columns x 32 row subsets, h and the g_h partial in registers
+//   RB == 3 : same, h[:, k] shared per column in shared memory
+//   RB >= 4 : 128 threads = 16 columns x 8 subsets, g_h partial in shared memory
 template <typename T, int RB> struct BwdShape {
-  static constexpr bool HREG = RB <= 2;              // h / g_h partial in registers
-  static constexpr int GP = BWD_NCH + Epc<T>::v;      // padded pitch of the staged g_z rows
+  static constexpr int THR = RB >= 4 ? 128 : 256;
+  static constexpr int COLS = RB >= 4 ? 16 : 8;        // input columns per CTA
+  static constexpr int SUB = THR / COLS;                // row subsets per CTA
+  static constexpr int UR = RB >= 4 ? 2 : 4;            // rows per thread per step (ILP)
+  static constexpr int NCH = SUB * UR;                  // rows of g_z staged per step
+  static constexpr bool HR = RB <= 2;                   // h in registers
+  static constexpr bool GR = RB <= 3;                   // g_h partial in registers
+  static constexpr int GP = NCH + Epc<T>::v;            // padded pitch of the staged g_z rows
 };
+constexpr int BWD_NCH_MAX = 128;
 
 template <typename T, int RB>
 __host__ __device__ constexpr size_t bwd_smem_elems() {
+  using Sh = BwdShape<T, RB>;
   constexpr int RP = 16 * RB;
-  return (size_t)2 * RP * BwdShape<T, RB>::GP + (size_t)BWD_SUB * 16 * BWD_COLS + (size_t)RP * BWD_COLS +
-         (BwdShape<T, RB>::HREG ? 0 : (size_t)2 * RP * NET_THREADS);
+  return (size_t)2 * RP * Sh::GP + (size_t)Sh::SUB * 16 * Sh::COLS + (size_t)RP * Sh::COLS +
+         (Sh::HR ? 0 : (size_t)RP * Sh::COLS) + (Sh::GR ? 0 : (size_t)RP * Sh::THR);
 }
 
 template <typename T, int RB, bool FUSED>
-__global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(NetBwdArgs<T> a) {
+__global__ void __launch_bounds__(BwdShape<T, RB>::THR, RB == 1 ? 2 : 1) net_bwd_kernel(NetBwdArgs<T> a) {
   using Sh = BwdShape<T, RB>;
   constexpr int RP = 16 * RB, EPC = Epc<T>::v, GP = Sh::GP;
-  constexpr bool HREG = Sh::HREG;
-  constexpr int SEG = BWD_NCH / EPC;
+  constexpr int THR = Sh::THR, COLS = Sh::COLS, SUB = Sh::SUB, UR = Sh::UR, NCH = Sh::NCH;
+  constexpr bool HR = Sh::HR, GR = Sh::GR;
+  constexpr int SEG = NCH / EPC;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Gs = reinterpret_cast<T*>(smem_raw);            // 2 x [RP][GP]   g_z[r][n0 + i]
-  T* red = Gs + 2 * RP * GP;                         // [BWD_SUB][16][BWD_COLS] reduction scratch
-  T* Hs = red + BWD_SUB * 16 * BWD_COLS + RP * BWD_COLS;   // [RP][NET_THREADS] when !HREG (after cpart)
-  T* GHs = Hs + RP * NET_THREADS;                    // [RP][NET_THREADS] when !HREG
+  T* red = Gs + 2 * RP * GP;                         // [SUB][16][COLS] reduction scratch
+  T* cpart = red + SUB * 16 * COLS;                  // [RP][COLS] CTA partial of g_h
+  T* Hs = cpart + RP * COLS;                         // [RP][COLS] h when !HR
+  T* GHs = Hs + (HR ? 0 : RP * COLS);                // [RP][THR]  g_h partial when !GR
   __shared__ T bc_s[2];
   cg::cluster_group cluster = cg::this_cluster();
   const int CN = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   const int scene = blockIdx.z;
   const int tid = threadIdx.x;
-  const int col = tid % BWD_COLS, sub = tid / BWD_COLS;
-  const int k = blockIdx.x * BWD_COLS + col;
+  const int col = tid % COLS, sub = tid / COLS;
+  const int k = blockIdx.x * COLS + col;
   const int K = a.K, N = a.N, rows = a.rows;
   const bool kok = k < K;
   // this cluster rank's rows of W (CN = 1 when the batch alone fills the GPU)
@@ -301,7 +310,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
 
   auto stage = [&](int n0, int s) {
     T* dst = Gs + s * RP * GP;
-    for (int i = tid; i < RP * SEG; i += NET_THREADS) {
+    for (int i = tid; i < RP * SEG; i += THR) {
       const int r = i / SEG, sg = i % SEG, gn = n0 + sg * EPC;
       const bool ok = r < rows && gn < ne;
       cp_async16(dst + r * GP + sg * EPC, ok ? gz + (size_t)r * N + gn : gz, ok);
@@ -318,22 +327,23 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
       bc_s[0] = bc_s[1] = T(1);
     }
   }
-  T h[HREG ? RP : 1], gh[HREG ? RP : 1];
-#pragma unroll(HREG ? RP : 4)
+  T h[HR ? RP : 1], gh[GR ? RP : 1];
+#pragma unroll(GR ? RP : 4)
   for (int r = 0; r < RP; ++r) {
     const T hv = (kok && r < rows) ? hin[(size_t)r * K + k] : T(0);
-    if constexpr (HREG) { h[r] = hv; gh[r] = T(0); }
-    else { Hs[r * NET_THREADS + tid] = hv; GHs[r * NET_THREADS + tid] = T(0); }
+    if constexpr (HR) h[r] = hv; else if (sub == 0) Hs[r * COLS + col] = hv;
+    if constexpr (GR) gh[r] = T(0); else GHs[r * THR + tid] = T(0);
   }
-  // this thread's rows of a step: n0 + sub + BWD_SUB*u.  W, m, v of the first
+  if constexpr (!HR) __syncthreads();
+  // this thread's rows of a step: n0 + sub + SUB*u.  W, m, v of the first
   // step are final since the previous iteration, so they are loaded before
   // pdl_wait; later steps are prefetched one step ahead (register double
   // buffer where the register budget allows it).
-  constexpr bool DB = !HREG;
-  auto load_step = [&](int n0, T (&w_)[BWD_UR], T (&m_)[BWD_UR], T (&v_)[BWD_UR]) {
+  constexpr bool DB = !GR;
+  auto load_step = [&](int n0, T (&w_)[UR], T (&m_)[UR], T (&v_)[UR]) {
 #pragma unroll
-    for (int u = 0; u < BWD_UR; ++u) {
-      const int n = n0 + sub + BWD_SUB * u;
+    for (int u = 0; u < UR; ++u) {
+      const int n = n0 + sub + SUB * u;
       const bool ok = kok && n < ne;
       const size_t o = (size_t)n * K + k;
       w_[u] = ok ? W[o] : T(0);
@@ -345,17 +355,17 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
   };
   int errbits = 0;
   int s = 0;
-  T wv[BWD_UR], mv[BWD_UR], vv[BWD_UR];
+  T wv[UR], mv[UR], vv[UR];
   if (nb < ne) load_step(nb, wv, mv, vv);
   pdl_wait();
   if (nb < ne) stage(nb, 0);
-  for (int n0 = nb; n0 < ne; n0 += BWD_NCH, s ^= 1) {
-    T wn[DB ? BWD_UR : 1], mn[DB ? BWD_UR : 1], vn[DB ? BWD_UR : 1];
+  for (int n0 = nb; n0 < ne; n0 += NCH, s ^= 1) {
+    T wn[DB ? UR : 1], mn[DB ? UR : 1], vn[DB ? UR : 1];
     if constexpr (DB) {
-      if (n0 + BWD_NCH < ne) load_step(n0 + BWD_NCH, wn, mn, vn);
+      if (n0 + NCH < ne) load_step(n0 + NCH, wn, mn, vn);
     }
-    if (n0 + BWD_NCH < ne) {
-      stage(n0 + BWD_NCH, s ^ 1);
+    if (n0 + NCH < ne) {
+      stage(n0 + NCH, s ^ 1);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -363,24 +373,25 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
     __syncthreads();
     const T* G = Gs + s * RP * GP;
     const T ibc1 = bc_s[0], ibc2 = bc_s[1];
-    T gw[BWD_UR];
+    T gw[UR];
 #pragma unroll
-    for (int u = 0; u < BWD_UR; ++u) gw[u] = T(0);
-#pragma unroll(HREG ? RP : 4)
+    for (int u = 0; u < UR; ++u) gw[u] = T(0);
+#pragma unroll(GR ? RP : 4)
     for (int r = 0; r < RP; ++r) {
-      const T hr = HREG ? h[r] : Hs[r * NET_THREADS + tid];
+      T hr;
+      if constexpr (HR) hr = h[r]; else hr = Hs[r * COLS + col];
       T ghs = T(0);
 #pragma unroll
-      for (int u = 0; u < BWD_UR; ++u) {
-        const T g = G[r * GP + sub + BWD_SUB * u];
+      for (int u = 0; u < UR; ++u) {
+        const T g = G[r * GP + sub + SUB * u];
         gw[u] += g * hr;
         ghs += g * wv[u];
       }
-      if constexpr (HREG) gh[r] += ghs; else GHs[r * NET_THREADS + tid] += ghs;
+      if constexpr (GR) gh[r] += ghs; else GHs[r * THR + tid] += ghs;
     }
 #pragma unroll
-    for (int u = 0; u < BWD_UR; ++u) {
-      const int n = n0 + sub + BWD_SUB * u;
+    for (int u = 0; u < UR; ++u) {
+      const int n = n0 + sub + SUB * u;
       if (!kok || n >= ne) continue;
       const size_t o = (size_t)n * K + k;
       if (!isfinite(gw[u])) errbits |= ERR_NONFINITE_GRAD;
@@ -394,7 +405,7 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
       }
     }
     // bias (network.py:213,217): gb[n] = sum_r g_z[r, n], owned by the first column tile
-    if (blockIdx.x == 0 && tid < BWD_NCH && n0 + tid < ne) {
+    if (blockIdx.x == 0 && tid < NCH && n0 + tid < ne) {
       T gb = T(0);
       for (int r = 0; r < rows; ++r) gb += G[r * GP + tid];
       const int gn = n0 + tid;
@@ -413,9 +424,9 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
     }
     if constexpr (DB) {
 #pragma unroll
-      for (int u = 0; u < BWD_UR; ++u) { wv[u] = wn[u]; mv[u] = mn[u]; vv[u] = vn[u]; }
+      for (int u = 0; u < UR; ++u) { wv[u] = wn[u]; mv[u] = mn[u]; vv[u] = vn[u]; }
     } else {
-      if (n0 + BWD_NCH < ne) load_step(n0 + BWD_NCH, wv, mv, vv);
+      if (n0 + NCH < ne) load_step(n0 + NCH, wv, mv, vv);
     }
     __syncthreads();   // buffer s is restaged two steps later
   }
@@ -425,34 +436,33 @@ __global__ void __launch_bounds__(NET_THREADS, RB == 1 ? 2 : 1) net_bwd_kernel(N
   if (a.gzprev) {
     // g_h[r][k]: sum over the 32 row subsets (fixed order) into cpart, then over
     // the cluster ranks (fixed order) through DSMEM
-    T* cpart = red + BWD_SUB * 16 * BWD_COLS;        // [RP][BWD_COLS]
 #pragma unroll
     for (int rb = 0; rb < RP; rb += 16) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int r = rb + j;
         T v_;
-        if constexpr (HREG) {
+        if constexpr (GR) {
           v_ = T(0);
 #pragma unroll
           for (int q = 0; q < RP; ++q) if (q == r) v_ = gh[q];
         } else {
-          v_ = GHs[r * NET_THREADS + tid];
+          v_ = GHs[r * THR + tid];
         }
-        red[(sub * 16 + j) * BWD_COLS + col] = v_;
+        red[(sub * 16 + j) * COLS + col] = v_;
       }
       __syncthreads();
-      if (tid < 16 * BWD_COLS) {
-        const int j = tid / BWD_COLS, c = tid % BWD_COLS;
+      if (tid < 16 * COLS) {
+        const int j = tid / COLS, c = tid % COLS;
         T sum = T(0);
-        for (int q = 0; q < BWD_SUB; ++q) sum += red[(q * 16 + j) * BWD_COLS + c];
-        cpart[(rb + j) * BWD_COLS + c] = sum;
+        for (int q = 0; q < SUB; ++q) sum += red[(q * 16 + j) * COLS + c];
+        cpart[(rb + j) * COLS + c] = sum;
       }
       __syncthreads();
     }
     cluster.sync();
-    for (int e = rank * NET_THREADS + tid; e < rows * BWD_COLS; e += CN * NET_THREADS) {
-      const int r = e / BWD_COLS, c = e % BWD_COLS, gk = blockIdx.x * BWD_COLS + c;
+    for (int e = rank * THR + tid; e < rows * COLS; e += CN * THR) {
+      const int r = e / COLS, c = e % COLS, gk = blockIdx.x * COLS + c;
       if (gk >= K) continue;
       T sum = T(0);
       for (int q = 0; q < CN; ++q) sum += cluster.map_shared_rank(cpart, q)[e];
