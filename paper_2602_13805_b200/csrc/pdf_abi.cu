@@ -201,7 +201,7 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
   void* args[] = {&a};
   cudaError_t e;
   static const int vt = env_int("PDF_VIEW_THREADS", 256);
-  const int nthr = c->E <= 4 ? vt : 256;
+  const int nthr = std::min(vt, 256);
   dim3 grid(c->CS, count), block(nthr), cl(c->CS, 1, 1);
   switch (c->E) {
 #define VCASE(EE)                                                   \

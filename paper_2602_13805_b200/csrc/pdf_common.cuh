@@ -197,26 +197,46 @@ template <typename T> __device__ __forceinline__ C<T> tw_get(const C<T>* tw, int
 //   f = R + E * bitrev5(L),  L = ((p & 15) << 1) | (s >> (e-1)),
 //                            R = ((p >> 4) << (e-1)) | (s & (E/2 - 1)),  E = 2^e
 // (host side: spectrum_slot_freq).  The inverse mirrors the stages exactly.
+// Per-lane twiddles are the same for every transform a lane runs, so they are
+// read from the shared table once per thread and kept in registers:
+//   st[i]  = tw[(lane & (h-1)) * P/(2h)] for the lane stage h = 16 >> i
+//   rq[q]  = tw[(lane * q) mod P]         for the register-to-lane twiddle
 template <typename T, int E>
-__device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
-  constexpr int P = 32 * E;
+struct LaneTw {
+  C<T> st[5];
+  C<T> rq[E];
+  __device__ __forceinline__ void load(const C<T>* __restrict__ tw, int lane) {
+    constexpr int P = 32 * E;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const int h = 16 >> i;
+      st[i] = tw[(lane & (h - 1)) * (P / (2 * h))];
+    }
+#pragma unroll
+    for (int q = 0; q < E; ++q) rq[q] = tw[(lane * q) & (P - 1)];
+  }
+};
+
+template <typename T, int E>
+__device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const LaneTw<T, E>& lt, int lane) {
   reg_dft<T, E, -1>(x);
 #pragma unroll
-  for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], tw[(lane * q) & (P - 1)]);
+  for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], lt.rq[q]);
   if constexpr (E == 1) {
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
+    for (int i = 0; i < 5; ++i) {
+      const int h = 16 >> i;
       const bool upper = (lane & h) != 0;
-      const C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
       C<T> o = shfl_xor<T>(x[0], h);
-      x[0] = upper ? cmul<T>(csub<T>(o, x[0]), w) : cadd<T>(x[0], o);
+      x[0] = upper ? cmul<T>(csub<T>(o, x[0]), lt.st[i]) : cadd<T>(x[0], o);
     }
   } else {
     constexpr int H2 = E / 2;
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
+    for (int i = 0; i < 5; ++i) {
+      const int h = 16 >> i;
       const bool upper = (lane & h) != 0;
-      C<T> w = tw[((lane & (h - 1)) * (P / (2 * h)))];
+      C<T> w = lt.st[i];
       if (upper) w = mk<T>(-w.x, -w.y);
 #pragma unroll
       for (int j = 0; j < H2; ++j) {
@@ -231,22 +251,23 @@ __device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const C<T>* __restric
 }
 
 template <typename T, int E>
-__device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const C<T>* __restrict__ tw, int lane) {
-  constexpr int P = 32 * E;
+__device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const LaneTw<T, E>& lt, int lane) {
   if constexpr (E == 1) {
 #pragma unroll
-    for (int h = 1; h <= 16; h <<= 1) {
+    for (int i = 4; i >= 0; --i) {
+      const int h = 16 >> i;
       const bool upper = (lane & h) != 0;
-      const C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+      const C<T> w = conj_<T>(lt.st[i]);
       C<T> o = shfl_xor<T>(x[0], h);
       x[0] = upper ? csub<T>(o, cmul<T>(x[0], w)) : cadd<T>(x[0], cmul<T>(o, w));
     }
   } else {
     constexpr int H2 = E / 2;
 #pragma unroll
-    for (int h = 1; h <= 16; h <<= 1) {
+    for (int i = 4; i >= 0; --i) {
+      const int h = 16 >> i;
       const bool upper = (lane & h) != 0;
-      C<T> w = tw_get<T>(tw, (lane & (h - 1)) * (P / (2 * h)), true);
+      C<T> w = conj_<T>(lt.st[i]);
       if (upper) w = mk<T>(-w.x, -w.y);
 #pragma unroll
       for (int j = 0; j < H2; ++j) {
@@ -260,7 +281,7 @@ __device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const C<T>* __restric
     }
   }
 #pragma unroll
-  for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], tw[(lane * q) & (P - 1)]);
+  for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], lt.rq[q]);
   reg_dft<T, E, +1>(x);
 }
 

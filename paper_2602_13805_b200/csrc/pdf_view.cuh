@@ -66,8 +66,8 @@ template <typename T>
 struct ViewSmem {
   C<T>* tw;     // P
   C<T>* twm;    // M
-  C<T>* bufA;   // M * (P/CS)
-  C<T>* bufB;   // (M/CS) * P
+  C<T>* bufA;   // M * (P/CS + 1)   (rows padded by one element: conflict-free column reads)
+  C<T>* bufB;   // (M/CS) * (P + 1)
   C<T>* rows;   // (M/CS) * M
   C<T>* small;  // M0 + (M/CS)*K : A (spectral grid) then V / U
   // followed by xch: max(CS*R, M0) partial-sum exchange (read remotely)
@@ -79,7 +79,7 @@ __host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) 
   const int rp = M / CS;
   size_t a = (size_t)M0 + (size_t)rp * K;
   size_t xch = (size_t)CS * R > (size_t)M0 ? (size_t)CS * R : (size_t)M0;
-  size_t n = (size_t)P + M + (size_t)M * (P / CS) + (size_t)rp * P + (size_t)rp * M + a + xch;
+  size_t n = (size_t)P + M + (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M + a + xch;
   return n * sizeof(C<T>) + 64 * sizeof(double);
 }
 
@@ -103,7 +103,7 @@ __device__ inline double block_sum_d(double v, double* red) {
 }
 
 template <typename T, int E, int MODE>
-__global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a) {
+__global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int P = 32 * E;
   cg::cluster_group cluster = cg::this_cluster();
@@ -124,8 +124,9 @@ __global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a)
   C<T>* p = reinterpret_cast<C<T>*>(smem_raw);
   s.tw = p; p += P;
   s.twm = p; p += M;
-  s.bufA = p; p += (size_t)M * cp;
-  s.bufB = p; p += (size_t)rp * P;
+  const int cpp = cp + 1, Pp = P + 1;       // padded pitches of the transpose buffers
+  s.bufA = p; p += (size_t)M * cpp;
+  s.bufB = p; p += (size_t)rp * Pp;
   s.rows = p; p += (size_t)rp * M;
   s.small = p; p += (size_t)M0 + (size_t)rp * K;
   C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)M0 ? (size_t)CS * a.R : (size_t)M0);
@@ -134,6 +135,9 @@ __global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a)
   for (int i = tid; i < P; i += blockDim.x) s.tw[i] = a.twP[i];
   for (int i = tid; i < M; i += blockDim.x) s.twm[i] = a.twM[i];
   const size_t img = (size_t)M * M;
+  __syncthreads();
+  LaneTw<T, E> ltw;
+  ltw.load(s.tw, lane);
   pdl_wait();   // everything below reads the previous kernel's outputs
 
   // ---------------- stage 0: my input rows -> s.rows ----------------------
@@ -190,13 +194,13 @@ __global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a)
       const int col = lane + 32 * k;
       x[k] = (k < KH && lane_ok) ? s.rows[yl * M + col] : czero<T>();
     }
-    warp_fft_fwd<T, E>(x, s.tw, lane);
+    warp_fft_fwd<T, E>(x, ltw, lane);
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int pos = q * 32 + lane;
       const int dst = pos / cp, lc = pos - dst * cp;
       C<T>* rb = cluster.map_shared_rank(s.bufA, dst);
-      rb[(size_t)(y0 + yl) * cp + lc] = x[q];
+      rb[(size_t)(y0 + yl) * cpp + lc] = x[q];
     }
   }
 
@@ -254,24 +258,24 @@ __global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a)
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const int row = lane + 32 * k;
-      x[k] = (k < KH && lane_ok) ? s.bufA[(size_t)row * cp + cc] : czero<T>();
+      x[k] = (k < KH && lane_ok) ? s.bufA[(size_t)row * cpp + cc] : czero<T>();
     }
     // the kernel spectrum column is fetched before the FFT so its latency hides
     const C<T>* kh = a.khat + (size_t)posc * P;
     C<T> kv[E];
 #pragma unroll
     for (int q = 0; q < E; ++q) kv[q] = kh[q * 32 + lane];
-    warp_fft_fwd<T, E>(x, s.tw, lane);
+    warp_fft_fwd<T, E>(x, ltw, lane);
 #pragma unroll
     for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kv[q]);
-    warp_fft_inv<T, E>(x, s.tw, lane);
+    warp_fft_inv<T, E>(x, ltw, lane);
 #pragma unroll
     for (int k = 0; k < KH; ++k) {
       if (!lane_ok) break;
       const int y = lane + 32 * k;
       const int dst = y / rp, yl = y - dst * rp;
       C<T>* rb = cluster.map_shared_rank(s.bufB, dst);
-      rb[(size_t)yl * P + posc] = x[k];
+      rb[(size_t)yl * Pp + posc] = x[k];
     }
   }
   cluster.sync();
@@ -281,8 +285,8 @@ __global__ void __launch_bounds__(E <= 4 ? 512 : 256) view_kernel(ViewArgs<T> a)
   for (int yl = warp; yl < rp; yl += nw) {
     C<T> x[E];
 #pragma unroll
-    for (int q = 0; q < E; ++q) x[q] = s.bufB[(size_t)yl * P + q * 32 + lane];
-    warp_fft_inv<T, E>(x, s.tw, lane);
+    for (int q = 0; q < E; ++q) x[q] = s.bufB[(size_t)yl * Pp + q * 32 + lane];
+    warp_fft_inv<T, E>(x, ltw, lane);
     const size_t rowoff = (size_t)v * img + (size_t)(y0 + yl) * M;
 #pragma unroll
     for (int k = 0; k < KH; ++k) {
