@@ -22,6 +22,8 @@
  *   pdf_expand          expand                          spectral.py:68-79
  *   pdf_truncate        truncate                        spectral.py:56-65
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
+ *   pdf_shard_step_a/b/c  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
+ *                       (views split over ranks, caller all-reduces between the steps)
  *   pdf_get_error       PoleError / FloatingPointError  cie.py:27-29, losses.py:239-243,
  *                                                       network.py:221-222, 260-261
  *
@@ -140,6 +142,21 @@ int pdf_apply_cco(pdf_ctx* ctx, const void* chi, void* out, int32_t count, doubl
 int pdf_profile_train(pdf_ctx* ctx, void* theta, void* m, void* v, int32_t t0, int32_t iters, float* ms,
                       void* stream);
 int pdf_fp64_probe(double* gflops, void* stream);
+
+/* incidence sharding (one large scene, views split over ranks).
+ * The context is created for this rank's views only (desc.n = own views, c_inc / c_sca
+ * GLOBAL via pdf_set_norms).  One iteration =
+ *   pdf_shard_step_a  -> all-reduce red1: SUM over [0, 3 m1 m2) per scene, MAX of the last entry
+ *   pdf_shard_step_b  -> all-reduce red2: SUM
+ *   pdf_shard_step_c  -> all-reduce grad: SUM, then pdf_adam_step on every rank
+ * red1 / red2 are caller-owned float64 device buffers (sizes from pdf_shard_buffer_sizes);
+ * the collective is the caller's (NCCL over NVLink via torch.distributed). */
+int pdf_net_setup_sharded(pdf_ctx* ctx, const void* alpha0_all, int32_t n_all, int32_t view_offset, void* stream);
+int pdf_shard_buffer_sizes(const pdf_ctx* ctx, int64_t* red1_doubles, int64_t* red2_doubles);
+int pdf_shard_step_a(pdf_ctx* ctx, const void* theta, double* red1, void* stream);
+int pdf_shard_step_b(pdf_ctx* ctx, const double* red1, double* red2, void* chi_out, void* stream);
+int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* grad, double* breakdown,
+                     void* stream);
 
 /* copies the per-scene sticky error words to host (synchronises stream), then clears them */
 int pdf_get_error(pdf_ctx* ctx, int32_t* err_host, void* stream);

@@ -12,6 +12,7 @@
 #include "pdf_common.cuh"
 #include "pdf_net.cuh"
 #include "pdf_pixel.cuh"
+#include "pdf_shard.cuh"
 #include "pdf_view.cuh"
 
 using namespace pdf;
@@ -60,7 +61,7 @@ struct pdf_ctx {
   // workspace
   void *khat, *twP, *twM, *J, *E_, *gJ, *gE, *grows, *alpha0, *alpha_hat, *galpha;
   void *x0, *cout, *h1, *h2, *gy, *gz2, *gz1, *ab;
-  double *norms, *dloss, *part, *bd;
+  double *norms, *dloss, *part, *bd, *pix;
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
   double *c_inc, *c_sca;
@@ -95,6 +96,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->gz2 = w.take<T>((size_t)d.S * c->rows * c->H);
   c->gz1 = w.take<T>((size_t)d.S * c->rows * c->H);
   c->ab = w.take<T>((size_t)d.S * 4 * img);
+  c->pix = w.take<double>((size_t)d.S * img * 12);
   c->norms = w.take<double>(SN * c->CS);
   c->dloss = w.take<double>(SN);
   c->part = w.take<double>((size_t)d.S * c->ntiles * 4);
@@ -524,12 +526,16 @@ extern "C" int pdf_loss_value(pdf_ctx* c, const void* alpha, double* bd, void* c
 }
 
 template <typename T>
-static int net_setup_impl(pdf_ctx* c, const void* alpha0, cudaStream_t st) {
-  const size_t bytes = (size_t)c->d.S * c->d.n * c->M0 * sizeof(C<T>);
-  CK_CUDA(cudaMemcpyAsync(c->alpha0, alpha0, bytes, cudaMemcpyDeviceToDevice, st));
+static int net_setup_impl(pdf_ctx* c, const void* alpha0, int n_all, int off, cudaStream_t st) {
+  // keep this context's own views of alpha0 (the network output adds them back)
+  const size_t row = (size_t)c->M0 * sizeof(C<T>);
+  for (int s_ = 0; s_ < c->d.S; ++s_)
+    CK_CUDA(cudaMemcpyAsync((char*)c->alpha0 + (size_t)s_ * c->d.n * row,
+                            (const char*)alpha0 + ((size_t)s_ * n_all + off) * row, c->d.n * row,
+                            cudaMemcpyDeviceToDevice, st));
   NetSetupArgs<T> a = {};
-  a.n = c->d.n; a.M0 = c->M0; a.joint = c->d.joint; a.H = c->H;
-  a.alpha0 = (const C<T>*)c->alpha0; a.x0 = (T*)c->x0; a.cout = (T*)c->cout;
+  a.n = c->d.n; a.M0 = c->M0; a.joint = c->d.joint; a.H = c->H; a.n_all = n_all; a.off = off;
+  a.alpha0 = (const C<T>*)alpha0; a.x0 = (T*)c->x0; a.cout = (T*)c->cout;
   net_setup_kernel<T><<<c->d.S, 256, 0, st>>>(a);
   CK_CUDA(cudaGetLastError());
   return PDF_OK;
@@ -537,7 +543,7 @@ static int net_setup_impl(pdf_ctx* c, const void* alpha0, cudaStream_t st) {
 
 extern "C" int pdf_net_setup(pdf_ctx* c, const void* alpha0, void* stream) {
   if (!c || !alpha0) return fail(PDF_EINVAL, "null argument");
-  return DISPATCH(c, net_setup_impl, c, alpha0, (cudaStream_t)stream);
+  return DISPATCH(c, net_setup_impl, c, alpha0, c->d.n, 0, (cudaStream_t)stream);
 }
 
 template <typename T>
@@ -804,4 +810,96 @@ extern "C" int pdf_fp64_probe(double* gflops, void* stream) {
   cudaFreeAsync(out, st);
   *gflops = 2.0 * 64.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e9;
   return PDF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// incidence-sharded iteration; see pdf_shard.cuh
+
+extern "C" int pdf_net_setup_sharded(pdf_ctx* c, const void* alpha0_all, int32_t n_all, int32_t view_offset,
+                                     void* stream) {
+  if (!c || !alpha0_all || c->d.joint || view_offset < 0 || view_offset + c->d.n > n_all)
+    return fail(PDF_EINVAL, "bad sharded network setup (joint_views cannot be sharded)");
+  return DISPATCH(c, net_setup_impl, c, alpha0_all, n_all, view_offset, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_shard_buffer_sizes(const pdf_ctx* c, int64_t* red1, int64_t* red2) {
+  if (!c) return fail(PDF_EINVAL, "null ctx");
+  const int64_t img = (int64_t)c->M * c->M;
+  if (red1) *red1 = (int64_t)c->d.S * (3 * img + 1);
+  if (red2) *red2 = (int64_t)c->d.S * (2 * img + 2);
+  return PDF_OK;
+}
+
+template <typename T>
+static ShardArgs<T> shard_args(pdf_ctx* c, double* red1, double* red2) {
+  ShardArgs<T> a = {};
+  a.M = c->M; a.n = c->d.n; a.R = c->d.R; a.CS = c->CS;
+  a.beta = (T)c->d.beta; a.l1 = (T)c->d.lambda1; a.l2 = (T)c->d.lambda2; a.l3 = (T)c->d.lambda3;
+  a.tau = (T)c->d.tau_b;
+  a.J = (const C<T>*)c->J; a.E = (const C<T>*)c->E_; a.norms = c->norms; a.grows = (const C<T>*)c->grows;
+  a.gs = (const C<T>*)c->d.gs_matrix; a.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
+  a.c_inc = c->c_inc; a.red1 = red1; a.red2 = red2; a.dloss = c->dloss; a.pix = c->pix; a.part = c->part;
+  a.gJ = (C<T>*)c->gJ; a.gE = (C<T>*)c->gE; a.err = c->err;
+  return a;
+}
+
+template <typename T>
+static int shard_a_impl(pdf_ctx* c, const void* theta, double* red1, cudaStream_t st) {
+  TRY(net_forward_all<T>(c, theta, nullptr, st));
+  TRY(phys_forward<T>(c, c->alpha_hat, st));
+  ShardArgs<T> a = shard_args<T>(c, red1, nullptr);
+  const int img = c->M * c->M;
+  void* args[] = {&a};
+  CK_CUDA(plain_launch(shard_numden_kernel<T>, dim3((img + 255) / 256, c->d.S), dim3(256), 0, st, args));
+  return PDF_OK;
+}
+
+template <typename T>
+static int shard_b_impl(pdf_ctx* c, const double* red1, double* red2, void* chi_out, cudaStream_t st) {
+  ShardArgs<T> a = shard_args<T>(c, const_cast<double*>(red1), red2);
+  a.chi_out = (C<T>*)chi_out;
+  void* args[] = {&a};
+  const dim3 grid(c->M / c->TX, c->M, c->d.S);
+  CK_CUDA(plain_launch(shard_pixel_a_kernel<T>, grid, dim3(PIX_NW * 32), 0, st, args));
+  shard_loss_sums_kernel<<<c->d.S, 128, 0, st>>>(c->part, c->dloss, red2, c->ntiles, c->d.n,
+                                                 (size_t)c->M * c->M);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
+}
+
+template <typename T>
+static int shard_c_impl(pdf_ctx* c, const void* theta, const double* red2, void* grad, double* bd, cudaStream_t st) {
+  ShardArgs<T> a = shard_args<T>(c, nullptr, const_cast<double*>(red2));
+  void* args[] = {&a};
+  const dim3 grid(c->M / c->TX, c->M, c->d.S);
+  CK_CUDA(plain_launch(shard_pixel_b_kernel<T>, grid, dim3(PIX_NW * 32), 0, st, args));
+  TRY(phys_backward<T>(c, nullptr, c->gy, st));
+  FinalizeArgs f = fin_args(c, bd, nullptr);
+  shard_finalize_kernel<<<c->d.S, 128, 0, st>>>(f, red2, (size_t)c->M * c->M);
+  CK_CUDA(cudaGetLastError());
+  const Offs o = offsets(c);
+  T* th = (T*)const_cast<void*>(theta);
+  TRY(net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, nullptr, nullptr,
+                       (T*)grad, 0, (T*)c->gz2, st));
+  TRY(net_bwd_layer<T>(c, (const T*)c->gz2, (const T*)c->h1, c->H, c->H, th, o.w2, o.b2, nullptr, nullptr,
+                       (T*)grad, 0, (T*)c->gz1, st));
+  TRY(net_bwd_layer<T>(c, (const T*)c->gz1, (const T*)c->x0, c->D0, c->H, th, o.w1, o.b1, nullptr, nullptr,
+                       (T*)grad, 0, nullptr, st));
+  return PDF_OK;
+}
+
+extern "C" int pdf_shard_step_a(pdf_ctx* c, const void* theta, double* red1, void* stream) {
+  if (!c || !theta || !red1 || c->d.joint) return fail(PDF_EINVAL, "bad argument");
+  return DISPATCH(c, shard_a_impl, c, theta, red1, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_shard_step_b(pdf_ctx* c, const double* red1, double* red2, void* chi_out, void* stream) {
+  if (!c || !red1 || !red2) return fail(PDF_EINVAL, "bad argument");
+  return DISPATCH(c, shard_b_impl, c, red1, red2, chi_out, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_shard_step_c(pdf_ctx* c, const void* theta, const double* red2, void* grad, double* breakdown,
+                                void* stream) {
+  if (!c || !theta || !red2 || !grad) return fail(PDF_EINVAL, "bad argument");
+  return DISPATCH(c, shard_c_impl, c, theta, red2, grad, breakdown, (cudaStream_t)stream);
 }

@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(BwdShape<T, RB>::THR, RB == 1 ? 2 : 1) net_bwd
 template <typename T>
 struct NetSetupArgs {
   int n, M0, joint, H;
-  const C<T>* alpha0;   // [S][n][M0]
+  int n_all, off;       // alpha0 holds n_all views; this context's rows are views [off, off+n)
+  const C<T>* alpha0;   // [S][n_all][M0]
   T* x0;                // [S][rows][D0]
   T* cout;              // [S][D0]
 };
@@ -486,20 +487,20 @@ struct NetSetupArgs {
 template <typename T>
 __global__ void net_setup_kernel(NetSetupArgs<T> a) {
   const int scene = blockIdx.x, tid = threadIdx.x;
-  const int n = a.n, M0 = a.M0;
-  const C<T>* al = a.alpha0 + (size_t)scene * n * M0;
+  const int n = a.n, M0 = a.M0, na = a.n_all;
+  const C<T>* al = a.alpha0 + (size_t)scene * na * M0;
   __shared__ double red[32];
   __shared__ double gl_s;
   // global mean |alpha|^2 (fixed order)
   double loc = 0.0;
-  for (int i = tid; i < n * M0; i += blockDim.x) loc += (double)cabs2<T>(al[i]);
+  for (int i = tid; i < na * M0; i += blockDim.x) loc += (double)cabs2<T>(al[i]);
   loc = warp_sum<double>(loc);
   if ((tid & 31) == 0) red[tid >> 5] = loc;
   __syncthreads();
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    gl_s = sqrt(s / (double)(n * M0));
+    gl_s = sqrt(s / (double)(na * M0));
   }
   __syncthreads();
   const double glob = gl_s;
@@ -512,14 +513,14 @@ __global__ void net_setup_kernel(NetSetupArgs<T> a) {
     double sc = 1.0;
     if (glob != 0.0) {
       double acc = 0.0;
-      for (int i = 0; i < n; ++i) acc += (double)cabs2<T>(al[(size_t)i * M0 + m]);
-      const double mode = sqrt(acc / n);
+      for (int i = 0; i < na; ++i) acc += (double)cabs2<T>(al[(size_t)i * M0 + m]);
+      const double mode = sqrt(acc / na);
       sc = pow(mode, 0.7) * pow(glob, 1.0 - 0.7);
       const double fl = 0.1 * glob;
       sc = sc > fl ? sc : fl;
     }
     for (int i = 0; i < n; ++i) {
-      const C<T> z = al[(size_t)i * M0 + m];
+      const C<T> z = al[(size_t)(a.off + i) * M0 + m];
       const int row = a.joint ? 0 : i;
       const int fre = a.joint ? i * M0 + m : m;
       x0[(size_t)row * D0 + fre] = (T)(z.x / sc);

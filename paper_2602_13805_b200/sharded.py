@@ -1,0 +1,163 @@
+"""Incidence sharding for one large scene (BASELINE config 5).
+
+The views of a scene are split over ranks (`shard.shard_range`).  Every rank
+holds the full network (replicated parameters and Adam state) and runs the
+physics for its own views only.  One PDF iteration then needs three
+reductions, which the library exposes as float64 device buffers and the
+caller performs (NCCL over NVLink through torch.distributed on the B200 box):
+
+  red1 : per-pixel sum_i J_i conj(E_i), sum_i |E_i|^2 (SUM) and the max view
+         power for eps_reg (MAX)                     -- cie.py:42-80
+  red2 : per-pixel g_R = sum_i conj(P_i) g_S_i and the state / data loss sums
+         (SUM)                                       -- losses.py:227,232,293
+  grad : the flat network gradient (SUM), after which every rank applies the
+         same Adam step                              -- network.py:220, 248-264
+
+The one-time initialisation (bp_initialize, init_alpha) is replicated on
+every rank over all views.  `LocalShards` runs several shards in one process
+(the reductions become plain sums) so a single GPU can check the sharded
+algebra against the unsharded path; `TorchDistReducer` is the multi-GPU form.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .engine import DeviceProblem, _ptr, _stream
+from .shard import shard_range
+
+
+class IncidenceShard:
+    """This rank's slice of the views of one scene, resident on the GPU."""
+
+    def __init__(self, ops, e_inc_all, data_all, *, mf, beta, lambdas, tau_b, rank, world, mask=None,
+                 lr=1e-2, dtype="f64"):
+        e_inc_all = np.asarray(e_inc_all)
+        data_all = np.asarray(data_all)
+        self.n_all = e_inc_all.shape[0]
+        own = shard_range(self.n_all, rank, world)
+        if len(own) == 0:
+            raise ValueError("more ranks than incidences")
+        self.own = own
+        kw = dict(mf=mf, beta=beta, lambdas=lambdas, tau_b=tau_b, lr=lr, dtype=dtype)
+        mk = None if mask is None else np.asarray(mask)
+        # one-time initialisation over all views (replicated)
+        full = DeviceProblem(ops, e_inc_all, data_all, mask=mk, **kw)
+        self.chi0, r0 = full.bp_initialize()
+        self.alpha0_all = full.init_alpha(r0)
+        c_inc, c_sca = full.c_inc, full.c_sca
+        del full
+        sl = slice(own.start, own.stop)
+        self.dev = DeviceProblem(ops, np.ascontiguousarray(e_inc_all[sl]), np.ascontiguousarray(data_all[sl]),
+                                 mask=None if mk is None else np.ascontiguousarray(mk[sl]), **kw)
+        self.dev.set_norms(c_inc, c_sca)          # normalisers over ALL views (losses.py:67-76)
+        N.check(self.dev.lib.pdf_net_setup_sharded(self.dev.ctx, _ptr(self.alpha0_all), self.n_all, own.start,
+                                                   _stream()))
+        r1, r2 = ct.c_int64(), ct.c_int64()
+        N.check(self.dev.lib.pdf_shard_buffer_sizes(self.dev.ctx, ct.byref(r1), ct.byref(r2)))
+        dd = self.dev.device
+        self.red1 = torch.zeros(r1.value, dtype=torch.float64, device=dd)
+        self.red2 = torch.zeros(r2.value, dtype=torch.float64, device=dd)
+        self.img = self.dev.M * self.dev.M
+        self.bd = torch.zeros(1, 6, dtype=torch.float64, device=dd)
+
+    # the three segments of one iteration
+    def step_a(self, theta):
+        N.check(self.dev.lib.pdf_shard_step_a(self.dev.ctx, _ptr(theta), _ptr(self.red1), _stream()))
+
+    def step_b(self, chi_out=None):
+        N.check(self.dev.lib.pdf_shard_step_b(self.dev.ctx, _ptr(self.red1), _ptr(self.red2), _ptr(chi_out),
+                                              _stream()))
+
+    def step_c(self, theta, grad):
+        N.check(self.dev.lib.pdf_shard_step_c(self.dev.ctx, _ptr(theta), _ptr(self.red2), _ptr(grad),
+                                              _ptr(self.bd), _stream()))
+
+    def red1_sum_max(self):
+        """(slice reduced with SUM, slice reduced with MAX) of red1."""
+        return self.red1[: 3 * self.img], self.red1[3 * self.img:]
+
+
+class TorchDistReducer:
+    """Reductions over a torch.distributed group (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+
+    def __call__(self, shards, what):
+        d = self.dist
+        (s,) = shards
+        if what == "red1":
+            a, b = s.red1_sum_max()
+            d.all_reduce(a, op=d.ReduceOp.SUM, group=self.group)
+            d.all_reduce(b, op=d.ReduceOp.MAX, group=self.group)
+        elif what == "red2":
+            d.all_reduce(s.red2, op=d.ReduceOp.SUM, group=self.group)
+        else:
+            d.all_reduce(what, op=d.ReduceOp.SUM, group=self.group)
+
+
+class LocalShards:
+    """All shards of a scene in one process; reductions are fixed-order sums."""
+
+    def __call__(self, shards, what):
+        if what == "red1":
+            a = sum(s.red1_sum_max()[0] for s in shards)
+            b = torch.stack([s.red1_sum_max()[1] for s in shards]).max(dim=0).values
+            for s in shards:
+                s.red1[: 3 * s.img] = a
+                s.red1[3 * s.img:] = b
+        elif what == "red2":
+            t = sum(s.red2 for s in shards)
+            for s in shards:
+                s.red2.copy_(t)
+        else:   # list of gradient tensors, one per shard
+            t = sum(what)
+            for g in what:
+                g.copy_(t)
+
+
+def run_sharded(shards, reduce, theta0, k_iters: int, lr: float = 1e-2):
+    """k incidence-sharded Adam iterations for the given (local) shards.
+
+    Returns (thetas per shard, trace [k][6]).  Every shard keeps its own copy
+    of the replicated parameters and Adam state."""
+    thetas = [theta0.clone() for _ in shards]
+    ms = [torch.zeros_like(theta0) for _ in shards]
+    vs = [torch.zeros_like(theta0) for _ in shards]
+    grads = [torch.zeros_like(theta0) for _ in shards]
+    trace = []
+    for t in range(1, k_iters + 1):
+        for s, th in zip(shards, thetas):
+            s.step_a(th)
+        reduce(shards, "red1")
+        for s in shards:
+            s.step_b()
+        reduce(shards, "red2")
+        for s, th, g in zip(shards, thetas, grads):
+            s.step_c(th, g)
+        if isinstance(reduce, LocalShards):
+            reduce(shards, grads)
+        else:
+            for g in grads:
+                reduce(shards, g)
+        trace.append(shards[0].bd[0].cpu().numpy().copy())
+        for s, th, m, v, g in zip(shards, thetas, ms, vs, grads):
+            s.dev.adam_step(th, m, v, g, t)
+    for s in shards:
+        s.dev.check_errors()
+    return thetas, np.array(trace)
+
+
+def sharded_chi(shards, reduce, thetas):
+    """Recovered contrast at the current parameters (cie.py:83-99) via the sharded forward."""
+    for s, th in zip(shards, thetas):
+        s.step_a(th)
+    reduce(shards, "red1")
+    chi = torch.empty(1, shards[0].dev.M, shards[0].dev.M, dtype=shards[0].dev.cdt, device=shards[0].dev.device)
+    shards[0].step_b(chi)
+    return chi[0]

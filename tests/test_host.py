@@ -205,3 +205,43 @@ def test_scene_sharding_with_gloo_world_size_2(tmp_path):
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=240)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "OK 2.0" in out.stdout
+
+
+_REDUCER = r'''
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch, torch.distributed as dist
+from paper_2602_13805_b200.sharded import TorchDistReducer
+dist.init_process_group("gloo")
+r = dist.get_rank()
+
+class Fake:                      # the reduction buffers of one IncidenceShard (img = 4 pixels)
+    img = 4
+    def __init__(self):
+        self.red1 = torch.arange(13, dtype=torch.float64) + 100 * r
+        self.red1[-1] = 7.0 + r          # max view power
+        self.red2 = torch.full((10,), 1.0 + r, dtype=torch.float64)
+    def red1_sum_max(self):
+        return self.red1[:12], self.red1[12:]
+
+s = Fake()
+red = TorchDistReducer()
+red([s], "red1"); red([s], "red2")
+g = torch.full((5,), float(r + 1), dtype=torch.float64); red([s], g)
+assert s.red1[:12].tolist() == [2 * i + 100 for i in range(12)], s.red1
+assert s.red1[12].item() == 8.0
+assert s.red2.tolist() == [3.0] * 10 and g.tolist() == [3.0] * 5
+if r == 0:
+    print("REDUCER OK")
+dist.destroy_process_group()
+'''
+
+
+def test_incidence_shard_reducer_with_gloo(tmp_path):
+    script = tmp_path / "r.py"
+    script.write_text(_REDUCER)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", str(script), ROOT]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "REDUCER OK" in out.stdout
