@@ -1,5 +1,6 @@
 // C-ABI implementation (see include/pdf_abi.h): context, workspace plan,
 // kernel dispatch and the CUDA-graph replay of the training loop.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -14,6 +15,7 @@
 #include "pdf_pixel.cuh"
 #include "pdf_shard.cuh"
 #include "pdf_view.cuh"
+#include "pdf_view_large.cuh"
 
 using namespace pdf;
 
@@ -41,6 +43,8 @@ static int fail(int code, const std::string& msg) {
       return fail(PDF_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));   \
   } while (0)
 
+#define TRY(x) do { int r_ = (x); if (r_ != PDF_OK) return r_; } while (0)
+
 struct Ws {
   size_t off = 0;
   char* base = nullptr;
@@ -56,12 +60,16 @@ struct Ws {
 struct pdf_ctx {
   pdf_desc d;
   int M, P, E, K, M0, CS, rows, D0, H, RB, TX, ntiles;
+  // large-grid view path (pdf_view_large.cuh): partials per view, views per
+  // spectrum chunk, data-GEMM pixel chunking
+  int large, NPV, chunk, dg_chunk, dg_nchunks;
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
   void *khat, *twP, *twM, *J, *E_, *gJ, *gE, *grows, *alpha0, *alpha_hat, *galpha;
   void *x0, *cout, *h1, *h2, *gy, *gz2, *gz1, *ab;
   double *norms, *dloss, *part, *bd, *pix;
+  void *spec, *gpart, *dpart;
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
   double *c_inc, *c_sca;
@@ -97,7 +105,14 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->gz1 = w.take<T>((size_t)d.S * c->rows * c->H);
   c->ab = w.take<T>((size_t)d.S * 4 * img);
   c->pix = w.take<double>((size_t)d.S * img * 12);
-  c->norms = w.take<double>(SN * c->CS);
+  c->norms = w.take<double>(SN * c->NPV);
+  if (c->large) {
+    c->spec = w.take<C<T>>((size_t)c->chunk * c->P * c->M);
+    c->gpart = w.take<C<T>>(SN * c->NPV * c->M0);
+    c->dpart = w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R);
+  } else {
+    c->spec = c->gpart = c->dpart = nullptr;
+  }
   c->dloss = w.take<double>(SN);
   c->part = w.take<double>((size_t)d.S * c->ntiles * 4);
   c->bd = w.take<double>((size_t)d.S * 6);
@@ -113,8 +128,8 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   if (d->dtype != PDF_F64 && d->dtype != PDF_F32) return fail(PDF_EINVAL, "dtype");
   if (d->m1 != d->m2) return fail(PDF_EINVAL, "only square grids (m1 == m2) are supported");
   const int M = d->m1;
-  if (M != 16 && M != 32 && M != 64 && M != 128)
-    return fail(PDF_EINVAL, "grid size must be a power of two in [16, 128]");
+  if (M != 16 && M != 32 && M != 64 && M != 128 && M != 256)
+    return fail(PDF_EINVAL, "grid size must be a power of two in [16, 256]");
   if (d->mf < 1 || 2 * d->mf > M) return fail(PDF_EINVAL, "need 1 <= m_f and 2 m_f <= m1");
   if (d->S < 1 || d->n < 1 || d->R < 1) return fail(PDF_EINVAL, "S, n, R must be >= 1");
   c->d = *d;
@@ -133,6 +148,24 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   if (c->RB > 5) return fail(PDF_EINVAL, "at most 80 network rows (incidences) supported");
   c->TX = M < 32 ? M : 32;
   c->ntiles = (M / c->TX) * M;
+  // M = 256 needs the multi-pass spectrum path; PDF_VIEW_LARGE=1 forces it for
+  // M >= 32 (cross-checks the two paths on the small configs)
+  c->large = M >= 256 || (env_int("PDF_VIEW_LARGE", 0) && M >= 32);
+  c->NPV = c->large ? M / VL_ROWS : c->CS;
+  c->chunk = c->dg_chunk = c->dg_nchunks = 0;
+  if (c->large) {
+    const size_t csz = d->dtype == PDF_F64 ? 16 : 8;
+    const long long budget = (long long)env_int("PDF_SPEC_MIB", 48) << 20;   // L2-resident spectrum chunk
+    const long long per = (long long)2 * M * M * csz;
+    long long ch = std::max(1LL, budget / per);
+    c->chunk = (int)std::min<long long>(ch, (long long)d->S * d->n);
+    const int npix = M * M;
+    int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
+    want = std::min(want, npix / DG_KC);
+    c->dg_chunk = ((npix + want - 1) / want + DG_KC - 1) / DG_KC * DG_KC;
+    c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
+    if (d->n > 80 || d->R > 80) return fail(PDF_EINVAL, "at most 80 incidences / receivers on the large-grid path");
+  }
   c->rsz = d->dtype == PDF_F64 ? 8 : 4;
   c->csz = 2 * c->rsz;
   if (d->freeze_r && !d->r_fixed) return fail(PDF_EINVAL, "freeze_r requires r_fixed");
@@ -229,8 +262,85 @@ static ViewArgs<T> view_common(pdf_ctx* c) {
   return a;
 }
 
+// ---------------------------------------------------------------------------
+// large-grid path: rows / cols / out passes per chunk of views
+template <typename T>
+static VLArgs<T> vl_common(pdf_ctx* c) {
+  VLArgs<T> a = {};
+  a.M = c->M; a.mf = c->d.mf; a.R = c->d.R; a.n = c->d.n; a.NPV = c->NPV;
+  a.khat = (const C<T>*)c->khat; a.twP = (const C<T>*)c->twP; a.twM = (const C<T>*)c->twM;
+  a.spec = (C<T>*)c->spec;
+  return a;
+}
+
+template <typename T, int E, int MODE>
+static cudaError_t vl_chunk(pdf_ctx* c, VLArgs<T>& a, int cnt, cudaStream_t st) {
+  constexpr int P = 32 * E, M = P / 2;
+  void* args[] = {&a};
+  cudaError_t e = plain_launch(vl_rows_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256),
+                               vl_rows_smem<T>(E, c->d.mf), st, args);
+  if (e == cudaSuccess) e = plain_launch(vl_cols_kernel<T, E>, dim3(P / 8, cnt), dim3(256), 0, st, args);
+  if (e == cudaSuccess)
+    e = plain_launch(vl_out_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256), vl_out_smem<T>(E, c->d.mf), st,
+                     args);
+  return e;
+}
+
+template <typename T, int MODE>
+static int vl_conv(pdf_ctx* c, VLArgs<T>& a, int count, cudaStream_t st) {
+  for (int v0 = 0; v0 < count; v0 += c->chunk) {
+    a.v0 = v0;
+    const int cnt = std::min(c->chunk, count - v0);
+    cudaError_t e;
+    switch (c->E) {
+      case 2: e = vl_chunk<T, 2, MODE>(c, a, cnt, st); break;
+      case 4: e = vl_chunk<T, 4, MODE>(c, a, cnt, st); break;
+      case 8: e = vl_chunk<T, 8, MODE>(c, a, cnt, st); break;
+      case 16: e = vl_chunk<T, 16, MODE>(c, a, cnt, st); break;
+      default: return fail(PDF_EINVAL, "unsupported FFT size on the large-grid path");
+    }
+    if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("large view pass: ") + cudaGetErrorString(e));
+  }
+  return PDF_OK;
+}
+
+template <typename T>
+static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
+  VLArgs<T> a = vl_common<T>(c);
+  a.alpha = (const C<T>*)alpha_hat; a.J = (C<T>*)c->J;
+  a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
+  a.E = (C<T>*)c->E_; a.norms = c->norms;
+  TRY((vl_conv<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
+  DataArgs<T> g = {};
+  g.n = c->d.n; g.R = c->d.R; g.npix = c->M * c->M; g.chunk = c->dg_chunk; g.nchunks = c->dg_nchunks;
+  g.J = (const C<T>*)c->J; g.gs = (const C<T>*)c->d.gs_matrix; g.dpart = (C<T>*)c->dpart;
+  g.data = (const C<T>*)c->d.data; g.mask = (const T*)c->d.mask; g.c_sca = c->c_sca;
+  g.grows = (C<T>*)c->grows; g.dloss = c->dloss;
+  void* args[] = {&g};
+  cudaError_t e = plain_launch(data_gemm_kernel<T>, dim3(c->dg_nchunks, c->d.S), dim3(dg_threads<T>(g.n, g.R)),
+                               dg_smem<T>(g.n, g.R), st, args);
+  if (e == cudaSuccess) e = plain_launch(data_reduce_kernel<T>, dim3(c->d.S * c->d.n), dim3(128), 0, st, args);
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("data term: ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
+template <typename T>
+static int vl_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, const FinalizeArgs& fin, bool do_fin) {
+  VLArgs<T> a = vl_common<T>(c);
+  a.gE = (const C<T>*)c->gE; a.gJloc = (const C<T>*)c->gJ; a.gpart = (C<T>*)c->gpart;
+  TRY((vl_conv<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st)));
+  a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
+  a.fin = fin; a.do_fin = do_fin ? 1 : 0;
+  void* args[] = {&a};
+  cudaError_t e = plain_launch(vl_trunc_reduce_kernel<T>, dim3((c->M0 + 255) / 256, c->d.S * c->d.n), dim3(256), 0,
+                               st, args);
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("truncate reduce: ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
 template <typename T>
 static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
+  if (c->large) return vl_forward<T>(c, alpha_hat, st);
   ViewArgs<T> a = view_common<T>(c);
   a.alpha = (const C<T>*)alpha_hat;
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
@@ -243,7 +353,7 @@ static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
 template <typename T, bool GRAD>
 static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   PixelArgs<T> p = {};
-  p.M = c->M; p.n = c->d.n; p.R = c->d.R; p.CS = c->CS; p.S = c->d.S;
+  p.M = c->M; p.n = c->d.n; p.R = c->d.R; p.CS = c->NPV; p.S = c->d.S;
   p.beta = (T)c->d.beta; p.l1 = (T)c->d.lambda1; p.l2 = (T)c->d.lambda2; p.l3 = (T)c->d.lambda3;
   p.tau = (T)c->d.tau_b;
   p.J = (const C<T>*)c->J; p.E = (const C<T>*)c->E_; p.norms = c->norms; p.grows = (const C<T>*)c->grows;
@@ -273,6 +383,7 @@ static FinalizeArgs fin_args(pdf_ctx* c, double* bd, double* trace) {
 template <typename T>
 static int phys_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, double* bd = nullptr,
                          double* trace = nullptr, bool fin = false) {
+  if (c->large) return vl_backward<T>(c, galpha, gy, st, fin_args(c, bd, trace), fin);
   ViewArgs<T> a = view_common<T>(c);
   a.fin = fin_args(c, bd, trace);
   a.do_fin = fin ? 1 : 0;
@@ -384,7 +495,6 @@ static Offs offsets(const pdf_ctx* c) {
   return o;
 }
 
-#define TRY(x) do { int r_ = (x); if (r_ != PDF_OK) return r_; } while (0)
 
 template <typename T>
 static int net_forward_all(pdf_ctx* c, const void* theta, int* step, cudaStream_t st) {
@@ -647,6 +757,11 @@ extern "C" int pdf_train(pdf_ctx* c, void* theta, void* m, void* v, int32_t t0, 
 
 template <typename T>
 static int apply_gd_impl(pdf_ctx* c, const void* x, void* y, int count, int adjoint, cudaStream_t st) {
+  if (c->large) {
+    VLArgs<T> b = vl_common<T>(c);
+    b.x = (const C<T>*)x; b.y = (C<T>*)y; b.conj_in = adjoint; b.conj_out = adjoint;
+    return vl_conv<T, VIEW_APPLY>(c, b, count, st);
+  }
   ViewArgs<T> a = view_common<T>(c);
   a.x = (const C<T>*)x; a.y = (C<T>*)y; a.conj_in = adjoint; a.conj_out = adjoint;
   return launch_view<T, VIEW_APPLY>(c, a, count, st);
@@ -833,7 +948,7 @@ extern "C" int pdf_shard_buffer_sizes(const pdf_ctx* c, int64_t* red1, int64_t* 
 template <typename T>
 static ShardArgs<T> shard_args(pdf_ctx* c, double* red1, double* red2) {
   ShardArgs<T> a = {};
-  a.M = c->M; a.n = c->d.n; a.R = c->d.R; a.CS = c->CS;
+  a.M = c->M; a.n = c->d.n; a.R = c->d.R; a.CS = c->NPV;
   a.beta = (T)c->d.beta; a.l1 = (T)c->d.lambda1; a.l2 = (T)c->d.lambda2; a.l3 = (T)c->d.lambda3;
   a.tau = (T)c->d.tau_b;
   a.J = (const C<T>*)c->J; a.E = (const C<T>*)c->E_; a.norms = c->norms; a.grows = (const C<T>*)c->grows;

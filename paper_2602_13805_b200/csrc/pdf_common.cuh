@@ -203,17 +203,30 @@ template <typename T> __device__ __forceinline__ C<T> tw_get(const C<T>* tw, int
 //   rq[q]  = tw[(lane * q) mod P]         for the register-to-lane twiddle
 template <typename T, int E>
 struct LaneTw {
+  // E = 16 (P = 512) keeps the register-to-lane twiddles in the shared table:
+  // 16 more complex registers per thread would spill next to x[16]
+  static constexpr bool RQREG = E <= 8;
   C<T> st[5];
-  C<T> rq[E];
-  __device__ __forceinline__ void load(const C<T>* __restrict__ tw, int lane) {
+  C<T> rq[RQREG ? E : 1];
+  const C<T>* tw;
+  int ln;
+  __device__ __forceinline__ void load(const C<T>* __restrict__ tw_, int lane) {
     constexpr int P = 32 * E;
+    tw = tw_;
+    ln = lane;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       const int h = 16 >> i;
-      st[i] = tw[(lane & (h - 1)) * (P / (2 * h))];
+      st[i] = tw_[(lane & (h - 1)) * (P / (2 * h))];
     }
+    if constexpr (RQREG) {
 #pragma unroll
-    for (int q = 0; q < E; ++q) rq[q] = tw[(lane * q) & (P - 1)];
+      for (int q = 0; q < E; ++q) rq[q] = tw_[(lane * q) & (P - 1)];
+    }
+  }
+  __device__ __forceinline__ C<T> r(int q) const {
+    if constexpr (RQREG) return rq[q];
+    else return tw[(ln * q) & (32 * E - 1)];
   }
 };
 
@@ -221,7 +234,7 @@ template <typename T, int E>
 __device__ __forceinline__ void warp_fft_fwd(C<T> (&x)[E], const LaneTw<T, E>& lt, int lane) {
   reg_dft<T, E, -1>(x);
 #pragma unroll
-  for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], lt.rq[q]);
+  for (int q = 1; q < E; ++q) x[q] = cmul<T>(x[q], lt.r(q));
   if constexpr (E == 1) {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
@@ -281,7 +294,7 @@ __device__ __forceinline__ void warp_fft_inv(C<T> (&x)[E], const LaneTw<T, E>& l
     }
   }
 #pragma unroll
-  for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], lt.rq[q]);
+  for (int q = 1; q < E; ++q) x[q] = cmulc<T>(x[q], lt.r(q));
   reg_dft<T, E, +1>(x);
 }
 
@@ -294,6 +307,24 @@ __host__ __device__ inline int spectrum_slot_freq(int p, int s, int E) {
   const int L = ((p & 15) << 1) | (s >> (e - 1));
   const int R = ((p >> 4) << (e - 1)) | (s & ((1 << (e - 1)) - 1));
   return R + E * br5(L);
+}
+
+// max over views of sum_c norms[v][c] (fixed-order partial sums, exact max):
+// eps_reg's view power (cie.py:49-50).  Called by one full warp.
+__device__ __forceinline__ double warp_max_view_power(const double* norms, int n, int np) {
+  const int lane = threadIdx.x & 31;
+  double mx = -1.0;
+  for (int i = lane; i < n; i += 32) {
+    double pw = 0.0;
+    for (int c = 0; c < np; ++c) pw += norms[(size_t)i * np + c];
+    mx = pw > mx ? pw : mx;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double t = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = t > mx ? t : mx;
+  }
+  return mx;
 }
 
 // deterministic fixed-order warp sum

@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(BwdShape<T, RB>::THR, RB == 1 ? 2 : 1) net_bwd
         red[(sub * 16 + j) * COLS + col] = v_;
       }
       __syncthreads();
-      if (tid < 16 * COLS) {
-        const int j = tid / COLS, c = tid % COLS;
+      for (int e = tid; e < 16 * COLS; e += THR) {   // 16 * COLS exceeds THR when RB >= 4
+        const int j = e / COLS, c = e % COLS;
         T sum = T(0);
         for (int q = 0; q < SUB; ++q) sum += red[(q * 16 + j) * COLS + c];
         cpart[(rb + j) * COLS + c] = sum;

@@ -104,14 +104,9 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     cp_async_commit();
   }
 
-  if (tid == 0) {
-    double mx = 0.0;
-    for (int i = 0; i < n; ++i) {
-      double pw = 0.0;
-      for (int c = 0; c < a.CS; ++c) pw += a.norms[(vbase + i) * a.CS + c];
-      mx = i == 0 ? pw : (pw > mx ? pw : mx);
-    }
-    eps_s = 1e-10 * mx / (double)img;               // cie.py:49-50
+  if (warp == 0) {
+    const double mx = warp_max_view_power(a.norms + vbase * a.CS, n, a.CS);
+    if (lane == 0) eps_s = 1e-10 * mx / (double)img;   // cie.py:49-50
   }
 
   // ---- per-warp partial num/den on the halo --------------------------------

@@ -64,14 +64,9 @@ __global__ void shard_numden_kernel(ShardArgs<T> a) {
     r1[2 * p + 1] = num.y;
     r1[2 * img + p] = den;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double mx = 0.0;
-    for (int i = 0; i < n; ++i) {
-      double pw = 0.0;
-      for (int c = 0; c < a.CS; ++c) pw += a.norms[((size_t)scene * n + i) * a.CS + c];
-      mx = i == 0 ? pw : (pw > mx ? pw : mx);
-    }
-    r1[3 * img] = mx;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const double mx = warp_max_view_power(a.norms + (size_t)scene * n * a.CS, n, a.CS);
+    if (threadIdx.x == 0) r1[3 * img] = mx;
   }
 }
 

@@ -1,0 +1,442 @@
+// Large-grid view path (BASELINE config 5: M = 256, P = 512).
+//
+// A float64 P x P spectrum (4 MiB at P = 512) does not fit one cluster's
+// shared memory, so the zero-padded convolution of forward.py:140-146 runs
+// as three passes over a column-major spectrum buffer spec[view][P][M] that
+// stays L2-resident for a chunk of views:
+//
+//   rows pass : the M nonzero rows of the padded input (expand(alpha) in the
+//               forward, conj(g_E) in the adjoint), warp FFT each, write the
+//               permuted spectrum positions as columns (transposed through
+//               shared memory in 128-byte row segments)
+//   cols pass : per spectrum column: FFT of the M nonzero entries, x K^,
+//               inverse FFT, keep the first M entries -- in place
+//   out pass  : gather 8 rows, inverse row FFTs, crop to M columns, and the
+//               epilogue (E = E_inc + G_D J and ||E||^2 partials; or
+//               g_J = g_J_local + G_D^H g_E and the truncation partials)
+//
+// The data term D = J G_S^T - d (losses.py:229-232) is a tall complex GEMM
+// (views x pixels) x (pixels x receivers) here: data_gemm_kernel splits the
+// pixels over CTAs with register-tiled 4x4 outputs and a fixed-order reduce.
+// The warp FFT, the K^ permutation and every reduction order are the ones the
+// cluster path uses (pdf_view.cuh), so both paths are interchangeable; the
+// cluster path is kept for M <= 128 where its DSMEM transposes win.
+#pragma once
+#include "pdf_common.cuh"
+#include "pdf_pixel.cuh"
+#include "pdf_view.cuh"
+
+namespace pdf {
+
+constexpr int VL_ROWS = 8;   // rows per CTA in the rows / out passes (one per warp)
+
+template <typename T>
+struct VLArgs {
+  int M, mf, R, n, NPV;       // NPV = M / VL_ROWS partials per view
+  int v0;                      // first global view (scene * n + view) of this chunk
+  const C<T>* khat;            // permuted, 1/P^2-scaled kernel spectrum [P col pos][P row pos]
+  const C<T>* twP;
+  const C<T>* twM;
+  C<T>* spec;                  // [chunk views][P][M]
+  // rows pass
+  const C<T>* alpha;           // FWD  [S*n][M0]
+  C<T>* J;                     // FWD  [S*n][M][M]
+  const C<T>* gE;              // BWD
+  const C<T>* x;               // APPLY
+  int conj_in, conj_out;
+  // out pass
+  const C<T>* einc;
+  long long einc_scene_stride;
+  C<T>* E;
+  double* norms;               // [S*n][NPV]
+  const C<T>* gJloc;
+  C<T>* gpart;                 // [S*n][NPV][M0] truncation partials
+  C<T>* y;                     // APPLY
+  // truncation reduce
+  C<T>* galpha;
+  T* gy;
+  const T* cout;
+  int joint;
+  FinalizeArgs fin;
+  int do_fin;
+};
+
+template <typename T>
+__device__ __forceinline__ int vl_corner_freq(int u, int mf, int M) { return u < mf ? u : M - 2 * mf + u; }
+__device__ __forceinline__ int vl_corner_slot(int u, int v, int mf) {
+  return (((u / mf) * 2 + (v / mf)) * mf + (u % mf)) * mf + (v % mf);
+}
+
+template <typename T>
+__host__ __device__ inline size_t vl_rows_smem(int E, int mf) {
+  const int P = 32 * E, M = P / 2, K = 2 * mf;
+  return ((size_t)P + M + (size_t)P * (VL_ROWS + 1) + (size_t)K * K + (size_t)VL_ROWS * K) * sizeof(C<T>);
+}
+
+template <typename T>
+__host__ __device__ inline size_t vl_out_smem(int E, int mf) {
+  const int P = 32 * E, M = P / 2, K = 2 * mf;
+  (void)M;
+  return ((size_t)P + M + (size_t)VL_ROWS * (P + 1) + (size_t)VL_ROWS * K) * sizeof(C<T>) + 16 * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int E, int MODE>
+__global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
+  constexpr int P = 32 * E, M = P / 2, KH = E / 2, TP = VL_ROWS + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int mf = a.mf, K = 2 * mf, M0 = K * K;
+  C<T>* tw = reinterpret_cast<C<T>*>(smem_raw);
+  C<T>* twm = tw + P;
+  C<T>* tile = twm + M;                 // [P][TP]
+  C<T>* A = tile + P * TP;              // [K][K]
+  C<T>* V = A + M0;                     // [VL_ROWS][K]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int vr = blockIdx.y, v = a.v0 + vr, y0 = blockIdx.x * VL_ROWS, y = y0 + warp;
+  const size_t img = (size_t)M * M;
+  for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
+  __syncthreads();
+  LaneTw<T, E> ltw;
+  ltw.load(tw, lane);
+  pdl_wait();
+
+  C<T> x[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) x[k] = czero<T>();
+  if constexpr (MODE == VIEW_FWD) {
+    // J = expand(alpha) rows y0..y0+7 (spectral.py:68-79), separable direct sums
+    const C<T>* al = a.alpha + (size_t)v * M0;
+    for (int i = tid; i < M0; i += blockDim.x) A[i] = al[vl_corner_slot(i / K, i % K, mf)];
+    __syncthreads();
+    for (int i = tid; i < VL_ROWS * K; i += blockDim.x) {
+      const int yl = i / K, w = i % K, yy = y0 + yl;
+      C<T> acc = czero<T>();
+      for (int u = 0; u < K; ++u)
+        acc = cadd<T>(acc, cmulc<T>(A[u * K + w], twm[(vl_corner_freq<T>(u, mf, M) * yy) & (M - 1)]));
+      V[i] = acc;
+    }
+    __syncthreads();
+    const T inv = T(1) / (T(M) * T(M));
+    C<T>* jrow = a.J + (size_t)v * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int col = lane + 32 * k;
+      C<T> acc = czero<T>(), acc1 = czero<T>();
+      for (int w = 0; w < K; w += 2) {
+        acc = cadd<T>(acc, cmulc<T>(V[warp * K + w], twm[(vl_corner_freq<T>(w, mf, M) * col) & (M - 1)]));
+        acc1 = cadd<T>(acc1, cmulc<T>(V[warp * K + w + 1], twm[(vl_corner_freq<T>(w + 1, mf, M) * col) & (M - 1)]));
+      }
+      acc = cscale<T>(cadd<T>(acc, acc1), inv);
+      x[k] = acc;
+      jrow[col] = acc;
+    }
+  } else if constexpr (MODE == VIEW_BWD) {
+    const C<T>* g = a.gE + (size_t)v * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) x[k] = conj_<T>(g[lane + 32 * k]);
+  } else {
+    const C<T>* g = a.x + (size_t)v * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const C<T> t = g[lane + 32 * k];
+      x[k] = a.conj_in ? conj_<T>(t) : t;
+    }
+  }
+  warp_fft_fwd<T, E>(x, ltw, lane);
+#pragma unroll
+  for (int q = 0; q < E; ++q) tile[(q * 32 + lane) * TP + warp] = x[q];
+  __syncthreads();
+  pdl_trigger();
+  C<T>* out = a.spec + (size_t)vr * P * M + y0;
+  for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
+    const int pos = i / VL_ROWS, yl = i % VL_ROWS;
+    out[(size_t)pos * M + yl] = tile[pos * TP + yl];
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int E>
+__global__ void __launch_bounds__(256) vl_cols_kernel(VLArgs<T> a) {
+  constexpr int P = 32 * E, M = P / 2, KH = E / 2;
+  __shared__ C<T> tw[P];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  __syncthreads();
+  LaneTw<T, E> ltw;
+  ltw.load(tw, lane);
+  const int pos = blockIdx.x * (blockDim.x >> 5) + warp;
+  const C<T>* kh = a.khat + (size_t)pos * P;
+  pdl_wait();
+  C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
+  C<T> x[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) x[k] = k < KH ? col[lane + 32 * k] : czero<T>();
+  warp_fft_fwd<T, E>(x, ltw, lane);
+#pragma unroll
+  for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kh[q * 32 + lane]);
+  warp_fft_inv<T, E>(x, ltw, lane);
+  pdl_trigger();
+#pragma unroll
+  for (int k = 0; k < KH; ++k) col[lane + 32 * k] = x[k];
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int E, int MODE>
+__global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
+  constexpr int P = 32 * E, M = P / 2, KH = E / 2, SP = P + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int mf = a.mf, K = 2 * mf, M0 = K * K;
+  C<T>* tw = reinterpret_cast<C<T>*>(smem_raw);
+  C<T>* twm = tw + P;
+  C<T>* S = twm + M;                     // [VL_ROWS][SP]; reused as rows [VL_ROWS][M] (BWD)
+  C<T>* U = S + VL_ROWS * SP;            // [VL_ROWS][K]
+  double* red = reinterpret_cast<double*>(U + VL_ROWS * K);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int vr = blockIdx.y, v = a.v0 + vr, y0 = blockIdx.x * VL_ROWS, y = y0 + warp;
+  const int scene = v / a.n, view = v % a.n;
+  const size_t img = (size_t)M * M;
+  for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
+  pdl_wait();
+  const C<T>* in = a.spec + (size_t)vr * P * M + y0;
+  for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
+    const int pos = i / VL_ROWS, yl = i % VL_ROWS;
+    S[yl * SP + pos] = in[(size_t)pos * M + yl];
+  }
+  __syncthreads();
+  LaneTw<T, E> ltw;
+  ltw.load(tw, lane);
+  C<T> x[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) x[q] = S[warp * SP + q * 32 + lane];
+  warp_fft_inv<T, E>(x, ltw, lane);
+  pdl_trigger();
+  const size_t rowoff = (size_t)v * img + (size_t)y * M;
+  if constexpr (MODE == VIEW_FWD) {
+    double nrm = 0.0;
+    const C<T>* ei = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int col = lane + 32 * k;
+      const C<T> e = cadd<T>(ei[col], x[k]);
+      a.E[rowoff + col] = e;
+      nrm += (double)cabs2<T>(e);
+    }
+    const double tot = block_sum_d<T>(nrm, red);
+    if (tid == 0) a.norms[(size_t)v * a.NPV + blockIdx.x] = tot;
+  } else if constexpr (MODE == VIEW_BWD) {
+    __syncthreads();                     // S is reused as the g_J rows
+    C<T>* rows = S;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int col = lane + 32 * k;
+      rows[warp * M + col] = cadd<T>(a.gJloc[rowoff + col], conj_<T>(x[k]));
+    }
+    __syncthreads();
+    // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)   (spectral.py:56-65)
+    for (int i = tid; i < VL_ROWS * K; i += blockDim.x) {
+      const int yl = i / K, w = i % K;
+      const int f = vl_corner_freq<T>(w, mf, M);
+      C<T> acc = czero<T>(), acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
+      for (int xx = 0; xx < M; xx += 4) {
+        acc = cadd<T>(acc, cmul<T>(rows[yl * M + xx], twm[(f * xx) & (M - 1)]));
+        acc1 = cadd<T>(acc1, cmul<T>(rows[yl * M + xx + 1], twm[(f * (xx + 1)) & (M - 1)]));
+        acc2 = cadd<T>(acc2, cmul<T>(rows[yl * M + xx + 2], twm[(f * (xx + 2)) & (M - 1)]));
+        acc3 = cadd<T>(acc3, cmul<T>(rows[yl * M + xx + 3], twm[(f * (xx + 3)) & (M - 1)]));
+      }
+      U[i] = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
+    }
+    __syncthreads();
+    C<T>* gp = a.gpart + ((size_t)v * a.NPV + blockIdx.x) * M0;
+    for (int i = tid; i < M0; i += blockDim.x) {
+      const int u = i / K, w = i % K;
+      const int f = vl_corner_freq<T>(u, mf, M);
+      C<T> acc = czero<T>();
+      for (int yl = 0; yl < VL_ROWS; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], twm[(f * (y0 + yl)) & (M - 1)]));
+      gp[i] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int col = lane + 32 * k;
+      a.y[rowoff + col] = a.conj_out ? conj_<T>(x[k]) : x[k];
+    }
+  }
+}
+
+// g_alpha = sum of the truncation partials / (m1 m2), scattered into the
+// network's output-gradient rows; (view 0, block 0) of each scene finalises
+// the loss breakdown (losses.py:36-49)
+template <typename T>
+__global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
+  __shared__ double red[4][4];
+  const int M = a.M, mf = a.mf, K = 2 * mf, M0 = K * K;
+  const int v = blockIdx.y, scene = v / a.n, view = v % a.n;
+  pdl_wait();
+  if (a.do_fin && view == 0 && blockIdx.x == 0) finalize_block(a.fin, scene, red);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M0) return;
+  C<T> acc = czero<T>();
+  const C<T>* gp = a.gpart + (size_t)v * a.NPV * M0 + i;
+  for (int c = 0; c < a.NPV; ++c) acc = cadd<T>(acc, gp[(size_t)c * M0]);
+  acc = cscale<T>(acc, T(1) / (T(M) * T(M)));
+  const int u = i / K, w = i % K;
+  const int slot = vl_corner_slot(u, w, mf);
+  if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
+  if (a.gy) {
+    const int D0 = 2 * M0 * (a.joint ? a.n : 1);
+    const int rows = a.joint ? 1 : a.n;
+    const int re = a.joint ? view * M0 + slot : slot;
+    const int row = a.joint ? 0 : view;
+    T* gyrow = a.gy + ((size_t)scene * rows + row) * D0;
+    const T* co = a.cout + (size_t)scene * D0;
+    gyrow[re] = acc.x * co[re];
+    gyrow[re + D0 / 2] = acc.y * co[re + D0 / 2];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Data term D = J G_S^T - d as a split-K complex GEMM.
+template <typename T>
+struct DataArgs {
+  int n, R, npix, chunk, nchunks;
+  const C<T>* J;        // [S*n][npix]
+  const C<T>* gs;       // [R][npix]
+  C<T>* dpart;          // [S][nchunks][n][R]
+  const C<T>* data;     // [S][n][R]
+  const T* mask;
+  const double* c_sca;
+  C<T>* grows;
+  double* dloss;
+};
+
+constexpr int DG_KC = 32;          // pixels per staged sub-tile
+
+template <typename T>
+__host__ __device__ inline int dg_threads(int n, int R) {
+  const int t = ((n + 3) / 4) * ((R + 3) / 4);
+  return (t + 31) / 32 * 32;
+}
+template <typename T>
+__host__ __device__ inline size_t dg_smem(int n, int R) {
+  return (size_t)2 * (4 * ((n + 3) / 4) + 4 * ((R + 3) / 4)) * (DG_KC + 16 / sizeof(C<T>)) * sizeof(C<T>);
+}
+
+// CTA = (pixel chunk, scene).  Thread (ti, tr) owns views ti + NI*a and
+// receivers tr + NR*b (a, b < 4): strided ownership keeps the shared reads of
+// one warp on distinct banks.  Sub-tiles of DG_KC pixels are double-buffered
+// with cp.async.
+template <typename T>
+__global__ void __launch_bounds__(512) data_gemm_kernel(DataArgs<T> a) {
+  constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;   // complex per 16 B
+  constexpr int PT = DG_KC + EPC;                                         // padded pitch
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = a.n, R = a.R, NI = (n + 3) / 4, NR = (R + 3) / 4;
+  const int nr = 4 * NI, rr = 4 * NR;
+  C<T>* Js = reinterpret_cast<C<T>*>(smem_raw);   // 2 x [nr][PT]
+  C<T>* Gs = Js + 2 * nr * PT;                     // 2 x [rr][PT]
+  const int tid = threadIdx.x, scene = blockIdx.y, chunk = blockIdx.x;
+  const int ti = tid / NR, tr = tid % NR;
+  const bool active = ti < NI;
+  const int p0 = chunk * a.chunk, p1 = min(a.npix, p0 + a.chunk);
+  const C<T>* Jb = a.J + (size_t)scene * n * a.npix;
+  constexpr int SEG = DG_KC / EPC;
+  auto stage = [&](int k0, int s) {
+    C<T>* js = Js + s * nr * PT;
+    C<T>* gsm = Gs + s * rr * PT;
+    for (int i = tid; i < (nr + rr) * SEG; i += blockDim.x) {
+      const int row = i / SEG, sg = i % SEG, p = k0 + sg * EPC;
+      if (row < nr) {
+        const bool ok = row < n && p < p1;
+        cp_async16(js + row * PT + sg * EPC, ok ? Jb + (size_t)row * a.npix + p : Jb, ok);
+      } else {
+        const int r = row - nr;
+        const bool ok = r < R && p < p1;
+        cp_async16(gsm + r * PT + sg * EPC, ok ? a.gs + (size_t)r * a.npix + p : a.gs, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  C<T> acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = czero<T>();
+  pdl_wait();
+  stage(p0, 0);
+  int s = 0;
+  for (int k0 = p0; k0 < p1; k0 += DG_KC, s ^= 1) {
+    if (k0 + DG_KC < p1) {
+      stage(k0 + DG_KC, s ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (active) {
+      const C<T>* js = Js + s * nr * PT;
+      const C<T>* gsm = Gs + s * rr * PT;
+#pragma unroll 4
+      for (int kk = 0; kk < DG_KC; ++kk) {
+        C<T> jv[4], gv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) jv[i] = js[(ti + NI * i) * PT + kk];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gv[j] = gsm[(tr + NR * j) * PT + kk];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[i][j].x = fma(jv[i].x, gv[j].x, acc[i][j].x);
+            acc[i][j].x = fma(-jv[i].y, gv[j].y, acc[i][j].x);
+            acc[i][j].y = fma(jv[i].x, gv[j].y, acc[i][j].y);
+            acc[i][j].y = fma(jv[i].y, gv[j].x, acc[i][j].y);
+          }
+      }
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+  if (!active) return;
+  C<T>* dp = a.dpart + ((size_t)scene * a.nchunks + chunk) * n * R;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int vi = ti + NI * i, r = tr + NR * j;
+      if (vi < n && r < R) dp[vi * R + r] = acc[i][j];
+    }
+}
+
+// D = sum of chunk partials - d (masked), g_rows = 2 D mask / c_sca, ||D||^2 per view
+template <typename T>
+__global__ void __launch_bounds__(128) data_reduce_kernel(DataArgs<T> a) {
+  __shared__ double red[4];
+  const int v = blockIdx.x, scene = v / a.n, i = v % a.n, R = a.R;
+  pdl_wait();
+  double part = 0.0;
+  const double csca = a.c_sca[scene];
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    C<T> acc = czero<T>();
+    const C<T>* dp = a.dpart + ((size_t)scene * a.nchunks * a.n + i) * R + r;
+    for (int c = 0; c < a.nchunks; ++c) acc = cadd<T>(acc, dp[(size_t)c * a.n * R]);
+    const size_t di = (size_t)v * R + r;
+    C<T> d = csub<T>(acc, a.data[di]);
+    const T mk_ = a.mask ? a.mask[di] : T(1);
+    d = cscale<T>(d, mk_);
+    part += (double)cabs2<T>(d);
+    a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
+  }
+  pdl_trigger();
+  part = warp_sum<double>(part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    a.dloss[v] = s;
+  }
+}
+
+}  // namespace pdf

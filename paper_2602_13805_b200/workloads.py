@@ -34,8 +34,11 @@ def baseline_config(i: int, k_iters: int | None = None) -> ImagingConfig:
         c = ImagingConfig(m1=64, m2=64, n_tx=36, n_rx=36, m_f=8, k_iters=500, rng_seed=2, **base)
     elif i == 4:
         c = ImagingConfig(m1=64, m2=64, n_tx=16, n_rx=32, m_f=8, k_iters=500, rng_seed=0, **base)
+    elif i == 5:
+        c = ImagingConfig(frequency=C0, doi_side=4.0, ring_radius=5.0, m1=256, m2=256, n_tx=72, n_rx=72, m_f=16,
+                          k_iters=300, rng_seed=3)
     else:
-        raise ValueError(f"config {i} not supported on one B200 path yet")
+        raise ValueError(f"no BASELINE config {i}")
     if k_iters is not None:
         from dataclasses import replace
         c = replace(c, k_iters=k_iters)
@@ -63,6 +66,26 @@ def cfg4_scene(idx: int) -> tuple[Scene, np.random.Generator]:
     return Scene(tuple(shapes)), rng
 
 
+def cfg5_scene(seed: int = 3) -> tuple[Scene, np.random.Generator]:
+    """BASELINE config 5: 6 non-overlapping random ellipses on [-2, 2], semi-axes
+    U[0.2, 0.6], chi = U[0.5, 2.5] + i U[0, 0.5]; rng = default_rng(3), which
+    then also draws the AWGN (same draw order as tests/golden/make_golden.py)."""
+    rng = np.random.default_rng(seed)
+    shapes, placed, tries = [], [], 0
+    while len(shapes) < 6 and tries < 1000:
+        tries += 1
+        a, b = rng.uniform(0.2, 0.6, 2)
+        r = max(a, b)
+        cx, cy = rng.uniform(-2.0 + r, 2.0 - r, 2)
+        ang = rng.uniform(0.0, np.pi)
+        if any(math.hypot(cx - px, cy - py) < r + pr for px, py, pr in placed):
+            continue
+        chi = rng.uniform(0.5, 2.5) + 1j * rng.uniform(0.0, 0.5)
+        placed.append((cx, cy, r))
+        shapes.append(ellipse((cx, cy), a, b, ang, 1.0 + chi))
+    return Scene(tuple(shapes)), rng
+
+
 def baseline_scene(i: int, idx: int = 0) -> tuple[Scene, np.random.Generator, float]:
     """(scene, noise rng, snr_db) of BASELINE config i (scene idx for config 4)."""
     if i == 1:
@@ -75,6 +98,9 @@ def baseline_scene(i: int, idx: int = 0) -> tuple[Scene, np.random.Generator, fl
                       Shape(kind="disk", eps_r=2.5, center=(0.6, 0.6), radius=0.15))), np.random.default_rng(2), SNR_10PCT
     if i == 4:
         s, rng = cfg4_scene(idx)
+        return s, rng, SNR_5PCT
+    if i == 5:
+        s, rng = cfg5_scene(3)
         return s, rng, SNR_5PCT
     raise ValueError(i)
 

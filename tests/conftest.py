@@ -56,7 +56,7 @@ def cfg_tiny():
 
 
 def cfg_baseline(i: int):
-    """BASELINE.json configs 1-4 (SURVEY 8(d) mapping: m_f 5/8/8/8, lambda = 1 m)."""
+    """BASELINE.json configs 1-5 (SURVEY 8(d) mapping: m_f 5/8/8/8, lambda = 1 m)."""
     from paper_2602_13805_b200.config import C0, ImagingConfig
     if i == 1:
         return ImagingConfig(frequency=C0, doi_side=2.0, m1=32, m2=32, n_tx=16, n_rx=32, ring_radius=3.0,
@@ -67,6 +67,9 @@ def cfg_baseline(i: int):
     if i == 3:
         return ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=36, n_rx=36, ring_radius=3.0,
                              m_f=8, k_iters=500, rng_seed=2).validate()
+    if i == 5:
+        return ImagingConfig(frequency=C0, doi_side=4.0, m1=256, m2=256, n_tx=72, n_rx=72, ring_radius=5.0,
+                             m_f=16, k_iters=300, rng_seed=3).validate()
     raise ValueError(i)
 
 

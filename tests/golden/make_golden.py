@@ -71,6 +71,24 @@ def cfg4_scene(idx: int):
     return Scene(tuple(shapes)), rng
 
 
+def cfg5_scene(seed: int = 3):
+    """6 non-overlapping ellipses on [-2,2], semi-axes U[0.2,0.6], chi = U[0.5,2.5] + i U[0,0.5] (BASELINE cfg5)."""
+    rng = np.random.default_rng(seed)
+    shapes, placed, tries = [], [], 0
+    while len(shapes) < 6 and tries < 1000:
+        tries += 1
+        a, b = rng.uniform(0.2, 0.6, 2)
+        r = max(a, b)
+        cx, cy = rng.uniform(-2.0 + r, 2.0 - r, 2)
+        ang = rng.uniform(0.0, np.pi)
+        if any(np.hypot(cx - px, cy - py) < r + pr for px, py, pr in placed):
+            continue
+        chi = rng.uniform(0.5, 2.5) + 1j * rng.uniform(0.0, 0.5)
+        placed.append((cx, cy, r))
+        shapes.append(ellipse_poly(cx, cy, a, b, ang, 1.0 + chi))
+    return Scene(tuple(shapes)), rng
+
+
 def plane_problem(cfg, scene, snr_db, rng):
     grid, arr = build_grid(cfg), build_array(cfg)
     ops = build_greens(cfg, arr, grid)
@@ -227,6 +245,39 @@ def make_cfg4(n_scenes=2, k=500):
         save(f"cfg4_s{idx}", data=data.matrix, chi_true=chi.values, alpha0=out["alpha0"], trace=out["trace"],
              final=out["final"], chi_cco=out["chi_cco"], rel_error=np.array(out["rel_error"]))
         print(f"cfg4 scene {idx}: rel_error {out['rel_error']:.6f}", flush=True)
+
+
+def make_cfg5(k=300):
+    """BASELINE cfg5: one large scene, 256x256 on [-2,2], 72 tx / 72 rx at 5 lambda, m_f=16, 300 iterations."""
+    cfg = ImagingConfig(frequency=C0, doi_side=4.0, m1=256, m2=256, n_tx=72, n_rx=72, ring_radius=5.0, m_f=16,
+                        k_iters=k, rng_seed=3).validate()
+    scene, rng = cfg5_scene(3)
+    t0 = time.time()
+    grid, arr, ops, views, chi, data = plane_problem(cfg, scene, 20 * np.log10(100 / 5), rng)
+    print(f"cfg5 data ({time.time() - t0:.0f}s)", flush=True)
+    basis = SpectralBasis(cfg.m1, cfg.m2, cfg.m_f)
+    fs = FieldSet(views, "incident")
+    chi0, r0 = bp_initialize(data, fs, ops, cfg.beta)
+    alpha0 = init_alpha(r0, data, fs, ops, basis, cfg.beta)
+    ctx = LossContext(data=data, e_inc=views, ops=ops, basis=basis, beta=cfg.beta,
+                      lambdas=(cfg.lambda1, cfg.lambda2, cfg.lambda3), tau_b=cfg.tau_b)
+    g0, bd0 = grad_alpha(alpha0, ctx)
+    net = network.init_network(basis.m0, np.random.default_rng(cfg.rng_seed))
+    flat = network.flatten_params(net)
+    flat = flat + 0.02 * np.random.default_rng(123).standard_normal(flat.size)
+    gflat, bdn = network.grad_loss(network.unflatten_params(flat, net), alpha0, ctx)
+    idx = np.sort(np.random.default_rng(5).choice(flat.size, size=4096, replace=False))
+    common = dict(data=data.matrix, chi_true=chi.values, chi0=chi0, alpha0=alpha0, g_alpha0=g0,
+                  bd0=np.array(bd0.as_row()), grad_idx=idx, grad_sub=gflat[idx],
+                  grad_norms=np.array([np.linalg.norm(gflat), np.abs(gflat).max()]), bd_net=np.array(bdn.as_row()),
+                  einc_checksum=np.array([views.sum(), np.abs(views).sum()]),
+                  gs_checksum=np.array([ops.gs_matrix.sum(), np.abs(ops.gs_matrix).sum()]),
+                  khat_checksum=np.array([ops.gd_kernel_hat.sum(), np.abs(ops.gd_kernel_hat).sum()]))
+    save("cfg5", **common)
+    print(f"cfg5 single-step part ({time.time() - t0:.0f}s)", flush=True)
+    out = composed_reconstruct(cfg, data, views, ops, chi, k)
+    save("cfg5", trace=out["trace"], final=out["final"], rel_error=np.array(out["rel_error"]), **common)
+    print(f"cfg5: rel_error {out['rel_error']:.6f}  ({time.time() - t0:.1f}s)", flush=True)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,121 @@
+"""Large-grid view path (pdf_view_large.cuh): BASELINE config 5 (256 x 256,
+72 incidences / receivers, m_f = 16) against golden vectors from the
+unmodified reference, and the multi-pass path forced onto the small configs
+(PDF_VIEW_LARGE=1) against the same goldens the cluster path meets."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import Setup, cfg_baseline, golden, rel
+
+pytestmark = pytest.mark.gpu
+LAM = (1e-3, 1e-5, 1e-5)
+
+
+@pytest.fixture
+def force_large(monkeypatch):
+    monkeypatch.setenv("PDF_VIEW_LARGE", "1")
+
+
+def _dev(st, data, **kw):
+    from paper_2602_13805_b200.engine import DeviceProblem
+    c = st.cfg
+    return DeviceProblem(st.ops, st.e_inc, data, mf=c.m_f, beta=c.beta, lambdas=LAM, tau_b=c.tau_b, **kw)
+
+
+def _single_step_checks(st, g, tol=1e-10):
+    from oracle import pdf_oracle as O
+    dev = _dev(st, g["data"])
+    ga, bd = dev.loss_grad(torch.as_tensor(g["alpha0"][None], device="cuda"))
+    dev.check_errors()
+    assert rel(ga[0].cpu().numpy(), g["g_alpha0"]) < tol
+    np.testing.assert_allclose(bd[0].cpu().numpy(), g["bd0"], rtol=tol)
+    dev.net_setup(torch.as_tensor(g["alpha0"][None], device="cuda"))
+    flat = O.flat(O.init_net(g["alpha0"].shape[1], np.random.default_rng(st.cfg.rng_seed)))
+    flat = flat + 0.02 * np.random.default_rng(123).standard_normal(flat.size)
+    grad, bdn = dev.grad_loss(torch.as_tensor(flat[None], device="cuda").contiguous())
+    dev.check_errors()
+    gr = grad[0].cpu().numpy()
+    assert rel(gr[g["grad_idx"]], g["grad_sub"]) < tol
+    np.testing.assert_allclose(bdn[0].cpu().numpy(), g["bd_net"], rtol=tol)
+    return dev
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_forced_large_path_single_step(force_large, cfg_id):
+    g = golden(f"cfg{cfg_id}")
+    st = Setup(cfg_baseline(cfg_id), plane=True)
+    _single_step_checks(st, g)
+
+
+def test_forced_large_path_apply_gd_matches_cluster_path(monkeypatch):
+    st = Setup(cfg_baseline(2), plane=True)
+    g = golden("cfg2")
+    rng = np.random.default_rng(4)
+    x = torch.as_tensor(rng.standard_normal((5, 64, 64)) + 1j * rng.standard_normal((5, 64, 64)), device="cuda")
+    small = _dev(st, g["data"])
+    y0, y1 = small.apply_gd(x), small.apply_gd(x, adjoint=True)
+    monkeypatch.setenv("PDF_VIEW_LARGE", "1")
+    large = _dev(st, g["data"])
+    z0, z1 = large.apply_gd(x), large.apply_gd(x, adjoint=True)
+    assert rel(z0.cpu().numpy(), y0.cpu().numpy()) < 1e-13
+    assert rel(z1.cpu().numpy(), y1.cpu().numpy()) < 1e-13
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    g = golden("cfg5")
+    st = Setup(cfg_baseline(5), plane=True)
+    return st, g
+
+
+def test_cfg5_operators_match_reference(cfg5):
+    st, g = cfg5
+    np.testing.assert_allclose([st.ops.gd_kernel_hat.sum(), np.abs(st.ops.gd_kernel_hat).sum()], g["khat_checksum"],
+                               rtol=1e-12)
+    np.testing.assert_allclose([st.ops.gs_matrix.sum(), np.abs(st.ops.gs_matrix).sum()], g["gs_checksum"], rtol=1e-12)
+    np.testing.assert_allclose([st.e_inc.sum(), np.abs(st.e_inc).sum()], g["einc_checksum"], rtol=1e-12)
+
+
+def test_cfg5_single_step(cfg5):
+    """one PDF step at 256 x 256 / 72 views: g_alpha, breakdown, flat network gradient (33.6 M params)"""
+    st, g = cfg5
+    _single_step_checks(st, g)
+
+
+def test_cfg5_initialisation(cfg5):
+    st, g = cfg5
+    dev = _dev(st, g["data"])
+    chi0, r0 = dev.bp_initialize()
+    assert rel(chi0[0].cpu().numpy(), g["chi0"]) < 1e-10
+    a0 = dev.init_alpha(r0)
+    assert rel(a0[0].cpu().numpy(), g["alpha0"]) < 1e-10
+
+
+@pytest.mark.parametrize("n", [50, 72, 80])
+def test_network_many_rows_matches_oracle(tiny_setup, n):
+    """64-80 network rows (config 5 has 72 incidences) through the 128-thread
+    backward layout, against the oracle on a small synthetic problem."""
+    from oracle import pdf_oracle as O
+    from conftest import oracle_ops
+    from paper_2602_13805_b200.engine import DeviceProblem
+    rng = np.random.default_rng(n)
+    m, R = 16, tiny_setup.ops.gs_matrix.shape[0]
+    phi = 2 * np.pi * np.arange(n) / n
+    xy = np.linspace(-0.7, 0.7, m)
+    e_inc = np.exp(1j * 2 * np.pi * (np.cos(phi)[:, None, None] * xy[None, None, :]
+                                     + np.sin(phi)[:, None, None] * xy[None, :, None]))
+    data = 0.3 * (rng.standard_normal((n, R)) + 1j * rng.standard_normal((n, R)))
+    alpha0 = 0.05 * (rng.standard_normal((n, 36)) + 1j * rng.standard_normal((n, 36)))
+    params = O.init_net(36, np.random.default_rng(1))
+    flat = O.flat(params) + 0.02 * rng.standard_normal(O.flat(params).size)
+    ctx = O.Context(data, e_inc, oracle_ops(tiny_setup), 3, 6.0, LAM, 0.5)
+    want, parts = O.grad_loss(O.unflat(flat, params), alpha0, ctx)
+    dev = DeviceProblem(tiny_setup.ops, e_inc, data, mf=3, beta=6.0, lambdas=LAM, tau_b=0.5)
+    dev.net_setup(torch.as_tensor(alpha0[None], device="cuda"))
+    grad, bd = dev.grad_loss(torch.as_tensor(flat[None], device="cuda").contiguous())
+    dev.check_errors()
+    assert rel(grad[0].cpu().numpy(), want) < 1e-10
+    assert abs(bd[0, 5].item() - parts["total"]) < 1e-10 * abs(parts["total"])

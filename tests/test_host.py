@@ -97,6 +97,14 @@ def test_cfg4_random_ellipse_scenes_match_reference():
         assert np.array_equal(rasterize(scene, grid).values, g["chi_true"])
 
 
+def test_cfg5_scene_matches_reference():
+    from paper_2602_13805_b200 import build_grid, rasterize
+    from paper_2602_13805_b200.workloads import baseline_config, baseline_scene
+    g = golden("cfg5")
+    chi = rasterize(baseline_scene(5)[0], build_grid(baseline_config(5))).values
+    assert np.array_equal(chi, g["chi_true"])
+
+
 def test_host_simulate_matches_reference_data(g_tiny):
     from paper_2602_13805_b200 import builtin_scene, simulate
     sim = simulate(cfg_tiny(), builtin_scene("austria", 2.0, scale=0.9))
