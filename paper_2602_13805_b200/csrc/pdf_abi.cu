@@ -12,6 +12,7 @@
 #include "pdf_aux.cuh"
 #include "pdf_common.cuh"
 #include "pdf_net.cuh"
+#include "pdf_net_mma.cuh"
 #include "pdf_pixel.cuh"
 #include "pdf_shard.cuh"
 #include "pdf_view.cuh"
@@ -62,7 +63,7 @@ struct pdf_ctx {
   int M, P, E, K, M0, CS, rows, D0, H, RB, TX, ntiles;
   // large-grid view path (pdf_view_large.cuh): partials per view, views per
   // spectrum chunk, data-GEMM pixel chunking
-  int large, NPV, chunk, dg_chunk, dg_nchunks;
+  int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks;
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
@@ -109,10 +110,10 @@ static void plan(pdf_ctx* c, Ws& w) {
   if (c->large) {
     c->spec = w.take<C<T>>((size_t)c->chunk * c->P * c->M);
     c->gpart = w.take<C<T>>(SN * c->NPV * c->M0);
-    c->dpart = w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R);
   } else {
-    c->spec = c->gpart = c->dpart = nullptr;
+    c->spec = c->gpart = nullptr;
   }
+  c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
   c->dloss = w.take<double>(SN);
   c->part = w.take<double>((size_t)d.S * c->ntiles * 4);
   c->bd = w.take<double>((size_t)d.S * 6);
@@ -138,7 +139,10 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   c->E = c->P / 32;
   c->K = 2 * d->mf;
   c->M0 = c->K * c->K;
-  c->CS = env_int("PDF_VIEW_CLUSTER", 8);
+  // 8-CTA clusters while one wave holds every view (latency), 4 once the batch
+  // fills the GPU (half the cluster barriers per unit of work; measured -22%
+  // view time at 128 scenes)
+  c->CS = env_int("PDF_VIEW_CLUSTER", (long long)d->S * d->n * 8 <= 4 * 148 ? 8 : 4);
   if (c->CS < 1 || c->CS > 16 || (M % c->CS) || ((2 * M) % c->CS)) return fail(PDF_EINVAL, "view cluster size");
   c->rows = d->joint ? 1 : d->n;
   c->D0 = 2 * c->M0 * (d->joint ? d->n : 1);
@@ -159,12 +163,17 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
     const long long per = (long long)2 * M * M * csz;
     long long ch = std::max(1LL, budget / per);
     c->chunk = (int)std::min<long long>(ch, (long long)d->S * d->n);
+  }
+  // data term as a split-K GEMM (always on the large-grid path; PDF_DATA_GEMM=1
+  // selects it for the cluster path too)
+  c->dgemm = c->large || (env_int("PDF_DATA_GEMM", 0) && M >= 32);
+  if (c->dgemm) {
     const int npix = M * M;
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
     want = std::min(want, npix / DG_KC);
     c->dg_chunk = ((npix + want - 1) / want + DG_KC - 1) / DG_KC * DG_KC;
     c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
-    if (d->n > 80 || d->R > 80) return fail(PDF_EINVAL, "at most 80 incidences / receivers on the large-grid path");
+    if (d->n > 80 || d->R > 80) return fail(PDF_EINVAL, "at most 80 incidences / receivers for the data GEMM");
   }
   c->rsz = d->dtype == PDF_F64 ? 8 : 4;
   c->csz = 2 * c->rsz;
@@ -305,12 +314,7 @@ static int vl_conv(pdf_ctx* c, VLArgs<T>& a, int count, cudaStream_t st) {
 }
 
 template <typename T>
-static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
-  VLArgs<T> a = vl_common<T>(c);
-  a.alpha = (const C<T>*)alpha_hat; a.J = (C<T>*)c->J;
-  a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
-  a.E = (C<T>*)c->E_; a.norms = c->norms;
-  TRY((vl_conv<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
+static int data_term(pdf_ctx* c, cudaStream_t st) {
   DataArgs<T> g = {};
   g.n = c->d.n; g.R = c->d.R; g.npix = c->M * c->M; g.chunk = c->dg_chunk; g.nchunks = c->dg_nchunks;
   g.J = (const C<T>*)c->J; g.gs = (const C<T>*)c->d.gs_matrix; g.dpart = (C<T>*)c->dpart;
@@ -322,6 +326,16 @@ static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   if (e == cudaSuccess) e = plain_launch(data_reduce_kernel<T>, dim3(c->d.S * c->d.n), dim3(128), 0, st, args);
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("data term: ") + cudaGetErrorString(e));
   return PDF_OK;
+}
+
+template <typename T>
+static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
+  VLArgs<T> a = vl_common<T>(c);
+  a.alpha = (const C<T>*)alpha_hat; a.J = (C<T>*)c->J;
+  a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
+  a.E = (C<T>*)c->E_; a.norms = c->norms;
+  TRY((vl_conv<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
+  return data_term<T>(c, st);
 }
 
 template <typename T>
@@ -346,8 +360,9 @@ static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
   a.gs = (const C<T>*)c->d.gs_matrix; a.data = (const C<T>*)c->d.data; a.mask = (const T*)c->d.mask;
   a.c_sca = c->c_sca; a.J = (C<T>*)c->J; a.E = (C<T>*)c->E_; a.norms = c->norms;
-  a.grows = (C<T>*)c->grows; a.dloss = c->dloss;
-  return launch_view<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st);
+  a.grows = (C<T>*)c->grows; a.dloss = c->dloss; a.do_data = !c->dgemm;
+  TRY((launch_view<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
+  return c->dgemm ? data_term<T>(c, st) : PDF_OK;
 }
 
 template <typename T, bool GRAD>
@@ -409,6 +424,55 @@ static int net_split(long long base_ctas, int max_split) {
   return c;
 }
 
+// DMMA forward layer (float64): MT m-tiles of 8 rows, NT n-tiles of 8 per warp
+template <int MT, int NT>
+static cudaError_t fwd_mma_launch(dim3 grid, int CK, NetFwdArgs<double>& a, cudaStream_t st) {
+  const size_t smem = fwd_mma_smem_bytes(MT, NT);
+  auto k = net_fwd_mma_kernel<MT, NT>;
+  cudaError_t e = prep(k, smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&a};
+  return launch_cluster(k, grid, dim3(256), smem, st, dim3(1, CK, 1), args);
+}
+
+template <int MT>
+static cudaError_t fwd_mma_nt(int NT, dim3 grid, int CK, NetFwdArgs<double>& a, cudaStream_t st) {
+  if constexpr (MT <= 4) { if (NT == 4) return fwd_mma_launch<MT, 4>(grid, CK, a, st); }
+  if constexpr (MT <= 8) { if (NT == 2) return fwd_mma_launch<MT, 2>(grid, CK, a, st); }
+  return fwd_mma_launch<MT, 1>(grid, CK, a, st);
+}
+
+static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
+  const int MT = (c->rows + 7) / 8, S = c->d.S, N = a.N, K = a.K;
+  auto ctas = [&](int nt) { return (long long)((N + 64 * nt - 1) / (64 * nt)) * S; };
+  int NT = 1;
+  if (MT <= 4 && ctas(4) >= 2 * 148) NT = 4;
+  else if (MT <= 8 && ctas(2) >= 148) NT = 2;
+  static const int cap = env_int("PDF_FWD_CLUSTER", 8);
+  const long long base = ctas(NT);
+  const int kmax = (K + FM_KCH - 1) / FM_KCH;
+  int CK = 1;
+  while (CK < cap && 2 * CK <= kmax && base * CK < 2 * 148) CK *= 2;
+  a.ks = ((K + CK - 1) / CK + FM_KCH - 1) / FM_KCH * FM_KCH;
+  const dim3 grid((N + 64 * NT - 1) / (64 * NT), CK, S);
+  cudaError_t e;
+  switch (MT) {
+    case 1: e = fwd_mma_nt<1>(NT, grid, CK, a, st); break;
+    case 2: e = fwd_mma_nt<2>(NT, grid, CK, a, st); break;
+    case 3: e = fwd_mma_nt<3>(NT, grid, CK, a, st); break;
+    case 4: e = fwd_mma_nt<4>(NT, grid, CK, a, st); break;
+    case 5: e = fwd_mma_nt<5>(NT, grid, CK, a, st); break;
+    case 6: e = fwd_mma_nt<6>(NT, grid, CK, a, st); break;
+    case 7: e = fwd_mma_nt<7>(NT, grid, CK, a, st); break;
+    case 8: e = fwd_mma_nt<8>(NT, grid, CK, a, st); break;
+    case 9: e = fwd_mma_nt<9>(NT, grid, CK, a, st); break;
+    case 10: e = fwd_mma_nt<10>(NT, grid, CK, a, st); break;
+    default: return fail(PDF_EINVAL, "rows");
+  }
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net fwd (dmma): ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
 template <typename T>
 static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, long long woff, long long boff,
                          T* out, int final_layer, int* step, cudaStream_t st) {
@@ -421,6 +485,10 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
   a.n = c->d.n; a.M0 = c->M0; a.joint = c->d.joint; a.step = step;
   a.w_early = woff != 0;   // W2, W3 were last written >= 2 launches earlier; W1 by the launch right before
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
+  static const int use_mma = env_int("PDF_NET_MMA", 1);
+  if constexpr (sizeof(T) == 8) {
+    if (use_mma) return fwd_mma_layer(c, a, st);
+  }
   // one output row per warp while a single scene cannot fill the GPU, two otherwise
   const int opw = (c->RB == 1 && (c->d.S * N) / (NET_THREADS / 32) >= 2 * 148 * 4) ? 2 : 1;
   const int kch = c->RB <= 2 ? FwdShape<T, 1>::KCH : FwdShape<T, 3>::KCH;
@@ -448,6 +516,63 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
   return PDF_OK;
 }
 
+// DMMA backward layer (float64)
+template <int MT, int KT>
+static cudaError_t bwd_mma_launch(bool fused, dim3 grid, int CN, NetBwdArgs<double>& a, cudaStream_t st) {
+  const size_t smem = bwd_mma_smem_bytes(MT, KT);
+  void* args[] = {&a};
+  cudaError_t e;
+  if (fused) {
+    auto k = net_bwd_mma_kernel<MT, KT, true>;
+    e = prep(k, smem);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(BM_WARPS * 32), smem, st, dim3(1, CN, 1), args);
+  } else {
+    auto k = net_bwd_mma_kernel<MT, KT, false>;
+    e = prep(k, smem);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(BM_WARPS * 32), smem, st, dim3(1, CN, 1), args);
+  }
+  return e;
+}
+
+template <int MT>
+static cudaError_t bwd_mma_kt(int KT, bool fused, dim3 grid, int CN, NetBwdArgs<double>& a, cudaStream_t st) {
+  if constexpr (MT <= 4) { if (KT == 2) return bwd_mma_launch<MT, 2>(fused, grid, CN, a, st); }
+  return bwd_mma_launch<MT, 1>(fused, grid, CN, a, st);
+}
+
+static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStream_t st) {
+  const int MT = (c->rows + 7) / 8, S = c->d.S, N = a.N, K = a.K;
+  // two k-tiles per warp (128-byte W row segments) when the batch fills the GPU
+  static const int kt_env = env_int("PDF_BWD_KT", 0);
+  int KT = 1;
+  if (MT <= 4 && (long long)((K + 63) / 64) * S >= 2 * 148) KT = 2;
+  if (kt_env == 1 || (kt_env == 2 && MT <= 4)) KT = kt_env;
+  const int CW = BM_WARPS * 8 * KT;
+  static const int cap = env_int("PDF_BWD_CLUSTER", 16);
+  const long long base = (long long)((K + CW - 1) / CW) * S;
+  const int nmax = (N + BM_NCH - 1) / BM_NCH;
+  int CN = 1;
+  while (CN < cap && 2 * CN <= nmax && base * CN < 3 * 148) CN *= 2;
+  a.ns = ((N + CN - 1) / CN + BM_NCH - 1) / BM_NCH * BM_NCH;
+  const dim3 grid((K + CW - 1) / CW, CN, S);
+  cudaError_t e;
+  switch (MT) {
+    case 1: e = bwd_mma_kt<1>(KT, fused, grid, CN, a, st); break;
+    case 2: e = bwd_mma_kt<2>(KT, fused, grid, CN, a, st); break;
+    case 3: e = bwd_mma_kt<3>(KT, fused, grid, CN, a, st); break;
+    case 4: e = bwd_mma_kt<4>(KT, fused, grid, CN, a, st); break;
+    case 5: e = bwd_mma_kt<5>(KT, fused, grid, CN, a, st); break;
+    case 6: e = bwd_mma_kt<6>(KT, fused, grid, CN, a, st); break;
+    case 7: e = bwd_mma_kt<7>(KT, fused, grid, CN, a, st); break;
+    case 8: e = bwd_mma_kt<8>(KT, fused, grid, CN, a, st); break;
+    case 9: e = bwd_mma_kt<9>(KT, fused, grid, CN, a, st); break;
+    case 10: e = bwd_mma_kt<10>(KT, fused, grid, CN, a, st); break;
+    default: return fail(PDF_EINVAL, "rows");
+  }
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net bwd (dmma): ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
 template <typename T>
 static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T* theta, long long woff,
                          long long boff, T* m, T* v, T* grad, int fused, T* gzprev, cudaStream_t st) {
@@ -460,6 +585,10 @@ static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T*
   a.lr = (T)c->d.lr; a.b1 = (T)c->d.adam_b1; a.b2 = (T)c->d.adam_b2; a.eps = (T)c->d.adam_eps;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
+  static const int use_mma = env_int("PDF_NET_MMA", 1);
+  if constexpr (sizeof(T) == 8) {
+    if (use_mma) return bwd_mma_layer(c, a, fused != 0, st);
+  }
   const int cols = c->RB >= 4 ? BwdShape<T, 4>::COLS : BwdShape<T, 1>::COLS;
   const int nch = c->RB >= 4 ? BwdShape<T, 4>::NCH : BwdShape<T, 1>::NCH;
   const int thr = c->RB >= 4 ? BwdShape<T, 4>::THR : BwdShape<T, 1>::THR;

@@ -1,0 +1,391 @@
+// Network layers on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).
+//
+// Measured on the B200 (tools/dmma_bench.cu): DMMA reaches 34-37 TFLOP/s
+// with 4-32 warps per SM, the same ceiling as scalar DFMA but at 1/8 of the
+// issue slots and with operands reused inside the tensor core -- the scalar
+// kernels of pdf_net.cuh were bound by shared-memory loads and issue (one LDS
+// per FMA), not by the FP64 pipe.
+//
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64; g = lane >> 2, t = lane & 3):
+//   A (8 x 4, row)  : lane holds A[g][t]
+//   B (4 x 8, col)  : lane holds B[t][g]
+//   C/D (8 x 8)     : lane holds D[g][2t], D[g][2t+1]
+// The k index of a 4-wide MMA step is free to permute as long as A and B
+// agree: a block of 16 k is issued as 4 steps s where lane position t stands
+// for k = 4t + s, so every lane reads 32 contiguous bytes of a W row (four
+// lanes of a group cover a 128-byte line).
+#pragma once
+#include "pdf_common.cuh"
+#include "pdf_net.cuh"
+
+namespace pdf {
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int FM_KCH = 64;              // k per staged input chunk
+constexpr int FM_XP = FM_KCH + 2;       // pitch: conflict-free 16-byte fragment reads
+constexpr int FM_WARPS = 8;
+
+__host__ __device__ constexpr size_t fwd_mma_smem_bytes(int MT, int NT) {
+  const size_t xs = (size_t)2 * 8 * MT * FM_XP;
+  const size_t part = (size_t)FM_WARPS * NT * 8 * 8 * MT;
+  return (xs > part ? xs : part) * sizeof(double);
+}
+
+// z[r][n] = sum_k x[r][k] W[n][k] + b[n] for one layer (network.py:107-120).
+// CTA = 8 warps x NT n-tiles of 8 outputs, all rows (MT m-tiles of 8), the
+// K range [rank*ks, ...) of its cluster rank; partial sums meet in DSMEM and
+// are added in rank order.
+template <int MT, int NT>
+__global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) {
+  constexpr int RPM = 8 * MT, SEG = FM_KCH / 2;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Xs = reinterpret_cast<double*>(smem_raw);   // 2 x [RPM][FM_XP]
+  double* part = Xs;                                   // after the k loop: [8*NT*8][RPM]
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CK = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int scene = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int K = a.K, N = a.N, rows = a.rows;
+  const int nw0 = (blockIdx.x * FM_WARPS + warp) * NT * 8;
+  const int kb = rank * a.ks, ke = min(K, kb + a.ks);
+  const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  const double* __restrict__ X = a.in + scene * a.in_ss;
+  const double* wr[NT];
+  bool nok[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const int n = nw0 + 8 * j + g;
+    nok[j] = n < N;
+    wr[j] = W + (size_t)(nok[j] ? n : 0) * K;
+  }
+  auto stage = [&](int k0, int s) {
+    double* dst = Xs + s * RPM * FM_XP;
+    for (int i = tid; i < RPM * SEG; i += 256) {
+      const int r = i / SEG, sg = i % SEG, gk = k0 + 2 * sg;
+      const bool ok = r < rows && gk < ke;
+      cp_async16(dst + r * FM_XP + 2 * sg, ok ? X + (size_t)r * K + gk : X, ok);
+    }
+    cp_async_commit();
+  };
+  auto loadB = [&](int k, double (&b)[NT][4]) {
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kk = k + 4 * t + 2 * h;      // even; K and ke are even
+        double2 v = make_double2(0.0, 0.0);
+        if (nok[j] && kk < ke) v = *reinterpret_cast<const double2*>(wr[j] + kk);
+        b[j][2 * h] = v.x;
+        b[j][2 * h + 1] = v.y;
+      }
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double b[NT][4], bn[NT][4];
+  if (a.w_early && kb < ke) loadB(kb, b);
+  pdl_wait();
+  if (!a.w_early && kb < ke) loadB(kb, b);
+  if (a.step && tid == 0 && blockIdx.x == 0 && rank == 0 && scene == 0) atomicAdd(a.step, 1);
+  if (kb < ke) stage(kb, 0);
+  int s = 0;
+  for (int k0 = kb; k0 < ke; k0 += FM_KCH, s ^= 1) {
+    if (k0 + FM_KCH < ke) {
+      stage(k0 + FM_KCH, s ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* xs = Xs + s * RPM * FM_XP + g * FM_XP + 4 * t;
+#pragma unroll
+    for (int kk = 0; kk < FM_KCH; kk += 16) {
+      const int k = k0 + kk;
+      if (k >= ke) break;
+      if (k + 16 < ke) loadB(k + 16, bn);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double2 a01 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk);
+        const double2 a23 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk + 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma(acc[i][j][0], acc[i][j][1], av[q], b[j][q]);
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[j][q] = bn[j][q];
+    }
+    __syncthreads();   // buffer s is restaged two chunks later; the last pass frees Xs for part
+  }
+  pdl_trigger();
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) part[(warp * NT * 8 + 8 * j + 2 * t + c) * RPM + 8 * i + g] = acc[i][j][c];
+  cluster.sync();
+
+  const double* bias = a.theta + scene * a.th_ss + a.b_off;
+  const int total = FM_WARPS * NT * 8 * RPM;
+  for (int e = rank * 256 + tid; e < total; e += CK * 256) {
+    const int wo = e / RPM, r = e % RPM;
+    const int gn = blockIdx.x * FM_WARPS * NT * 8 + wo;
+    if (gn >= N || r >= rows) continue;
+    double z = 0.0;
+    for (int c = 0; c < CK; ++c) z += cluster.map_shared_rank(part, c)[e];
+    z += bias[gn];
+    if (!a.final_layer) {
+      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+    } else {
+      const double yv = z * a.cout[(size_t)scene * N + gn];
+      const int half = N / 2;
+      const int f = gn < half ? gn : gn - half;
+      int view, m;
+      if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
+      const size_t off = ((size_t)scene * a.n + view) * a.M0 + m;
+      double* dst = reinterpret_cast<double*>(a.alpha_hat + off);
+      const double* src = reinterpret_cast<const double*>(a.alpha0 + off);
+      if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
+    }
+  }
+  cluster.sync();
+}
+
+// ---------------------------------------------------------------------------
+// Backward layer + fused Adam on DMMA (network.py:201-219, 248-264):
+//   g_W[n][k] = sum_r g_z[r][n] h[r][k]     (MMA: M = n, N = k, K = r)
+//   g_h[r][k] = sum_n g_z[r][n] W_old[n][k] (MMA: M = r, N = k, K = n)
+// A warp owns KT k-tiles (8 KT columns) and streams the n rows of its
+// cluster rank's range 8 at a time (an "n-tile").  W, m, v of each n-tile
+// arrive in the D-fragment layout of the g_W product (lane: row n0+g,
+// columns 2t, 2t+1 of each k-tile) through a per-lane cp.async ring BM_D
+// n-tiles deep, so the Adam update is element-wise in registers and enough
+// bytes are in flight to stream HBM; the old W values of the other lanes'
+// ring slots are the B fragments of the g_h product.  g_z chunks of BM_NCH
+// columns ride in the same cp.async groups (double-buffered); h stays in
+// registers as B fragments for the whole kernel.
+constexpr int BM_WARPS = 4;
+constexpr int BM_NCH = 32;              // n per staged g_z chunk (4 n-tiles)
+constexpr int BM_GP = BM_NCH + 4;       // pitch: conflict-free fragment reads in both products
+constexpr int BM_D = 4;                 // n-tiles in flight per lane (<= BM_NCH / 8 with two chunk buffers)
+
+__host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT) {
+  return ((size_t)2 * 8 * MT * BM_GP + (size_t)BM_D * 3 * KT * BM_WARPS * 32 * 2 +
+          (size_t)8 * MT * BM_WARPS * 8 * KT) * sizeof(double);
+}
+
+template <int MT, int KT, bool FUSED>
+__global__ void __launch_bounds__(BM_WARPS * 32) net_bwd_mma_kernel(NetBwdArgs<double> a) {
+  constexpr int RPM = 8 * MT, SEG = BM_NCH / 2, KC = 8 * KT, CW = BM_WARPS * KC;
+  constexpr int THR = BM_WARPS * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Gs = reinterpret_cast<double*>(smem_raw);              // 2 x [RPM][BM_GP]  g_z[r][c0 + i]
+  double2* ring = reinterpret_cast<double2*>(Gs + 2 * RPM * BM_GP);   // [BM_D][3][KT][THR]
+  double* cpart = reinterpret_cast<double*>(ring + BM_D * 3 * KT * THR);   // [RPM][CW]
+  __shared__ double bc_s[2];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CN = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int scene = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int K = a.K, N = a.N, rows = a.rows;
+  const int kw0 = blockIdx.x * CW + warp * KC;
+  const int nb = min(N, rank * a.ns), ne = min(N, nb + a.ns);
+  const int ntl = (ne - nb + 7) / 8;                 // n-tiles of this rank
+  const double* __restrict__ hin = a.hin + scene * a.hin_ss;
+  const double* __restrict__ gz = a.gz + scene * a.gz_ss;
+  double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  double* __restrict__ mW = FUSED ? a.m + scene * a.th_ss + a.w_off : nullptr;
+  double* __restrict__ vW = FUSED ? a.v + scene * a.th_ss + a.w_off : nullptr;
+  double* __restrict__ gW = FUSED ? nullptr : a.grad + scene * a.th_ss + a.w_off;
+  auto slot = [&](int sl, int arr, int j) { return ring + ((sl * 3 + arr) * KT + j) * THR; };
+
+  auto stage_gz = [&](int c) {          // chunk c of this rank (no commit)
+    const int n0 = nb + c * BM_NCH;
+    double* dst = Gs + (c & 1) * RPM * BM_GP;
+    for (int i = tid; i < RPM * SEG; i += THR) {
+      const int r = i / SEG, sg = i % SEG, gn = n0 + 2 * sg;
+      const bool ok = r < rows && gn < ne;
+      cp_async16(dst + r * BM_GP + 2 * sg, ok ? gz + (size_t)r * N + gn : gz, ok);
+    }
+  };
+  auto stage_w = [&](int it) {          // W, m, v of n-tile it into ring slot it % BM_D (no commit)
+    const int n = nb + 8 * it + g, sl = it % BM_D;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const int kk = kw0 + 8 * j + 2 * t;
+      const bool ok = n < ne && kk < K;
+      const size_t o = ok ? (size_t)n * K + kk : 0;
+      cp_async16(slot(sl, 0, j) + tid, W + o, ok);
+      if constexpr (FUSED) {
+        cp_async16(slot(sl, 1, j) + tid, mW + o, ok);
+        cp_async16(slot(sl, 2, j) + tid, vW + o, ok);
+      }
+    }
+  };
+
+  if (tid == 0) {
+    if (FUSED) {
+      const int tt = *a.step;
+      bc_s[0] = 1.0 / (1.0 - pow(a.b1, (double)tt));
+      bc_s[1] = 1.0 / (1.0 - pow(a.b2, (double)tt));
+    } else {
+      bc_s[0] = bc_s[1] = 1.0;
+    }
+  }
+  // W, m, v are final since the previous iteration: the first BM_D n-tiles
+  // are requested before the dependency wait
+  for (int it = 0; it < BM_D; ++it) {
+    if (it < ntl) stage_w(it);
+    cp_async_commit();
+  }
+  pdl_wait();
+  // h as B fragments of the g_W product: hf[j][s] = h[4s + t][kw0 + 8j + g]
+  double hf[KT][RPM / 4];
+#pragma unroll
+  for (int j = 0; j < KT; ++j)
+#pragma unroll
+    for (int s4 = 0; s4 < RPM / 4; ++s4) {
+      const int r = 4 * s4 + t, kk = kw0 + 8 * j + g;
+      hf[j][s4] = (r < rows && kk < K) ? hin[(size_t)r * K + kk] : 0.0;
+    }
+  double gh[MT][KT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) gh[i][j][0] = gh[i][j][1] = 0.0;
+  if (ntl > 0) stage_gz(0);
+  cp_async_commit();
+
+  int errbits = 0;
+  // g_h B fragment source: lane (4s+t)*4 + (g>>1) of this warp holds W[n0+4s+t][8j + g] in component g&1
+  const int bsrc = warp * 32 + (g >> 1);
+#pragma unroll 1
+  for (int it = 0; it < ntl; ++it) {
+    if (it == 0) cp_async_wait<0>(); else cp_async_wait<BM_D - 1>();
+    const int c = it >> 2, nt = (it & 3) * 8;
+    if ((it & 3) == 0) __syncthreads();   // chunk c visible to all; chunk c-1 no longer read
+    else __syncwarp();
+    const double* G = Gs + (c & 1) * RPM * BM_GP;
+    const double ibc1 = bc_s[0], ibc2 = bc_s[1];
+    const int sl = it % BM_D;
+    // bias of chunk c (network.py:213,217), by the first column tile
+    if ((it & 3) == 0 && blockIdx.x == 0 && tid < BM_NCH && nb + c * BM_NCH + tid < ne) {
+      double gb = 0.0;
+      for (int r = 0; r < rows; ++r) gb += G[r * BM_GP + tid];
+      const int gn = nb + c * BM_NCH + tid;
+      if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
+      if constexpr (FUSED) {
+        double* th = a.theta + scene * a.th_ss + a.b_off;
+        double* mb = a.m + scene * a.th_ss + a.b_off;
+        double* vb = a.v + scene * a.th_ss + a.b_off;
+        double p = th[gn], m1 = mb[gn], v1 = vb[gn];
+        adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
+        th[gn] = p; mb[gn] = m1; vb[gn] = v1;
+      } else {
+        a.grad[scene * a.th_ss + a.b_off + gn] = gb;
+      }
+    }
+    // g_W: NA independent accumulators break the dependent DMMA chain over the rows
+    constexpr int NA = RPM / 4 < 4 ? RPM / 4 : 4;
+    double gwp[NA][KT][2];
+#pragma unroll
+    for (int q = 0; q < NA; ++q)
+#pragma unroll
+      for (int j = 0; j < KT; ++j) gwp[q][j][0] = gwp[q][j][1] = 0.0;
+#pragma unroll
+    for (int s4 = 0; s4 < RPM / 4; ++s4) {
+      const double av = G[(4 * s4 + t) * BM_GP + nt + g];
+#pragma unroll
+      for (int j = 0; j < KT; ++j) dmma(gwp[s4 % NA][j][0], gwp[s4 % NA][j][1], av, hf[j][s4]);
+    }
+    // g_h with the old W tile (other lanes' ring slots)
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      double bw[KT];
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+        bw[j] = reinterpret_cast<const double*>(slot(sl, 0, j) + bsrc + (4 * s2 + t) * 4)[g & 1];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double av = G[(8 * i + g) * BM_GP + nt + 4 * s2 + t];
+#pragma unroll
+        for (int j = 0; j < KT; ++j) dmma(gh[i][j][0], gh[i][j][1], av, bw[j]);
+      }
+    }
+    const int n = nb + 8 * it + g;
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+      const int kk = kw0 + 8 * j + 2 * t;
+      double gw0 = gwp[0][j][0], gw1 = gwp[0][j][1];
+#pragma unroll
+      for (int q = 1; q < NA; ++q) { gw0 += gwp[q][j][0]; gw1 += gwp[q][j][1]; }
+      if (n < ne && kk < K) {
+        const size_t o = (size_t)n * K + kk;
+        if (!isfinite(gw0) || !isfinite(gw1)) errbits |= ERR_NONFINITE_GRAD;
+        if constexpr (FUSED) {
+          double2 p = slot(sl, 0, j)[tid], m2 = slot(sl, 1, j)[tid], v2 = slot(sl, 2, j)[tid];
+          adam_one<double>(p.x, m2.x, v2.x, gw0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+          adam_one<double>(p.y, m2.y, v2.y, gw1, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+          if (!isfinite(p.x) || !isfinite(p.y)) errbits |= ERR_NONFINITE_PARAM;
+          *reinterpret_cast<double2*>(W + o) = p;
+          *reinterpret_cast<double2*>(mW + o) = m2;
+          *reinterpret_cast<double2*>(vW + o) = v2;
+        } else {
+          *reinterpret_cast<double2*>(gW + o) = make_double2(gw0, gw1);
+        }
+      }
+    }
+    __syncwarp();   // every lane is done with ring slot sl before it is refilled
+    // refill: n-tile it + BM_D, and the g_z chunk it needs when it starts one
+    const int nx = it + BM_D;
+    if (nx < ntl) {
+      stage_w(nx);
+      if ((nx & 3) == 0) stage_gz(nx >> 2);
+    }
+    cp_async_commit();
+  }
+  pdl_trigger();
+  if (errbits) atomicOr(&a.err[scene], errbits);
+
+  if (a.gzprev) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) cpart[(8 * i + g) * CW + warp * KC + 8 * j + 2 * t + c] = gh[i][j][c];
+    cluster.sync();
+    for (int e = rank * THR + tid; e < rows * CW; e += CN * THR) {
+      const int r = e / CW, cl = e % CW, gk = blockIdx.x * CW + cl;
+      if (gk >= K) continue;
+      double sum = 0.0;
+      for (int q = 0; q < CN; ++q) sum += cluster.map_shared_rank(cpart, q)[e];
+      const double hv = hin[(size_t)r * K + gk];
+      a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = sum * (1.0 - hv * hv);
+    }
+    cluster.sync();
+  } else {
+    cp_async_wait<0>();
+  }
+}
+
+}  // namespace pdf

@@ -46,6 +46,7 @@ struct ViewArgs {
   double* norms;      // [S*n][CS]
   C<T>* grows;        // [S*n][R]
   double* dloss;      // [S*n]
+  int do_data;        // 0: the data term runs as a separate GEMM (data_gemm_kernel)
   // BWD
   const C<T>* gE;     // [S*n][M][M]
   const C<T>* gJloc;  // [S*n][M][M]
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
   }
 
-  if constexpr (MODE == VIEW_FWD) {
+  if (MODE == VIEW_FWD && a.do_data) {
     // partial data residual over my pixels: sum_p J[p] G_S[r, p]
     const size_t p0 = (size_t)y0 * M;
     const int np = rp * M;
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   }
   cluster.sync();
 
-  if constexpr (MODE == VIEW_FWD) {
+  if (MODE == VIEW_FWD && a.do_data) {
     if (rank == 0) {
       // D = sum of partials - d, masked; g_rows = 2 D mask / c_sca
       double part = 0.0;
