@@ -445,9 +445,11 @@ static cudaError_t fwd_mma_nt(int NT, dim3 grid, int CK, NetFwdArgs<double>& a, 
 static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
   const int MT = (c->rows + 7) / 8, S = c->d.S, N = a.N, K = a.K;
   auto ctas = [&](int nt) { return (long long)((N + 64 * nt - 1) / (64 * nt)) * S; };
+  // one n-tile per warp measured fastest in every regime (more CTAs and more
+  // W bytes in flight per SM); PDF_FWD_NT=2/4 for experiments
   int NT = 1;
-  if (MT <= 4 && ctas(4) >= 2 * 148) NT = 4;
-  else if (MT <= 8 && ctas(2) >= 148) NT = 2;
+  static const int nt_env = env_int("PDF_FWD_NT", 1);
+  if ((nt_env == 2 && MT <= 8) || (nt_env == 4 && MT <= 4)) NT = nt_env;
   static const int cap = env_int("PDF_FWD_CLUSTER", 8);
   const long long base = ctas(NT);
   const int kmax = (K + FM_KCH - 1) / FM_KCH;

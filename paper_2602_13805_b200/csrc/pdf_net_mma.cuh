@@ -26,7 +26,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-constexpr int FM_KCH = 64;              // k per staged input chunk
+constexpr int FM_KCH = 64;              // k per staged input chunk (4 k-blocks of 16)
 constexpr int FM_XP = FM_KCH + 2;       // pitch: conflict-free 16-byte fragment reads
 constexpr int FM_WARPS = 8;
 
@@ -39,10 +39,13 @@ __host__ __device__ constexpr size_t fwd_mma_smem_bytes(int MT, int NT) {
 // z[r][n] = sum_k x[r][k] W[n][k] + b[n] for one layer (network.py:107-120).
 // CTA = 8 warps x NT n-tiles of 8 outputs, all rows (MT m-tiles of 8), the
 // K range [rank*ks, ...) of its cluster rank; partial sums meet in DSMEM and
-// are added in rank order.
+// are added in rank order.  The B fragments (W) go straight from global
+// memory into registers one 64-wide chunk (four k-blocks) ahead of their use,
+// so each lane keeps 4 x NT x 32 bytes of W in flight; the input rows x are
+// staged per chunk with cp.async (double-buffered).
 template <int MT, int NT>
 __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) {
-  constexpr int RPM = 8 * MT, SEG = FM_KCH / 2;
+  constexpr int RPM = 8 * MT, SEG = FM_KCH / 2, THR = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Xs = reinterpret_cast<double*>(smem_raw);   // 2 x [RPM][FM_XP]
   double* part = Xs;                                   // after the k loop: [8*NT*8][RPM]
@@ -67,13 +70,14 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
   }
   auto stage = [&](int k0, int s) {
     double* dst = Xs + s * RPM * FM_XP;
-    for (int i = tid; i < RPM * SEG; i += 256) {
+    for (int i = tid; i < RPM * SEG; i += THR) {
       const int r = i / SEG, sg = i % SEG, gk = k0 + 2 * sg;
       const bool ok = r < rows && gk < ke;
       cp_async16(dst + r * FM_XP + 2 * sg, ok ? X + (size_t)r * K + gk : X, ok);
     }
     cp_async_commit();
   };
+  // B fragments of k-block k (lane: W[n][k + 4t .. k + 4t + 3])
   auto loadB = [&](int k, double (&b)[NT][4]) {
 #pragma unroll
     for (int j = 0; j < NT; ++j)
@@ -93,10 +97,13 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double b[NT][4], bn[NT][4];
-  if (a.w_early && kb < ke) loadB(kb, b);
-  pdl_wait();
-  if (!a.w_early && kb < ke) loadB(kb, b);
+  double b[4][NT][4];
+  // W1 is written by the launch right before (Adam of the previous
+  // iteration); W2, W3 two or more launches back and may stream early
+  if (!a.w_early) pdl_wait();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) loadB(kb + 16 * q, b[q]);
+  if (a.w_early) pdl_wait();
   if (a.step && tid == 0 && blockIdx.x == 0 && rank == 0 && scene == 0) atomicAdd(a.step, 1);
   if (kb < ke) stage(kb, 0);
   int s = 0;
@@ -110,29 +117,26 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
     __syncthreads();
     const double* xs = Xs + s * RPM * FM_XP + g * FM_XP + 4 * t;
 #pragma unroll
-    for (int kk = 0; kk < FM_KCH; kk += 16) {
-      const int k = k0 + kk;
-      if (k >= ke) break;
-      if (k + 16 < ke) loadB(k + 16, bn);
+    for (int q = 0; q < 4; ++q) {
+      const int kk = 16 * q;
+      if (k0 + kk < ke) {
 #pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const double2 a01 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk);
-        const double2 a23 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk + 2);
-        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        for (int i = 0; i < MT; ++i) {
+          const double2 a01 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk);
+          const double2 a23 = *reinterpret_cast<const double2*>(xs + i * 8 * FM_XP + kk + 2);
+          const double av[4] = {a01.x, a01.y, a23.x, a23.y};
 #pragma unroll
-        for (int j = 0; j < NT; ++j)
+          for (int j = 0; j < NT; ++j)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) dmma(acc[i][j][0], acc[i][j][1], av[q], b[j][q]);
+            for (int u = 0; u < 4; ++u) dmma(acc[i][j][0], acc[i][j][1], av[u], b[q][j][u]);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) b[j][q] = bn[j][q];
+      loadB(k0 + FM_KCH + kk, b[q]);     // the same slot one chunk ahead (zero past ke)
     }
     __syncthreads();   // buffer s is restaged two chunks later; the last pass frees Xs for part
   }
   pdl_trigger();
-  __syncthreads();
+  __syncthreads();                        // Xs is reused as the partial-sum buffer
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
