@@ -119,3 +119,20 @@ def test_network_many_rows_matches_oracle(tiny_setup, n):
     dev.check_errors()
     assert rel(grad[0].cpu().numpy(), want) < 1e-10
     assert abs(bd[0, 5].item() - parts["total"]) < 1e-10 * abs(parts["total"])
+
+
+def test_cfg5_trajectory_gate(cfg5):
+    """BASELINE config 5: 300 iterations at 256 x 256 / 72 views; the final
+    relative contrast error within 1e-3 of the reference's (north-star gate)."""
+    from paper_2602_13805_b200.api import BatchReconstructor
+    st, g = cfg5
+    if "trace" not in g:
+        pytest.skip("cfg5 golden has no trajectory")
+    rb = BatchReconstructor(st.cfg, 1, e_inc=st.e_inc)
+    res = rb.run([g["data"]], seeds=[st.cfg.rng_seed], chi_trues=[g["chi_true"]])[0]
+    assert rel(res.chi0.values, g["chi0"]) < 1e-10
+    tr = np.array([b.as_row() for b in res.trace])
+    assert tr.shape == g["trace"].shape
+    np.testing.assert_allclose(tr[:3, 5], g["trace"][:3, 5], rtol=1e-9)
+    assert abs(res.rel_error - float(g["rel_error"])) < 1e-3, (res.rel_error, float(g["rel_error"]))
+    print(f"cfg5: rel_error {res.rel_error:.6f} vs reference {float(g['rel_error']):.6f}")
