@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-sample-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--large-iters", type=int, default=300, help="iterations of the config-5 leg; 0 = skip")
     return ap.parse_args()
 
 
@@ -228,6 +229,66 @@ def algorithmic_work(dev, phase: str):
     return "hbm", S * es * (6 * N_ * K_ + rows * (K_ + 2 * N_))
 
 
+def large_leg(args, d: Dist):
+    """BASELINE config 5: one 256x256 scene, 72 incidences / receivers, m_f = 16.
+    N = 1: the whole scene on one GPU (CUDA-graph replay).  N > 1: incidences
+    sharded over the ranks, three NCCL allreduces per iteration (sharded.py)."""
+    import torch
+    from paper_2602_13805_b200 import build_grid, plane_wave_fields
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, TorchDistReducer, run_sharded
+    from paper_2602_13805_b200.workloads import baseline_config, baseline_scene, synthesize_gpu
+    k = args.large_iters
+    cfg = baseline_config(5, k_iters=k)
+    scene, rng, snr = baseline_scene(5)
+    data, chi_true = synthesize_gpu(cfg, [scene], [rng], snr)
+    e_inc = plane_wave_fields(cfg, build_grid(cfg)).views
+    rec = BatchReconstructor(cfg, 1, e_inc=e_inc, dtype=args.dtype)
+    theta0 = torch.as_tensor(_theta0([cfg.rng_seed], rec.m0_eff), dtype=rec.dev.rdt, device=rec.dev.device)
+    out = {"workload": "cfg5: 256x256 on [-2,2] lambda, 72 plane-wave incidences, 72 receivers at 5 lambda, "
+                       f"m_f=16 (31x31 modes, 33.6 M network parameters), {k} Adam iterations"}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if d.world == 1:
+        dev = rec.dev
+        dev.set_data(data)
+        _, r0 = dev.bp_initialize()
+        dev.net_setup(dev.init_alpha(r0))
+        th, m, v = theta0.clone(), torch.zeros_like(theta0), torch.zeros_like(theta0)
+        tr = torch.zeros(k, 1, 6, dtype=torch.float64, device=dev.device)
+        dev.train(th, m, v, 0, 20, tr)
+        th.copy_(theta0); m.zero_(); v.zero_()
+        torch.cuda.synchronize()
+        e0.record()
+        dev.train(th, m, v, 0, k, tr)
+        e1.record()
+        torch.cuda.synchronize()
+        dev.check_errors()
+        secs = e0.elapsed_time(e1) / 1e3
+        th.copy_(theta0); m.zero_(); v.zero_()
+        out.update({"mode": "single GPU, CUDA graph", "phases_ms": dev.profile_phases(th, m, v, 0, 5),
+                    "final_loss_total": float(tr[-1, 0, 5])})
+        del dev
+    else:
+        c = cfg
+        sh = IncidenceShard(rec.ops, e_inc, data[0], mf=c.m_f, beta=c.beta, lambdas=rec.lambdas, tau_b=c.tau_b,
+                            rank=d.rank, world=d.world)
+        red = TorchDistReducer()
+        run_sharded([sh], red, theta0, 3, trace_on_device=True)
+        torch.cuda.synchronize()
+        d.barrier()
+        e0.record()
+        _, tr = run_sharded([sh], red, theta0, k, trace_on_device=True)
+        e1.record()
+        torch.cuda.synchronize()
+        secs = d.max(e0.elapsed_time(e1) / 1e3)
+        out.update({"mode": f"incidence-sharded over {d.world} GPUs ({len(sh.own)} views on rank {d.rank}), "
+                            "NCCL allreduce of num/den, g_R and the flat gradient per iteration",
+                    "final_loss_total": float(tr[-1, 5])})
+    out.update({"iter_per_s": k / secs, "ms_per_iter": 1e3 * secs / k, "s_per_reconstruction": secs,
+                "scaling": "strong (one scene, incidences split over the GPUs)"})
+    return out
+
+
 def run_ours(args, d: Dist):
     import torch
     from paper_2602_13805_b200 import plane_wave_fields, build_grid
@@ -284,6 +345,9 @@ def run_ours(args, d: Dist):
     dev.check_errors()
     final_total = float(trace[-1, 0, 5].item())
 
+    # kernels per fused iteration: 3 forward layers, view_fwd, pixel, view_bwd
+    # (loss finalize fused), 3 backward layers with Adam
+    launches_per_iter = 9
     # ---- per-kernel live timing (events between kernels of un-graphed iterations)
     theta.copy_(theta0); m.zero_(); v.zero_()
     phases = dev.profile_phases(theta, m, v, 0, 20)
@@ -366,6 +430,13 @@ def run_ours(args, d: Dist):
                    "median_rel_error": float(np.median(rels)), "phases_ms": phb,
                    "scaling": "strong (256 scenes split over the GPUs)"}
 
+    large = None
+    if args.large_iters:
+        try:
+            large = large_leg(args, d)
+        except Exception as ex:   # reported, never fatal for the headline line
+            large = {"error": f"{type(ex).__name__}: {ex}"}
+
     cpu = None
     if d.rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.cpu_sample_iters)
@@ -384,7 +455,7 @@ def run_ours(args, d: Dist):
                     "rel_error": res[0].rel_error},
             "roofline": roof, "phases_ms": phases, "fp64_peak_tflops_measured": fp64_peak_tflops,
             "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": args.steps * (1 + 10 * k), "batched": batched}
+            "gpu_launches": args.steps * (1 + launches_per_iter * k), "batched": batched, "large": large}
     if d.rank == 0:
         print(json.dumps(line), flush=True)
 

@@ -121,16 +121,19 @@ class LocalShards:
                 g.copy_(t)
 
 
-def run_sharded(shards, reduce, theta0, k_iters: int, lr: float = 1e-2):
+def run_sharded(shards, reduce, theta0, k_iters: int, lr: float = 1e-2, trace_on_device: bool = False):
     """k incidence-sharded Adam iterations for the given (local) shards.
 
     Returns (thetas per shard, trace [k][6]).  Every shard keeps its own copy
-    of the replicated parameters and Adam state."""
+    of the replicated parameters and Adam state.  trace_on_device keeps the
+    breakdown rows on the GPU (no per-iteration host synchronisation) and
+    returns them as a tensor."""
     thetas = [theta0.clone() for _ in shards]
     ms = [torch.zeros_like(theta0) for _ in shards]
     vs = [torch.zeros_like(theta0) for _ in shards]
     grads = [torch.zeros_like(theta0) for _ in shards]
     trace = []
+    dtrace = torch.zeros(k_iters, 6, dtype=torch.float64, device=shards[0].bd.device) if trace_on_device else None
     for t in range(1, k_iters + 1):
         for s, th in zip(shards, thetas):
             s.step_a(th)
@@ -145,12 +148,15 @@ def run_sharded(shards, reduce, theta0, k_iters: int, lr: float = 1e-2):
         else:
             for g in grads:
                 reduce(shards, g)
-        trace.append(shards[0].bd[0].cpu().numpy().copy())
+        if dtrace is not None:
+            dtrace[t - 1].copy_(shards[0].bd[0])
+        else:
+            trace.append(shards[0].bd[0].cpu().numpy().copy())
         for s, th, m, v, g in zip(shards, thetas, ms, vs, grads):
             s.dev.adam_step(th, m, v, g, t)
     for s in shards:
         s.dev.check_errors()
-    return thetas, np.array(trace)
+    return thetas, (dtrace if dtrace is not None else np.array(trace))
 
 
 def sharded_chi(shards, reduce, thetas):
