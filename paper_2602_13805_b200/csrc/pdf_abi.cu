@@ -63,7 +63,7 @@ struct pdf_ctx {
   int M, P, E, K, M0, CS, rows, D0, H, RB, TX, ntiles;
   // large-grid view path (pdf_view_large.cuh): partials per view, views per
   // spectrum chunk, data-GEMM pixel chunking
-  int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks;
+  int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks, dg_nq;
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
@@ -164,15 +164,21 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
     long long ch = std::max(1LL, budget / per);
     c->chunk = (int)std::min<long long>(ch, (long long)d->S * d->n);
   }
-  // data term as a split-K GEMM (always on the large-grid path; PDF_DATA_GEMM=1
-  // selects it for the cluster path too)
-  c->dgemm = c->large || (env_int("PDF_DATA_GEMM", 0) && M >= 32);
+  // data term as a split-K GEMM over all views of a scene (G_S read once per
+  // scene instead of once per view): always on the large-grid path, and on
+  // the cluster path for float64 batches (DMMA; measured -27% view_fwd at 128
+  // scenes, +10 us per iteration for one scene where the in-kernel term wins)
+  const int dg_env = env_int("PDF_DATA_GEMM", -1);
+  c->dgemm = c->large || (M >= 32 && (dg_env == 1 || (dg_env < 0 && d->dtype == PDF_F64 && d->S >= 4)));
+  c->dg_nq = 1;
   if (c->dgemm) {
     const int npix = M * M;
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
     want = std::min(want, npix / DG_KC);
     c->dg_chunk = ((npix + want - 1) / want + DG_KC - 1) / DG_KC * DG_KC;
     c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
+    const int ntp = ((d->n + 7) / 8) * ((d->R + 8 * DM_NTL - 1) / (8 * DM_NTL));
+    c->dg_nq = std::max(1, std::min(4, 8 / ntp));
     if (d->n > 80 || d->R > 80) return fail(PDF_EINVAL, "at most 80 incidences / receivers for the data GEMM");
   }
   c->rsz = d->dtype == PDF_F64 ? 8 : 4;
@@ -320,9 +326,14 @@ static int data_term(pdf_ctx* c, cudaStream_t st) {
   g.J = (const C<T>*)c->J; g.gs = (const C<T>*)c->d.gs_matrix; g.dpart = (C<T>*)c->dpart;
   g.data = (const C<T>*)c->d.data; g.mask = (const T*)c->d.mask; g.c_sca = c->c_sca;
   g.grows = (C<T>*)c->grows; g.dloss = c->dloss;
+  g.nq = c->dg_nq;
   void* args[] = {&g};
-  cudaError_t e = plain_launch(data_gemm_kernel<T>, dim3(c->dg_nchunks, c->d.S), dim3(dg_threads<T>(g.n, g.R)),
-                               dg_smem<T>(g.n, g.R), st, args);
+  cudaError_t e;
+  if constexpr (sizeof(T) == 8)
+    e = plain_launch(data_mma_kernel, dim3(c->dg_nchunks, c->d.S), dim3(256), dm_smem(g.n, g.R, g.nq), st, args);
+  else
+    e = plain_launch(data_gemm_kernel<T>, dim3(c->dg_nchunks, c->d.S), dim3(dg_threads<T>(g.n, g.R)),
+                     dg_smem<T>(g.n, g.R), st, args);
   if (e == cudaSuccess) e = plain_launch(data_reduce_kernel<T>, dim3(c->d.S * c->d.n), dim3(128), 0, st, args);
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("data term: ") + cudaGetErrorString(e));
   return PDF_OK;

@@ -16,8 +16,9 @@
 //               g_J = g_J_local + G_D^H g_E and the truncation partials)
 //
 // The data term D = J G_S^T - d (losses.py:229-232) is a tall complex GEMM
-// (views x pixels) x (pixels x receivers) here: data_gemm_kernel splits the
-// pixels over CTAs with register-tiled 4x4 outputs and a fixed-order reduce.
+// (views x pixels) x (pixels x receivers) here: data_mma_kernel (float64,
+// DMMA) or data_gemm_kernel (float32, register-tiled 4x4 outputs) split the
+// pixels over CTAs, and a fixed-order reduce finishes D.
 // The warp FFT, the K^ permutation and every reduction order are the ones the
 // cluster path uses (pdf_view.cuh), so both paths are interchangeable; the
 // cluster path is kept for M <= 128 where its DSMEM transposes win.
@@ -301,6 +302,7 @@ __global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
 template <typename T>
 struct DataArgs {
   int n, R, npix, chunk, nchunks;
+  int nq;               // pixel sub-ranges per chunk (data_mma_kernel)
   const C<T>* J;        // [S*n][npix]
   const C<T>* gs;       // [R][npix]
   C<T>* dpart;          // [S][nchunks][n][R]
@@ -407,6 +409,96 @@ __global__ void __launch_bounds__(512) data_gemm_kernel(DataArgs<T> a) {
       const int vi = ti + NI * i, r = tr + NR * j;
       if (vi < n && r < R) dp[vi * R + r] = acc[i][j];
     }
+}
+
+// The same split-K data GEMM on the FP64 tensor cores (mma.m8n8k4, see
+// pdf_net_mma.cuh for the fragment layouts).  A work item is (8 views, 16
+// receivers, a pixel sub-range); a complex product is four real MMAs
+// (Dr += Jr Gr - Ji Gi, Di += Jr Gi + Ji Gr).  Lane (g, t) streams pixels
+// p + 4t .. p + 4t + 3 of one J row and of two G_S rows as 64-byte pieces
+// (k permuted identically in A and B), so a 4-lane group reads 256
+// contiguous bytes.  Sub-range partials meet in shared memory in a fixed
+// order; chunk partials are summed by data_reduce_kernel.
+constexpr int DM_NTL = 2;   // receiver n-tiles (of 8) per work item
+
+__host__ __device__ inline size_t dm_smem(int n, int R, int nq) {
+  return (size_t)nq * 8 * ((n + 7) / 8) * (8 * DM_NTL) * ((R + 8 * DM_NTL - 1) / (8 * DM_NTL)) * 16;
+}
+
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = a.n, R = a.R, npix = a.npix, NQ = a.nq;
+  const int MTs = (n + 7) / 8, RGs = (R + 8 * DM_NTL - 1) / (8 * DM_NTL), NTP = MTs * RGs;
+  const int NP = 8 * MTs, RP = 8 * DM_NTL * RGs;
+  double2* part = reinterpret_cast<double2*>(smem_raw);   // [NQ][NP][RP]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int chunk = blockIdx.x, scene = blockIdx.y;
+  const int p0 = chunk * a.chunk, p1 = min(npix, p0 + a.chunk);
+  const int sub = ((a.chunk + NQ - 1) / NQ + 15) / 16 * 16;
+  const double2* J = reinterpret_cast<const double2*>(a.J) + (size_t)scene * n * npix;
+  const double2* G = reinterpret_cast<const double2*>(a.gs);
+  pdl_wait();
+  for (int item = warp; item < NTP * NQ; item += 8) {
+    const int tp = item % NTP, q = item / NTP, mt = tp / RGs, rg = tp % RGs;
+    const int v = 8 * mt + g;
+    const double2* jr = J + (size_t)(v < n ? v : 0) * npix;
+    const double2* gr[DM_NTL];
+    bool rok[DM_NTL];
+#pragma unroll
+    for (int j = 0; j < DM_NTL; ++j) {
+      const int r = rg * 8 * DM_NTL + 8 * j + g;
+      rok[j] = r < R;
+      gr[j] = G + (size_t)(rok[j] ? r : 0) * npix;
+    }
+    double dr[DM_NTL][2], di[DM_NTL][2];
+#pragma unroll
+    for (int j = 0; j < DM_NTL; ++j) dr[j][0] = dr[j][1] = di[j][0] = di[j][1] = 0.0;
+    const int ps = p0 + q * sub, pe = min(p1, ps + sub);
+    for (int p = ps; p < pe; p += 16) {
+      double2 jv[4], gv[DM_NTL][4];
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int pp = p + 4 * t + s4;
+        const bool ok = pp < pe;
+        jv[s4] = (ok && v < n) ? jr[pp] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < DM_NTL; ++j) gv[j][s4] = (ok && rok[j]) ? gr[j][pp] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4)
+#pragma unroll
+        for (int j = 0; j < DM_NTL; ++j) {
+          dmma_f64(dr[j][0], dr[j][1], jv[s4].x, gv[j][s4].x);
+          dmma_f64(dr[j][0], dr[j][1], -jv[s4].y, gv[j][s4].y);
+          dmma_f64(di[j][0], di[j][1], jv[s4].x, gv[j][s4].y);
+          dmma_f64(di[j][0], di[j][1], jv[s4].y, gv[j][s4].x);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < DM_NTL; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        part[((size_t)q * NP + v) * RP + rg * 8 * DM_NTL + 8 * j + 2 * t + c] = make_double2(dr[j][c], di[j][c]);
+  }
+  __syncthreads();
+  pdl_trigger();
+  double2* dp = reinterpret_cast<double2*>(a.dpart) + ((size_t)scene * a.nchunks + chunk) * n * R;
+  for (int e = tid; e < n * R; e += blockDim.x) {
+    const int v = e / R, r = e % R;
+    double2 acc = part[(size_t)v * RP + r];
+    for (int q = 1; q < NQ; ++q) {
+      const double2 x = part[((size_t)q * NP + v) * RP + r];
+      acc.x += x.x;
+      acc.y += x.y;
+    }
+    dp[e] = acc;
+  }
 }
 
 // D = sum of chunk partials - d (masked), g_rows = 2 D mask / c_sca, ||D||^2 per view
