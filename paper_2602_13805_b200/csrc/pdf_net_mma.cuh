@@ -184,10 +184,10 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
 // ring slots are the B fragments of the g_h product.  g_z chunks of BM_NCH
 // columns ride in the same cp.async groups (double-buffered); h stays in
 // registers as B fragments for the whole kernel.
-constexpr int BM_WARPS = 4;
+constexpr int BM_WARPS = 8;
 constexpr int BM_NCH = 32;              // n per staged g_z chunk (4 n-tiles)
 constexpr int BM_GP = BM_NCH + 4;       // pitch: conflict-free fragment reads in both products
-constexpr int BM_D = 4;                 // n-tiles in flight per lane (<= BM_NCH / 8 with two chunk buffers)
+constexpr int BM_D = 3;                 // n-tiles in flight per lane (<= BM_NCH / 8 with two chunk buffers)
 
 __host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT) {
   return ((size_t)2 * 8 * MT * BM_GP + (size_t)BM_D * 3 * KT * BM_WARPS * 32 * 2 +
