@@ -270,8 +270,14 @@ def large_leg(args, d: Dist):
         del dev
     else:
         c = cfg
-        sh = IncidenceShard(rec.ops, e_inc, data[0], mf=c.m_f, beta=c.beta, lambdas=rec.lambdas, tau_b=c.tau_b,
-                            rank=d.rank, world=d.world)
+        err = None
+        try:
+            sh = IncidenceShard(rec.ops, e_inc, data[0], mf=c.m_f, beta=c.beta, lambdas=rec.lambdas, tau_b=c.tau_b,
+                                rank=d.rank, world=d.world)
+        except Exception as ex:      # every rank must agree before the first collective of the loop
+            err = f"{type(ex).__name__}: {ex}"
+        if d.max(1.0 if err else 0.0) > 0:
+            raise RuntimeError(err or "incidence-shard setup failed on another rank")
         red = TorchDistReducer()
         run_sharded([sh], red, theta0, 3, trace_on_device=True)
         torch.cuda.synchronize()
