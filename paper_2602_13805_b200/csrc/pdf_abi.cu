@@ -530,27 +530,31 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
 }
 
 // DMMA backward layer (float64)
-template <int MT, int KT>
+template <int MT, int KT, int WB>
 static cudaError_t bwd_mma_launch(bool fused, dim3 grid, int CN, NetBwdArgs<double>& a, cudaStream_t st) {
-  const size_t smem = bwd_mma_smem_bytes(MT, KT);
+  const size_t smem = bwd_mma_smem_bytes(MT, KT, WB);
   void* args[] = {&a};
   cudaError_t e;
   if (fused) {
-    auto k = net_bwd_mma_kernel<MT, KT, true>;
+    auto k = net_bwd_mma_kernel<MT, KT, true, WB>;
     e = prep(k, smem);
-    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(BM_WARPS * 32), smem, st, dim3(1, CN, 1), args);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, CN, 1), args);
   } else {
-    auto k = net_bwd_mma_kernel<MT, KT, false>;
+    auto k = net_bwd_mma_kernel<MT, KT, false, WB>;
     e = prep(k, smem);
-    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(BM_WARPS * 32), smem, st, dim3(1, CN, 1), args);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, CN, 1), args);
   }
   return e;
 }
 
 template <int MT>
-static cudaError_t bwd_mma_kt(int KT, bool fused, dim3 grid, int CN, NetBwdArgs<double>& a, cudaStream_t st) {
-  if constexpr (MT <= 4) { if (KT == 2) return bwd_mma_launch<MT, 2>(fused, grid, CN, a, st); }
-  return bwd_mma_launch<MT, 1>(fused, grid, CN, a, st);
+static cudaError_t bwd_mma_kt(int KT, int WB, bool fused, dim3 grid, int CN, NetBwdArgs<double>& a,
+                              cudaStream_t st) {
+  if constexpr (MT <= 4) {
+    if (KT == 2) return WB == 8 ? bwd_mma_launch<MT, 2, 8>(fused, grid, CN, a, st)
+                                : bwd_mma_launch<MT, 2, 4>(fused, grid, CN, a, st);
+  }
+  return WB == 8 ? bwd_mma_launch<MT, 1, 8>(fused, grid, CN, a, st) : bwd_mma_launch<MT, 1, 4>(fused, grid, CN, a, st);
 }
 
 static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStream_t st) {
@@ -560,7 +564,8 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   int KT = 1;
   if (MT <= 4 && (long long)((K + 63) / 64) * S >= 2 * 148) KT = 2;
   if (kt_env == 1 || (kt_env == 2 && MT <= 4)) KT = kt_env;
-  const int CW = BM_WARPS * 8 * KT;
+  const int WB = S >= 4 ? BM_WARPS : 4;     // one scene: narrower CTAs, more of them
+  const int CW = WB * 8 * KT;
   static const int cap = env_int("PDF_BWD_CLUSTER", 16);
   const long long base = (long long)((K + CW - 1) / CW) * S;
   const int nmax = (N + BM_NCH - 1) / BM_NCH;
@@ -570,16 +575,16 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   const dim3 grid((K + CW - 1) / CW, CN, S);
   cudaError_t e;
   switch (MT) {
-    case 1: e = bwd_mma_kt<1>(KT, fused, grid, CN, a, st); break;
-    case 2: e = bwd_mma_kt<2>(KT, fused, grid, CN, a, st); break;
-    case 3: e = bwd_mma_kt<3>(KT, fused, grid, CN, a, st); break;
-    case 4: e = bwd_mma_kt<4>(KT, fused, grid, CN, a, st); break;
-    case 5: e = bwd_mma_kt<5>(KT, fused, grid, CN, a, st); break;
-    case 6: e = bwd_mma_kt<6>(KT, fused, grid, CN, a, st); break;
-    case 7: e = bwd_mma_kt<7>(KT, fused, grid, CN, a, st); break;
-    case 8: e = bwd_mma_kt<8>(KT, fused, grid, CN, a, st); break;
-    case 9: e = bwd_mma_kt<9>(KT, fused, grid, CN, a, st); break;
-    case 10: e = bwd_mma_kt<10>(KT, fused, grid, CN, a, st); break;
+    case 1: e = bwd_mma_kt<1>(KT, WB, fused, grid, CN, a, st); break;
+    case 2: e = bwd_mma_kt<2>(KT, WB, fused, grid, CN, a, st); break;
+    case 3: e = bwd_mma_kt<3>(KT, WB, fused, grid, CN, a, st); break;
+    case 4: e = bwd_mma_kt<4>(KT, WB, fused, grid, CN, a, st); break;
+    case 5: e = bwd_mma_kt<5>(KT, WB, fused, grid, CN, a, st); break;
+    case 6: e = bwd_mma_kt<6>(KT, WB, fused, grid, CN, a, st); break;
+    case 7: e = bwd_mma_kt<7>(KT, WB, fused, grid, CN, a, st); break;
+    case 8: e = bwd_mma_kt<8>(KT, WB, fused, grid, CN, a, st); break;
+    case 9: e = bwd_mma_kt<9>(KT, WB, fused, grid, CN, a, st); break;
+    case 10: e = bwd_mma_kt<10>(KT, WB, fused, grid, CN, a, st); break;
     default: return fail(PDF_EINVAL, "rows");
   }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net bwd (dmma): ") + cudaGetErrorString(e));

@@ -184,20 +184,20 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
 // ring slots are the B fragments of the g_h product.  g_z chunks of BM_NCH
 // columns ride in the same cp.async groups (double-buffered); h stays in
 // registers as B fragments for the whole kernel.
-constexpr int BM_WARPS = 8;
+constexpr int BM_WARPS = 8;              // warps per CTA for batches (4 for one scene: more CTAs)
 constexpr int BM_NCH = 32;              // n per staged g_z chunk (4 n-tiles)
 constexpr int BM_GP = BM_NCH + 4;       // pitch: conflict-free fragment reads in both products
 constexpr int BM_D = 3;                 // n-tiles in flight per lane (<= BM_NCH / 8 with two chunk buffers)
 
-__host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT) {
-  return ((size_t)2 * 8 * MT * BM_GP + (size_t)BM_D * 3 * KT * BM_WARPS * 32 * 2 +
-          (size_t)8 * MT * BM_WARPS * 8 * KT) * sizeof(double);
+__host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT, int WB) {
+  return ((size_t)2 * 8 * MT * BM_GP + (size_t)BM_D * 3 * KT * WB * 32 * 2 +
+          (size_t)8 * MT * WB * 8 * KT) * sizeof(double);
 }
 
-template <int MT, int KT, bool FUSED>
-__global__ void __launch_bounds__(BM_WARPS * 32) net_bwd_mma_kernel(NetBwdArgs<double> a) {
-  constexpr int RPM = 8 * MT, SEG = BM_NCH / 2, KC = 8 * KT, CW = BM_WARPS * KC;
-  constexpr int THR = BM_WARPS * 32;
+template <int MT, int KT, bool FUSED, int WB>
+__global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double> a) {
+  constexpr int RPM = 8 * MT, SEG = BM_NCH / 2, KC = 8 * KT, CW = WB * KC;
+  constexpr int THR = WB * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Gs = reinterpret_cast<double*>(smem_raw);              // 2 x [RPM][BM_GP]  g_z[r][c0 + i]
   double2* ring = reinterpret_cast<double2*>(Gs + 2 * RPM * BM_GP);   // [BM_D][3][KT][THR]

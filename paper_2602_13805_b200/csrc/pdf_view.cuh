@@ -205,6 +205,10 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
   }
 
+  // Split cluster barrier: the arrive releases my stage-A scatter; the data
+  // term (local rows, G_S from L2) then runs while the other CTAs finish
+  // theirs, and the wait acquires everyone's scatter before stage B.
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (MODE == VIEW_FWD && a.do_data) {
     // partial data residual over my pixels: sum_p J[p] G_S[r, p]
     const size_t p0 = (size_t)y0 * M;
@@ -230,27 +234,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       }
     }
   }
-  cluster.sync();
-
-  if (MODE == VIEW_FWD && a.do_data) {
-    if (rank == 0) {
-      // D = sum of partials - d, masked; g_rows = 2 D mask / c_sca
-      double part = 0.0;
-      const double csca = a.c_sca[scene];
-      for (int r = tid; r < a.R; r += blockDim.x) {
-        C<T> acc = czero<T>();
-        for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * a.R + r]);
-        const size_t di = (size_t)v * a.R + r;
-        C<T> d = csub<T>(acc, a.data[di]);
-        T mk_ = a.mask ? a.mask[di] : T(1);
-        d = cscale<T>(d, mk_);
-        part += (double)cabs2<T>(d);
-        a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
-      }
-      double tot = block_sum_d<T>(part, red);
-      if (tid == 0) a.dloss[v] = tot;
-    }
-  }
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
   // ---------------- stage B: columns: FFT, x K^, inverse FFT ---------------
   for (int cc = warp; cc < cp; cc += nw) {
@@ -279,7 +263,27 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       rb[(size_t)yl * Pp + posc] = x[k];
     }
   }
-  cluster.sync();
+  cluster.sync();   // also publishes the data partials (written before this arrive) to rank 0
+
+  if (MODE == VIEW_FWD && a.do_data) {
+    if (rank == 0) {
+      // D = sum of partials - d, masked; g_rows = 2 D mask / c_sca
+      double part = 0.0;
+      const double csca = a.c_sca[scene];
+      for (int r = tid; r < a.R; r += blockDim.x) {
+        C<T> acc = czero<T>();
+        for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * a.R + r]);
+        const size_t di = (size_t)v * a.R + r;
+        C<T> d = csub<T>(acc, a.data[di]);
+        T mk_ = a.mask ? a.mask[di] : T(1);
+        d = cscale<T>(d, mk_);
+        part += (double)cabs2<T>(d);
+        a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
+      }
+      double tot = block_sum_d<T>(part, red);
+      if (tid == 0) a.dloss[v] = tot;
+    }
+  }
 
   // ---------------- stage C: inverse row FFTs, crop ------------------------
   double nrm = 0.0;
