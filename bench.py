@@ -295,6 +295,39 @@ def large_leg(args, d: Dist):
     return out
 
 
+PHASE_KERNEL = {"view_fwd": "view_kernel<double, 4, 0>", "view_bwd": "view_kernel<double, 4, 1>",
+                "pixel": "pixel_kernel<double, 1>", "fwd_l1": "net_fwd_mma_kernel", "fwd_l2": "net_fwd_mma_kernel",
+                "fwd_l3": "net_fwd_mma_kernel", "bwd_l1": "net_bwd_mma_kernel", "bwd_l2": "net_bwd_mma_kernel",
+                "bwd_l3": "net_bwd_mma_kernel"}
+
+
+def ncu_traffic(phase: str):
+    """Mean DRAM bytes (read + write) per launch of the phase's kernel from the
+    committed ncu launch list of this bench command (profiles/), else None."""
+    import glob
+    import gzip
+    import csv
+    files = sorted(glob.glob(os.path.join(HERE, "profiles", "*_launches_cfg2.csv.gz")))
+    key = PHASE_KERNEL.get(phase)
+    if not files or not key:
+        return None
+    try:
+        rows = list(csv.reader(gzip.open(files[-1], "rt")))
+        hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+        h = rows[hi]
+        ki, mi, vi, idi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+        ui = h.index("Metric Unit")
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        per = {}
+        for r in rows[hi + 1:]:
+            if key in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                per[r[idi]] = per.get(r[idi], 0.0) + float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        return {"bytes_per_launch": float(np.mean(list(per.values()))), "launches": len(per),
+                "source": os.path.relpath(files[-1], HERE)} if per else None
+    except Exception:
+        return None
+
+
 def run_ours(args, d: Dist):
     import torch
     from paper_2602_13805_b200 import plane_wave_fields, build_grid
@@ -376,8 +409,8 @@ def run_ours(args, d: Dist):
         achieved = work / launch_s / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak_tflops, "peak_source": "pdf_fp64_probe DFMA kernel (measured live)"}
-    roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom], "traffic": None,
-                 "share_of_step": share[dom]})
+    roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom],
+                 "traffic": ncu_traffic(dom), "share_of_step": share[dom]})
 
     # ---- e2e through the public API with host buffers (per step: H2D data, D2H results)
     res = rec.run([data[0]], seeds=[cfg.rng_seed], chi_trues=[chi_true[0]])   # warm (theta0 cache)
