@@ -16,15 +16,10 @@
 // lanes of a group cover a 128-byte line).
 #pragma once
 #include "pdf_common.cuh"
+#include "pdf_dmma.cuh"
 #include "pdf_net.cuh"
 
 namespace pdf {
-
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 constexpr int FM_KCH = 64;              // k per staged input chunk (4 k-blocks of 16)
 constexpr int FM_XP = FM_KCH + 2;       // pitch: conflict-free 16-byte fragment reads

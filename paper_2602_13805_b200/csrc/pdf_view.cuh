@@ -21,6 +21,7 @@
 //   C: inverse row FFTs of my rows, crop to M columns
 #pragma once
 #include "pdf_common.cuh"
+#include "pdf_dmma.cuh"
 #include "pdf_pixel.cuh"
 
 namespace pdf {
@@ -150,28 +151,48 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
     __syncthreads();
     // V[yl][w] = sum_u A[u][w] exp(+2 pi i kr_u y / M)  -> stored after A
+    // J[yl][x] = sum_w V[yl][w] exp(+2 pi i kc_w x / M) / (m1 m2)
     C<T>* V = s.small + M0;
-    for (int i = tid; i < rp * K; i += blockDim.x) {
-      const int yl = i / K, w = i % K, y = y0 + yl;
-      C<T> acc = czero<T>();
-      for (int u = 0; u < K; ++u) {
-        const int f = corner_freq<T>(u, mf, M);
-        acc = cadd<T>(acc, cmulc<T>(s.small[u * K + w], s.twm[(f * y) & (M - 1)]));
-      }
-      V[i] = acc;
-    }
-    __syncthreads();
     const T inv = T(1) / (T(M) * T(M));
-    for (int i = tid; i < rp * M; i += blockDim.x) {
-      const int yl = i / M, x = i % M;
-      C<T> acc = czero<T>();
-      for (int w = 0; w < K; ++w) {
-        const int f = corner_freq<T>(w, mf, M);
-        acc = cadd<T>(acc, cmulc<T>(V[yl * K + w], s.twm[(f * x) & (M - 1)]));
+    C<T>* Jg = a.J + (size_t)v * img + (size_t)y0 * M;
+    if constexpr (sizeof(T) == 8) {
+      // the two contractions as complex GEMMs on the FP64 tensor cores
+      const C<T>* A_ = s.small;
+      const C<T>* tw_ = s.twm;
+      cgemm_dmma(rp, K, K,
+                 [&](int yl, int u) { return conj_<T>(tw_[(corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]); },
+                 [&](int u, int w) { return A_[u * K + w]; },
+                 [&](int yl, int w, C<T> val) { V[yl * K + w] = val; });
+      __syncthreads();
+      cgemm_dmma(rp, M, K, [&](int yl, int w) { return V[yl * K + w]; },
+                 [&](int w, int x) { return conj_<T>(tw_[(corner_freq<T>(w, mf, M) * x) & (M - 1)]); },
+                 [&](int yl, int x, C<T> val) {
+                   val = cscale<T>(val, inv);
+                   s.rows[yl * M + x] = val;
+                   Jg[yl * M + x] = val;
+                 });
+    } else {
+      for (int i = tid; i < rp * K; i += blockDim.x) {
+        const int yl = i / K, w = i % K, y = y0 + yl;
+        C<T> acc = czero<T>();
+        for (int u = 0; u < K; ++u) {
+          const int f = corner_freq<T>(u, mf, M);
+          acc = cadd<T>(acc, cmulc<T>(s.small[u * K + w], s.twm[(f * y) & (M - 1)]));
+        }
+        V[i] = acc;
       }
-      acc = cscale<T>(acc, inv);
-      s.rows[i] = acc;
-      a.J[(size_t)v * img + (size_t)(y0 + yl) * M + x] = acc;
+      __syncthreads();
+      for (int i = tid; i < rp * M; i += blockDim.x) {
+        const int yl = i / M, x = i % M;
+        C<T> acc = czero<T>();
+        for (int w = 0; w < K; ++w) {
+          const int f = corner_freq<T>(w, mf, M);
+          acc = cadd<T>(acc, cmulc<T>(V[yl * K + w], s.twm[(f * x) & (M - 1)]));
+        }
+        acc = cscale<T>(acc, inv);
+        s.rows[i] = acc;
+        Jg[i] = acc;
+      }
     }
     __syncthreads();
   } else if constexpr (MODE == VIEW_BWD) {
@@ -324,30 +345,42 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       __syncthreads();
     }
     // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)
-    C<T>* U = s.small + M0;
-    for (int i = tid; i < rp * K; i += blockDim.x) {
-      const int yl = i / K, w = i % K;
-      const int f = corner_freq<T>(w, mf, M);
-      C<T> acc = czero<T>();
-      C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
-      for (int x = 0; x < M; x += 4) {   // M is a multiple of 4: four independent chains
-        acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
-        acc1 = cadd<T>(acc1, cmul<T>(s.rows[yl * M + x + 1], s.twm[(f * (x + 1)) & (M - 1)]));
-        acc2 = cadd<T>(acc2, cmul<T>(s.rows[yl * M + x + 2], s.twm[(f * (x + 2)) & (M - 1)]));
-        acc3 = cadd<T>(acc3, cmul<T>(s.rows[yl * M + x + 3], s.twm[(f * (x + 3)) & (M - 1)]));
-      }
-      acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
-      U[i] = acc;
-    }
-    __syncthreads();
     // my partial G[u][w] = sum_yl exp(-2 pi i kr_u y / M) U[yl][w]
+    C<T>* U = s.small + M0;
     C<T>* mine = xch;
-    for (int i = tid; i < M0; i += blockDim.x) {
-      const int u = i / K, w = i % K;
-      const int f = corner_freq<T>(u, mf, M);
-      C<T> acc = czero<T>();
-      for (int yl = 0; yl < rp; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], s.twm[(f * (y0 + yl)) & (M - 1)]));
-      mine[i] = acc;
+    if constexpr (sizeof(T) == 8) {
+      const C<T>* tw_ = s.twm;
+      const C<T>* rw = s.rows;
+      cgemm_dmma(rp, K, M, [&](int yl, int x) { return rw[yl * M + x]; },
+                 [&](int x, int w) { return tw_[(corner_freq<T>(w, mf, M) * x) & (M - 1)]; },
+                 [&](int yl, int w, C<T> val) { U[yl * K + w] = val; });
+      __syncthreads();
+      cgemm_dmma(K, K, rp, [&](int u, int yl) { return tw_[(corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]; },
+                 [&](int yl, int w) { return U[yl * K + w]; },
+                 [&](int u, int w, C<T> val) { mine[u * K + w] = val; });
+    } else {
+      for (int i = tid; i < rp * K; i += blockDim.x) {
+        const int yl = i / K, w = i % K;
+        const int f = corner_freq<T>(w, mf, M);
+        C<T> acc = czero<T>();
+        C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
+        for (int x = 0; x < M; x += 4) {   // M is a multiple of 4: four independent chains
+          acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
+          acc1 = cadd<T>(acc1, cmul<T>(s.rows[yl * M + x + 1], s.twm[(f * (x + 1)) & (M - 1)]));
+          acc2 = cadd<T>(acc2, cmul<T>(s.rows[yl * M + x + 2], s.twm[(f * (x + 2)) & (M - 1)]));
+          acc3 = cadd<T>(acc3, cmul<T>(s.rows[yl * M + x + 3], s.twm[(f * (x + 3)) & (M - 1)]));
+        }
+        acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
+        U[i] = acc;
+      }
+      __syncthreads();
+      for (int i = tid; i < M0; i += blockDim.x) {
+        const int u = i / K, w = i % K;
+        const int f = corner_freq<T>(u, mf, M);
+        C<T> acc = czero<T>();
+        for (int yl = 0; yl < rp; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], s.twm[(f * (y0 + yl)) & (M - 1)]));
+        mine[i] = acc;
+      }
     }
     cluster.sync();
     const T inv = T(1) / (T(M) * T(M));

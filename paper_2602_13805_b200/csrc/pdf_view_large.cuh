@@ -24,6 +24,7 @@
 // cluster path is kept for M <= 128 where its DSMEM transposes win.
 #pragma once
 #include "pdf_common.cuh"
+#include "pdf_dmma.cuh"
 #include "pdf_pixel.cuh"
 #include "pdf_view.cuh"
 
@@ -105,7 +106,31 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   C<T> x[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) x[k] = czero<T>();
-  if constexpr (MODE == VIEW_FWD) {
+  if constexpr (MODE == VIEW_FWD && sizeof(T) == 8) {
+    // J = expand(alpha) rows y0..y0+7 (spectral.py:68-79): V = Tr A, J = V T as
+    // complex GEMMs on the FP64 tensor cores, J staged through `tile`
+    const C<T>* al = a.alpha + (size_t)v * M0;
+    for (int i = tid; i < M0; i += blockDim.x) A[i] = al[vl_corner_slot(i / K, i % K, mf)];
+    __syncthreads();
+    cgemm_dmma(VL_ROWS, K, K,
+               [&](int yl, int u) { return conj_<T>(twm[(vl_corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]); },
+               [&](int u, int w) { return A[u * K + w]; }, [&](int yl, int w, C<T> val) { V[yl * K + w] = val; });
+    __syncthreads();
+    const T inv = T(1) / (T(M) * T(M));
+    C<T>* jrows = tile;   // [VL_ROWS][M] (tile is free until after the FFT)
+    cgemm_dmma(VL_ROWS, M, K, [&](int yl, int w) { return V[yl * K + w]; },
+               [&](int w, int x) { return conj_<T>(twm[(vl_corner_freq<T>(w, mf, M) * x) & (M - 1)]); },
+               [&](int yl, int x, C<T> val) { jrows[yl * M + x] = cscale<T>(val, inv); });
+    __syncthreads();
+    C<T>* jrow = a.J + (size_t)v * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+      const int col = lane + 32 * k;
+      x[k] = jrows[warp * M + col];
+      jrow[col] = x[k];
+    }
+    __syncthreads();   // tile is rewritten by the transposed spectrum below
+  } else if constexpr (MODE == VIEW_FWD) {
     // J = expand(alpha) rows y0..y0+7 (spectral.py:68-79), separable direct sums
     const C<T>* al = a.alpha + (size_t)v * M0;
     for (int i = tid; i < M0; i += blockDim.x) A[i] = al[vl_corner_slot(i / K, i % K, mf)];
@@ -236,6 +261,17 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
     }
     __syncthreads();
     // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)   (spectral.py:56-65)
+    C<T>* gp = a.gpart + ((size_t)v * a.NPV + blockIdx.x) * M0;
+    if constexpr (sizeof(T) == 8) {
+      cgemm_dmma(VL_ROWS, K, M, [&](int yl, int xx) { return rows[yl * M + xx]; },
+                 [&](int xx, int w) { return twm[(vl_corner_freq<T>(w, mf, M) * xx) & (M - 1)]; },
+                 [&](int yl, int w, C<T> val) { U[yl * K + w] = val; });
+      __syncthreads();
+      cgemm_dmma(K, K, VL_ROWS,
+                 [&](int u, int yl) { return twm[(vl_corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]; },
+                 [&](int yl, int w) { return U[yl * K + w]; }, [&](int u, int w, C<T> val) { gp[u * K + w] = val; });
+      return;
+    }
     for (int i = tid; i < VL_ROWS * K; i += blockDim.x) {
       const int yl = i / K, w = i % K;
       const int f = vl_corner_freq<T>(w, mf, M);
@@ -249,7 +285,6 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
       U[i] = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
     }
     __syncthreads();
-    C<T>* gp = a.gpart + ((size_t)v * a.NPV + blockIdx.x) * M0;
     for (int i = tid; i < M0; i += blockDim.x) {
       const int u = i / K, w = i % K;
       const int f = vl_corner_freq<T>(u, mf, M);
@@ -425,11 +460,6 @@ __host__ __device__ inline size_t dm_smem(int n, int R, int nq) {
   return (size_t)nq * 8 * ((n + 7) / 8) * (8 * DM_NTL) * ((R + 8 * DM_NTL - 1) / (8 * DM_NTL)) * 16;
 }
 
-__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -474,10 +504,10 @@ __global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
       for (int s4 = 0; s4 < 4; ++s4)
 #pragma unroll
         for (int j = 0; j < DM_NTL; ++j) {
-          dmma_f64(dr[j][0], dr[j][1], jv[s4].x, gv[j][s4].x);
-          dmma_f64(dr[j][0], dr[j][1], -jv[s4].y, gv[j][s4].y);
-          dmma_f64(di[j][0], di[j][1], jv[s4].x, gv[j][s4].y);
-          dmma_f64(di[j][0], di[j][1], jv[s4].y, gv[j][s4].x);
+          dmma(dr[j][0], dr[j][1], jv[s4].x, gv[j][s4].x);
+          dmma(dr[j][0], dr[j][1], -jv[s4].y, gv[j][s4].y);
+          dmma(di[j][0], di[j][1], jv[s4].x, gv[j][s4].y);
+          dmma(di[j][0], di[j][1], jv[s4].y, gv[j][s4].x);
         }
     }
 #pragma unroll
