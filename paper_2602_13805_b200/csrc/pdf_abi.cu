@@ -64,6 +64,7 @@ struct pdf_ctx {
   // large-grid view path (pdf_view_large.cuh): partials per view, views per
   // spectrum chunk, data-GEMM pixel chunking
   int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks, dg_nq;
+  int split;         // pixel stage as numden / pixel_a / pixel_b (pdf_shard.cuh) in the training loop
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
@@ -71,6 +72,7 @@ struct pdf_ctx {
   void *x0, *cout, *h1, *h2, *gy, *gz2, *gz1, *ab;
   double *norms, *dloss, *part, *bd, *pix;
   void *spec, *gpart, *dpart;
+  double *red1, *red2;   // split pixel stage scratch (local reductions)
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
   double *c_inc, *c_sca;
@@ -114,6 +116,8 @@ static void plan(pdf_ctx* c, Ws& w) {
     c->spec = c->gpart = nullptr;
   }
   c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
+  c->red1 = c->split ? w.take<double>((size_t)d.S * (3 * img + 1)) : nullptr;
+  c->red2 = c->split ? w.take<double>((size_t)d.S * (2 * img + 2)) : nullptr;
   c->dloss = w.take<double>(SN);
   c->part = w.take<double>((size_t)d.S * c->ntiles * 4);
   c->bd = w.take<double>((size_t)d.S * 6);
@@ -171,6 +175,9 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   const int dg_env = env_int("PDF_DATA_GEMM", -1);
   c->dgemm = c->large || (M >= 32 && (dg_env == 1 || (dg_env < 0 && d->dtype == PDF_F64 && d->S >= 4)));
   c->dg_nq = 1;
+  // measured slower than the fused pixel kernel (with its DMMA G_S^H) on every
+  // config; kept as an option (PDF_SPLIT_PIXEL=1), covered by the sharded tests
+  c->split = env_int("PDF_SPLIT_PIXEL", 0) && !d->joint;
   if (c->dgemm) {
     const int npix = M * M;
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
@@ -654,6 +661,33 @@ static int net_forward_all(pdf_ctx* c, const void* theta, int* step, cudaStream_
 }
 
 template <typename T>
+static ShardArgs<T> shard_args(pdf_ctx* c, double* red1, double* red2);
+
+// the pixel stage split in three (numden / pixel_a / pixel_b) with local
+// reduction buffers: one thread per pixel for the view sums, no halo
+// recomputation of num/den
+template <typename T>
+static int split_pixel(pdf_ctx* c, cudaStream_t st) {
+  ShardArgs<T> a = shard_args<T>(c, c->red1, c->red2);
+  const int img = c->M * c->M;
+  void* args[] = {&a};
+  CK_CUDA(plain_launch(shard_numden_kernel<T>, dim3((img + 255) / 256, c->d.S), dim3(256), 0, st, args));
+  const dim3 grid(c->M / c->TX, c->M, c->d.S);
+  CK_CUDA(plain_launch(shard_pixel_a_kernel<T>, grid, dim3(PIX_NW * 32), 0, st, args));
+  shard_loss_sums_kernel<<<c->d.S, 128, 0, st>>>(c->part, c->dloss, c->red2, c->ntiles, c->d.n, (size_t)img);
+  CK_CUDA(cudaGetLastError());
+  CK_CUDA(plain_launch(shard_pixel_b_kernel<T>, grid, dim3(PIX_NW * 32), 0, st, args));
+  return PDF_OK;
+}
+
+static int split_finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st) {
+  FinalizeArgs f = fin_args(c, bd, trace);
+  shard_finalize_kernel<<<c->d.S, 128, 0, st>>>(f, c->red2, (size_t)c->M * c->M);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
+}
+
+template <typename T>
 static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, double* bd, double* trace, int fused,
                      cudaStream_t st, cudaEvent_t* ev = nullptr) {
   // phase order (PDF_NPHASES = 10): fwd_l1 fwd_l2 fwd_l3 view_fwd pixel view_bwd finalize bwd_l3 bwd_l2 bwd_l1
@@ -675,11 +709,15 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   mark();
   if (run()) TRY(phys_forward<T>(c, c->alpha_hat, st));
   mark();
-  if (run()) TRY((phys_pixel<T, true>(c, nullptr, st)));
+  if (run()) {
+    if (c->split) TRY(split_pixel<T>(c, st));
+    else TRY((phys_pixel<T, true>(c, nullptr, st)));
+  }
   mark();
-  if (run()) TRY(phys_backward<T>(c, nullptr, c->gy, st, bd, trace, true));
+  if (run()) TRY(phys_backward<T>(c, nullptr, c->gy, st, bd, trace, !c->split));
   mark();
-  mark();   // finalize is fused into view_bwd (phase kept for a stable layout)
+  if (run() && c->split) TRY(split_finalize(c, bd, trace, st));
+  mark();   // finalize is fused into view_bwd unless the pixel stage is split
   if (run()) TRY(net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, (T*)m, (T*)v,
                                   (T*)grad, fused, (T*)c->gz2, st));
   mark();

@@ -21,6 +21,7 @@
 // processed.  All cross-view sums are fixed-order (deterministic).
 #pragma once
 #include "pdf_common.cuh"
+#include "pdf_dmma.cuh"
 
 namespace pdf {
 
@@ -48,8 +49,8 @@ constexpr int PIX_NW = 8;          // warps per CTA
 
 template <typename T>
 __host__ __device__ inline size_t pixel_smem_bytes(int n, int R) {
-  // gs tile [R][TX] + g_rows [n][R]
-  return ((size_t)R * PIX_TX + (size_t)n * R) * sizeof(C<T>);
+  // gs tile [R][TX] + g_rows [n][R] (float32), or + G_S^H g_rows [n][TX] (float64, DMMA)
+  return ((size_t)R * PIX_TX + (size_t)n * (sizeof(T) == 8 ? PIX_TX : R)) * sizeof(C<T>);
 }
 
 template <typename T>
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   __shared__ double eps_s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C<T>* gsS = reinterpret_cast<C<T>*>(smem_raw);     // [R][TX]
-  C<T>* grS = gsS + (size_t)a.R * PIX_TX;             // [n][R]
+  C<T>* grS = gsS + (size_t)a.R * PIX_TX;             // [n][R] (float32) or G_S^H g_rows [n][TX] (float64)
 
   const int M = a.M, n = a.n, R = a.R;
   const int TX = M < PIX_TX ? M : PIX_TX;
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     cp_async_commit();
   }
   pdl_wait();   // J, E, norms, g_rows come from the previous kernel
-  if constexpr (GRAD) {
+  if constexpr (GRAD && sizeof(T) != 8) {
     constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
     const int gseg = (n * R) / EPC;
     for (int i = tid; i < gseg; i += blockDim.x)
@@ -246,6 +247,16 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     }
     cp_async_wait<0>();
     __syncthreads();
+    if constexpr (sizeof(T) == 8) {
+      // G_S^H g_rows for the tile (forward.py:303-306) as a complex GEMM on
+      // the FP64 tensor cores: [n views] x [R] x [TX pixels]
+      const C<T>* gsT = gsS;
+      const C<T>* grG = a.grows + vbase * R;
+      cgemm_dmma(n, TX, R, [&](int v, int r) { return grG[(size_t)v * R + r]; },
+                 [&](int r, int xl) { return conj_<T>(gsT[r * PIX_TX + xl]); },
+                 [&](int v, int xl, C<T> val) { grS[v * PIX_TX + xl] = val; });
+      __syncthreads();
+    }
     if (lane < TX) {
       const size_t pix = (size_t)y * M + x0 + lane;
       const C<T> R_ = Rs[lane];
@@ -261,15 +272,19 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
         const C<T> gP = cmul<T>(conj_<T>(R_), gS);
         C<T> gj = cscale<T>(csub<T>(gP, gS), beta);
         // G_S^H g_rows at this pixel (forward.py:303-306), shared-memory operands
-        const C<T>* gr = grS + (size_t)i * R;
-        C<T> acc0 = czero<T>(), acc1 = czero<T>();
-        int r = 0;
-        for (; r + 1 < R; r += 2) {
-          acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
-          acc1 = cadd<T>(acc1, cmulc<T>(gr[r + 1], gsS[(r + 1) * PIX_TX + lane]));
+        if constexpr (sizeof(T) == 8) {
+          gj = cadd<T>(gj, grS[i * PIX_TX + lane]);
+        } else {
+          const C<T>* gr = grS + (size_t)i * R;
+          C<T> acc0 = czero<T>(), acc1 = czero<T>();
+          int r = 0;
+          for (; r + 1 < R; r += 2) {
+            acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
+            acc1 = cadd<T>(acc1, cmulc<T>(gr[r + 1], gsS[(r + 1) * PIX_TX + lane]));
+          }
+          if (r < R) acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
+          gj = cadd<T>(gj, cadd<T>(acc0, acc1));
         }
-        if (r < R) acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
-        gj = cadd<T>(gj, cadd<T>(acc0, acc1));
         gj = cadd<T>(gj, cmul<T>(e, gn));
         C<T> ge = cadd<T>(gP, cmul<T>(conj_<T>(gn), j));
         ge = cadd<T>(ge, cscale<T>(e, T(2) * gd));
