@@ -351,6 +351,26 @@ def _theta0(seeds, m0_eff: int, workers: int = 8) -> np.ndarray:
         return np.stack(list(ex.map(one, seeds)))
 
 
+_THETA_POOL = None
+
+
+def _flat_size(m0_eff: int) -> int:
+    d0 = 2 * m0_eff
+    h = 2 * d0
+    return h * d0 + h + h * h + h + d0 * h + d0
+
+
+def _theta0_async(seeds, m0_eff: int, out: np.ndarray, workers: int = 8):
+    """Start the per-scene draws of _theta0 into `out` rows; returns futures."""
+    global _THETA_POOL
+    if _THETA_POOL is None:
+        _THETA_POOL = ThreadPoolExecutor(max_workers=workers)
+
+    def one(i, s):
+        out[i] = flatten_params(init_network(m0_eff, np.random.default_rng(int(s))))
+    return [_THETA_POOL.submit(one, i, s) for i, s in enumerate(seeds)]
+
+
 class BatchReconstructor:
     """Reconstruct S scenes that share one geometry, all resident on one GPU.
 
@@ -394,16 +414,24 @@ class BatchReconstructor:
         seeds = [cfg.rng_seed] * self.S if seeds is None else list(seeds)
         k = cfg.k_iters if k_iters is None else k_iters
         dev = self.dev
-        dev.set_data(mats)
-        chi0, r0 = dev.bp_initialize()
         if cfg.freeze_r:
             raise NotImplementedError("freeze_r with BatchReconstructor: build DeviceProblem(r_fixed=...)")
-        alpha0 = dev.init_alpha(r0)
-        dev.net_setup(alpha0)
         key = tuple(int(x) for x in seeds)
         theta0 = self._theta0.get(key)
+        pending = None
         if theta0 is None:
-            theta0 = torch.as_tensor(_theta0(seeds, self.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
+            # the reference-identical initial weights are host RNG draws: fill a
+            # pinned buffer on worker threads while the GPU runs the initialisation
+            host = torch.empty((self.S, _flat_size(self.m0_eff)), dtype=torch.float64, pin_memory=True)
+            pending = _theta0_async(seeds, self.m0_eff, host.numpy())
+        dev.set_data(mats)
+        chi0, r0 = dev.bp_initialize()
+        alpha0 = dev.init_alpha(r0)
+        dev.net_setup(alpha0)
+        if pending is not None:
+            for f in pending:
+                f.result()
+            theta0 = host.to(device=dev.device, dtype=dev.rdt, non_blocking=True).contiguous()
             if self.theta_cache:
                 self._theta0 = {key: theta0}
         theta = theta0.clone()
