@@ -147,7 +147,7 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // fills the GPU (half the cluster barriers per unit of work; measured -22%
   // view time at 128 scenes)
   c->CS = env_int("PDF_VIEW_CLUSTER", (long long)d->S * d->n * 8 <= 4 * 148 ? 8 : 4);
-  if (c->CS < 1 || c->CS > 16 || (M % c->CS) || ((2 * M) % c->CS)) return fail(PDF_EINVAL, "view cluster size");
+  if (c->CS != 4 && c->CS != 8) return fail(PDF_EINVAL, "view cluster size must be 4 or 8");
   c->rows = d->joint ? 1 : d->n;
   c->D0 = 2 * c->M0 * (d->joint ? d->n : 1);
   c->H = 2 * c->D0;
@@ -260,17 +260,17 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
   static const int vt = env_int("PDF_VIEW_THREADS", 256);
   const int nthr = std::min(vt, 256);
   dim3 grid(c->CS, count), block(nthr), cl(c->CS, 1, 1);
-  switch (c->E) {
-#define VCASE(EE)                                                   \
-  case EE: {                                                        \
-    auto k = view_kernel<T, EE, MODE>;                              \
+  switch (c->E * 100 + c->CS) {
+#define VCASE(EE, CC)                                               \
+  case EE * 100 + CC: {                                             \
+    auto k = view_kernel<T, EE, MODE, CC>;                          \
     e = prep(k, smem);                                              \
     if (e == cudaSuccess) e = launch_cluster(k, grid, block, smem, st, cl, args); \
     break;                                                          \
   }
-    VCASE(1) VCASE(2) VCASE(4) VCASE(8)
+    VCASE(1, 4) VCASE(1, 8) VCASE(2, 4) VCASE(2, 8) VCASE(4, 4) VCASE(4, 8) VCASE(8, 4) VCASE(8, 8)
 #undef VCASE
-    default: return fail(PDF_EINVAL, "unsupported FFT size");
+    default: return fail(PDF_EINVAL, "unsupported FFT size / view cluster size (4 or 8)");
   }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("view kernel: ") + cudaGetErrorString(e));
   return PDF_OK;

@@ -104,15 +104,16 @@ __device__ inline double block_sum_d(double v, double* red) {
   return s;
 }
 
-template <typename T, int E, int MODE>
+template <typename T, int E, int MODE, int CSZ>
 __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int P = 32 * E;
   cg::cluster_group cluster = cg::this_cluster();
-  const int CS = a.CS;
+  constexpr int CS = CSZ;   // cluster size: compile-time so the row / column owner maps are shifts
   const int rank = (int)cluster.block_rank();
-  const int M = a.M, mf = a.mf, K = 2 * mf, M0 = K * K;
-  const int rp = M / CS, cp = P / CS;
+  constexpr int M = P / 2;
+  const int mf = a.mf, K = 2 * mf, M0 = K * K;
+  constexpr int rp = M / CS, cp = P / CS;
   const int y0 = rank * rp;
   const int v = blockIdx.y;                 // global view index (scene*n + view)
   const int scene = v / a.n, view = v % a.n;
