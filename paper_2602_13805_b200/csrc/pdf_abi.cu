@@ -755,7 +755,8 @@ static int create_impl(pdf_ctx* c, void* ws, size_t bytes, cudaStream_t st) {
   CK_CUDA(cudaMemsetAsync(c->err, 0, c->d.S * sizeof(int), st));
   CK_CUDA(cudaMemsetAsync(c->step, 0, 2 * sizeof(int), st));
   const int PP = c->P * c->P;
-  permute_khat_kernel<T><<<(PP + 255) / 256, 256, 0, st>>>((const C<T>*)c->d.gd_kernel_hat, (C<T>*)c->khat, c->P);
+  permute_khat_kernel<T><<<(PP + 255) / 256, 256, 0, st>>>((const C<T>*)c->d.gd_kernel_hat, (C<T>*)c->khat, c->P,
+                                                            c->large && c->E >= 4 ? 1 : 0);
   CK_CUDA(cudaGetLastError());
   CK_CUDA(cudaStreamSynchronize(st));
   return PDF_OK;

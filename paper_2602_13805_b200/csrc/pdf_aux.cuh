@@ -9,15 +9,22 @@ namespace pdf {
 
 __device__ inline int bitrev5(int l) { return __brev((unsigned)l) >> 27; }
 
-// khat_p[pos_c * P + pos_r] = khat[f(pos_r)][f(pos_c)] / P^2, f(q*32+l) = spectrum_slot_freq(l, q, E)
-template <typename T>
-__global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P) {
+// khat_p[pos_c * P + pos_r] = khat[f(pos_r)][f(pos_c)] / P^2, f(q*32+l) = spectrum_slot_freq(l, q, E);
+// split (large-grid path): pos = h * P/2 + q*32 + l holds frequency 2 f_{E/2}(q*32+l) + h
+__device__ inline int khat_pos_freq(int pos, int P, int split) {
   const int E = P / 32;
+  if (!split) return spectrum_slot_freq(pos % 32, pos / 32, E);
+  const int h = pos / (P / 2), r = pos % (P / 2);
+  return 2 * spectrum_slot_freq(r % 32, r / 32, E / 2) + h;
+}
+
+template <typename T>
+__global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P, int split) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= P * P) return;
   const int posc = idx / P, posr = idx % P;
-  const int fr = spectrum_slot_freq(posr % 32, posr / 32, E);
-  const int fc = spectrum_slot_freq(posc % 32, posc / 32, E);
+  const int fr = khat_pos_freq(posr, P, split);
+  const int fc = khat_pos_freq(posc, P, split);
   const T s = T(1) / (T(P) * T(P));
   out[idx] = cscale<T>(khat[(size_t)fr * P + fc], s);
 }

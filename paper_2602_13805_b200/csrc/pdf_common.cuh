@@ -203,9 +203,9 @@ template <typename T> __device__ __forceinline__ C<T> tw_get(const C<T>* tw, int
 //   rq[q]  = tw[(lane * q) mod P]         for the register-to-lane twiddle
 template <typename T, int E>
 struct LaneTw {
-  // E = 16 (P = 512) keeps the register-to-lane twiddles in the shared table:
-  // 16 more complex registers per thread would spill next to x[16]
-  static constexpr bool RQREG = E <= 8;
+  // E >= 8 keeps the register-to-lane twiddles in the shared table (register
+  // pressure of the large-grid passes; M = 128 is not a BASELINE config)
+  static constexpr bool RQREG = E <= 4;
   C<T> st[5];
   C<T> rq[RQREG ? E : 1];
   const C<T>* tw;

@@ -72,14 +72,14 @@ __device__ __forceinline__ int vl_corner_slot(int u, int v, int mf) {
 template <typename T>
 __host__ __device__ inline size_t vl_rows_smem(int E, int mf) {
   const int P = 32 * E, M = P / 2, K = 2 * mf;
-  return ((size_t)P + M + (size_t)P * (VL_ROWS + 1) + (size_t)K * K + (size_t)VL_ROWS * K) * sizeof(C<T>);
+  return ((size_t)P + P / 2 + M + (size_t)P * (VL_ROWS + 1) + (size_t)K * K + (size_t)VL_ROWS * K) * sizeof(C<T>);
 }
 
 template <typename T>
 __host__ __device__ inline size_t vl_out_smem(int E, int mf) {
   const int P = 32 * E, M = P / 2, K = 2 * mf;
   (void)M;
-  return ((size_t)P + M + (size_t)VL_ROWS * (P + 1) + (size_t)VL_ROWS * K) * sizeof(C<T>) + 16 * sizeof(double);
+  return ((size_t)P + P / 2 + M + (size_t)VL_ROWS * (P + 1) + (size_t)VL_ROWS * K) * sizeof(C<T>) + 16 * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------
@@ -88,8 +88,11 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   constexpr int P = 32 * E, M = P / 2, KH = E / 2, TP = VL_ROWS + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mf = a.mf, K = 2 * mf, M0 = K * K;
+  constexpr bool SPLIT = E >= 4;
+  constexpr int EH = E / 2;
   C<T>* tw = reinterpret_cast<C<T>*>(smem_raw);
-  C<T>* twm = tw + P;
+  C<T>* twh = tw + P;                   // exp(-2 pi i k / (P/2)), the half-length FFT table
+  C<T>* twm = twh + P / 2;
   C<T>* tile = twm + M;                 // [P][TP]
   C<T>* A = tile + P * TP;              // [K][K]
   C<T>* V = A + M0;                     // [VL_ROWS][K]
@@ -97,10 +100,12 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   const int vr = blockIdx.y, v = a.v0 + vr, y0 = blockIdx.x * VL_ROWS, y = y0 + warp;
   const size_t img = (size_t)M * M;
   for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  for (int i = tid; i < P / 2; i += blockDim.x) twh[i] = a.twP[2 * i];
   for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
   __syncthreads();
   LaneTw<T, E> ltw;
-  ltw.load(tw, lane);
+  LaneTw<T, (SPLIT ? E / 2 : 1)> ltwh;
+  if constexpr (SPLIT) ltwh.load(twh, lane); else ltw.load(tw, lane);
   pdl_wait();
 
   C<T> x[E];
@@ -169,9 +174,24 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
       x[k] = a.conj_in ? conj_<T>(t) : t;
     }
   }
-  warp_fft_fwd<T, E>(x, ltw, lane);
+  if constexpr (SPLIT) {
+    // zero padding: X[2m] = F_{P/2}(x)[m], X[2m+1] = F_{P/2}(x w^n)[m], w = exp(-2 pi i / P)
+    C<T> t[EH];
 #pragma unroll
-  for (int q = 0; q < E; ++q) tile[(q * 32 + lane) * TP + warp] = x[q];
+    for (int k = 0; k < EH; ++k) t[k] = x[k];
+    warp_fft_fwd<T, EH>(t, ltwh, lane);
+#pragma unroll
+    for (int q = 0; q < EH; ++q) tile[(q * 32 + lane) * TP + warp] = t[q];
+#pragma unroll
+    for (int k = 0; k < EH; ++k) t[k] = cmul<T>(x[k], tw[lane + 32 * k]);
+    warp_fft_fwd<T, EH>(t, ltwh, lane);
+#pragma unroll
+    for (int q = 0; q < EH; ++q) tile[(P / 2 + q * 32 + lane) * TP + warp] = t[q];
+  } else {
+    warp_fft_fwd<T, E>(x, ltw, lane);
+#pragma unroll
+    for (int q = 0; q < E; ++q) tile[(q * 32 + lane) * TP + warp] = x[q];
+  }
   __syncthreads();
   pdl_trigger();
   C<T>* out = a.spec + (size_t)vr * P * M + y0;
@@ -183,16 +203,48 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
 
 // ---------------------------------------------------------------------------
 template <typename T, int E>
-__global__ void __launch_bounds__(256) vl_cols_kernel(VLArgs<T> a) {
+__global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T> a) {
   constexpr int P = 32 * E, M = P / 2, KH = E / 2;
+  constexpr bool SPLIT = E >= 4;
+  constexpr int EH = E / 2;
   __shared__ C<T> tw[P];
+  __shared__ C<T> twh[P / 2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  for (int i = tid; i < P / 2; i += blockDim.x) twh[i] = a.twP[2 * i];
   __syncthreads();
-  LaneTw<T, E> ltw;
-  ltw.load(tw, lane);
   const int pos = blockIdx.x * (blockDim.x >> 5) + warp;
   const C<T>* kh = a.khat + (size_t)pos * P;
+  if constexpr (SPLIT) {
+    // y[n] = F^-1(K_e F(x))[n] + w^-n F^-1(K_o F(x w^n))[n] for the first P/2 outputs
+    LaneTw<T, E / 2> lt;
+    lt.load(twh, lane);
+    pdl_wait();
+    C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
+    C<T> xin[EH], r[EH], t[EH];
+#pragma unroll
+    for (int k = 0; k < EH; ++k) xin[k] = col[lane + 32 * k];
+#pragma unroll
+    for (int k = 0; k < EH; ++k) t[k] = xin[k];
+    warp_fft_fwd<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[q * 32 + lane]);
+    warp_fft_inv<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int k = 0; k < EH; ++k) r[k] = t[k];
+#pragma unroll
+    for (int k = 0; k < EH; ++k) t[k] = cmul<T>(xin[k], tw[lane + 32 * k]);
+    warp_fft_fwd<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[P / 2 + q * 32 + lane]);
+    warp_fft_inv<T, EH>(t, lt, lane);
+    pdl_trigger();
+#pragma unroll
+    for (int k = 0; k < EH; ++k) col[lane + 32 * k] = cadd<T>(r[k], cmulc<T>(t[k], tw[lane + 32 * k]));
+    return;
+  }
+  LaneTw<T, E> ltw;
+  ltw.load(tw, lane);
   pdl_wait();
   C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
   C<T> x[E];
@@ -213,8 +265,11 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   constexpr int P = 32 * E, M = P / 2, KH = E / 2, SP = P + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mf = a.mf, K = 2 * mf, M0 = K * K;
+  constexpr bool SPLIT = E >= 4;
+  constexpr int EH = E / 2;
   C<T>* tw = reinterpret_cast<C<T>*>(smem_raw);
-  C<T>* twm = tw + P;
+  C<T>* twh = tw + P;
+  C<T>* twm = twh + P / 2;
   C<T>* S = twm + M;                     // [VL_ROWS][SP]; reused as rows [VL_ROWS][M] (BWD)
   C<T>* U = S + VL_ROWS * SP;            // [VL_ROWS][K]
   double* red = reinterpret_cast<double*>(U + VL_ROWS * K);
@@ -223,6 +278,7 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   const int scene = v / a.n, view = v % a.n;
   const size_t img = (size_t)M * M;
   for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
+  for (int i = tid; i < P / 2; i += blockDim.x) twh[i] = a.twP[2 * i];
   for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
   pdl_wait();
   const C<T>* in = a.spec + (size_t)vr * P * M + y0;
@@ -231,12 +287,28 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
     S[yl * SP + pos] = in[(size_t)pos * M + yl];
   }
   __syncthreads();
-  LaneTw<T, E> ltw;
-  ltw.load(tw, lane);
   C<T> x[E];
+  if constexpr (SPLIT) {
+    LaneTw<T, E / 2> lt;
+    lt.load(twh, lane);
+    C<T> t[EH];
 #pragma unroll
-  for (int q = 0; q < E; ++q) x[q] = S[warp * SP + q * 32 + lane];
-  warp_fft_inv<T, E>(x, ltw, lane);
+    for (int q = 0; q < EH; ++q) t[q] = S[warp * SP + q * 32 + lane];
+    warp_fft_inv<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int k = 0; k < EH; ++k) x[k] = t[k];
+#pragma unroll
+    for (int q = 0; q < EH; ++q) t[q] = S[warp * SP + P / 2 + q * 32 + lane];
+    warp_fft_inv<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int k = 0; k < EH; ++k) x[k] = cadd<T>(x[k], cmulc<T>(t[k], tw[lane + 32 * k]));
+  } else {
+    LaneTw<T, E> ltw;
+    ltw.load(tw, lane);
+#pragma unroll
+    for (int q = 0; q < E; ++q) x[q] = S[warp * SP + q * 32 + lane];
+    warp_fft_inv<T, E>(x, ltw, lane);
+  }
   pdl_trigger();
   const size_t rowoff = (size_t)v * img + (size_t)y * M;
   if constexpr (MODE == VIEW_FWD) {
