@@ -267,6 +267,12 @@ def large_leg(args, d: Dist):
         th.copy_(theta0); m.zero_(); v.zero_()
         out.update({"mode": "single GPU, CUDA graph", "phases_ms": dev.profile_phases(th, m, v, 0, 5),
                     "final_loss_total": float(tr[-1, 0, 5])})
+        peaks = json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(HERE, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+        pr = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), 36.2, peaks["hbm_gbs"])
+        pr["frac"] = pr["t_roof_us_per_scene_iter"] * k / (1e6 * secs)
+        pr["fp64_peak_note"] = "36.2 TFLOP/s (pdf_fp64_probe on this pool)"
+        out["path_roofline"] = pr
         del dev
     else:
         c = cfg
@@ -326,6 +332,20 @@ def ncu_traffic(phase: str):
                 "source": os.path.relpath(files[-1], HERE)} if per else None
     except Exception:
         return None
+
+
+def path_roofline(M: int, n: int, R: int, np_params: int, fp64_tflops: float, hbm_gbs: float) -> dict:
+    """SURVEY 8(d) path roofline per scene-iteration, restated for float64:
+    F_phys = n [20 P^2 log2 P^2 + 12 P^2 + 10 M^2 log2 M^2 + 16 M^2 R] flop at the
+    FP64 peak, B_net = 56 Np bytes (W read forward, W/m/v read + written by the
+    fused backward/Adam) at the HBM peak."""
+    P = 2 * M
+    f = n * (20 * P * P * np.log2(P * P) + 12 * P * P + 10 * M * M * np.log2(M * M) + 16 * M * M * R)
+    b = 56.0 * np_params
+    t_phys = f / (fp64_tflops * 1e12)
+    t_net = b / (hbm_gbs * 1e9)
+    return {"F_phys_flop": float(f), "B_net_bytes": b, "t_phys_us": 1e6 * t_phys, "t_net_us": 1e6 * t_net,
+            "t_roof_us_per_scene_iter": 1e6 * (t_phys + t_net)}
 
 
 def run_ours(args, d: Dist):
@@ -409,6 +429,8 @@ def run_ours(args, d: Dist):
         achieved = work / launch_s / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak_tflops, "peak_source": "pdf_fp64_probe DFMA kernel (measured live)"}
+    proof = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), fp64_peak_tflops, peaks["hbm_gbs"])
+    proof["frac"] = proof["t_roof_us_per_scene_iter"] / (1e3 * ms_step / k)
     roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom],
                  "traffic": ncu_traffic(dom), "share_of_step": share[dom]})
 
@@ -462,11 +484,13 @@ def run_ours(args, d: Dist):
         phb = devb.profile_phases(thb, mb, vb, 0, 3)
         devb.check_errors()
         rels = [o.rel_error for o in outb]
+        proof_b = path_roofline(devb.M, devb.n, devb.R, int(devb.n_params), fp64_peak_tflops, peaks["hbm_gbs"])
+        proof_b["frac"] = proof_b["t_roof_us_per_scene_iter"] * S * k / (1e6 * tdev)
         batched = {"workload": f"cfg4: {S * d.world} scenes of 1-4 random ellipses (seed = scene index), "
                                f"{S} per GPU, {k} iterations each",
                    "scenes_per_s": d.world * S / tdev, "iter_per_s": d.world * S * k / tdev,
                    "e2e_scenes_per_s": d.world * S / tb, "s_per_batch": tdev, "e2e_s_per_batch": tb,
-                   "median_rel_error": float(np.median(rels)), "phases_ms": phb,
+                   "median_rel_error": float(np.median(rels)), "phases_ms": phb, "path_roofline": proof_b,
                    "scaling": "strong (256 scenes split over the GPUs)"}
 
     large = None
@@ -492,7 +516,7 @@ def run_ours(args, d: Dist):
                     "d2h_bytes_per_step": int(d2h), "s_per_reconstruction": e2e_s,
                     "api": "BatchReconstructor.run(host data) -> ReconstructionResult",
                     "rel_error": res[0].rel_error},
-            "roofline": roof, "phases_ms": phases, "fp64_peak_tflops_measured": fp64_peak_tflops,
+            "roofline": roof, "path_roofline": proof, "phases_ms": phases, "fp64_peak_tflops_measured": fp64_peak_tflops,
             "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": args.steps * (1 + launches_per_iter * k), "batched": batched, "large": large}
     if d.rank == 0:
