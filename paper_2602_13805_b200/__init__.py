@@ -19,7 +19,7 @@ _API = ("LossBreakdown", "LossContext", "PipelineState", "SpectralBasis", "Netwo
         "ReconstructionResult", "BatchReconstructor", "pipeline_forward", "pipeline_backward", "grad_alpha",
         "loss_total", "init_network", "forward_net", "flatten_params", "unflatten_params", "grad_loss",
         "adam_step", "bp_initialize", "init_alpha", "recover_contrast", "apply_cco", "reconstruct",
-        "relative_error", "count_components", "PoleError", "ZeroDataError")
+        "relative_error", "count_components", "PoleError", "ZeroDataError", "PhysicsLoss")
 
 
 def __getattr__(name):

@@ -174,6 +174,32 @@ def loss_total(alpha: np.ndarray, ctx: LossContext) -> LossBreakdown:
 
 # ---------------------------------------------------------------------------- network
 @dataclass
+class PhysicsLoss(torch.autograd.Function):
+    """The PDF physics loss as a differentiable torch op: the
+    per-scene total of losses.py:215-247 for spectral coefficients alpha_hat
+    (S, n, M0) complex on a DeviceProblem, with the hand adjoint of
+    losses.py:267-306 as its backward.  The fused kernel computes loss and
+    gradient in one pass, so the gradient is produced eagerly in forward and
+    scaled by the incoming gradient in backward.  torch's complex gradient
+    convention (dL/dRe + i dL/dIm) is the reference's (losses.py:255-264).
+
+        loss = PhysicsLoss.apply(alpha_hat, dev)   # (S,) float64
+        loss.sum().backward()                       # -> alpha_hat.grad
+    """
+
+    @staticmethod
+    def forward(ctx, alpha_hat, dev):
+        g, bd = dev.loss_grad(alpha_hat.detach())
+        dev.check_errors()
+        ctx.save_for_backward(g.clone())
+        return bd[:, 5].clone()
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        (g,) = ctx.saved_tensors
+        return g * grad_out.to(g.real.dtype)[:, None, None], None
+
+
 class NetworkParams:
     weights: list
     biases: list

@@ -224,3 +224,30 @@ def test_nonfinite_loss_terms_named(tiny_setup, g_tiny):
     dev.loss_grad(_t(alpha[None], dev))
     with pytest.raises(FloatingPointError, match="nonfinite loss term"):
         dev.check_errors()
+
+
+def test_physics_loss_autograd_function():
+    """PhysicsLoss: torch autograd through the fused physics reproduces the
+    reference gradient, and chains into torch-side parameters (finite difference)."""
+    from paper_2602_13805_b200.api import PhysicsLoss
+    from paper_2602_13805_b200.engine import DeviceProblem
+    from conftest import Setup, cfg_baseline
+    g = golden("cfg2")
+    st = Setup(cfg_baseline(2), plane=True)
+    c = st.cfg
+    dev = DeviceProblem(st.ops, st.e_inc, g["data"], mf=c.m_f, beta=c.beta, lambdas=(1e-3, 1e-5, 1e-5),
+                        tau_b=c.tau_b)
+    a = torch.as_tensor(g["alpha0"][None], device="cuda").clone().requires_grad_(True)
+    loss = PhysicsLoss.apply(a, dev)
+    loss.sum().backward()
+    assert rel(a.grad[0].cpu().numpy(), g["g_alpha0"]) < 1e-10
+    assert abs(loss.item() - float(g["bd0"][5])) < 1e-10 * abs(float(g["bd0"][5]))
+    # chain rule into a torch-side real scale s: alpha_hat = alpha0 * (1 + s)
+    a0 = torch.as_tensor(g["alpha0"][None], device="cuda")
+    s = torch.zeros(1, dtype=torch.float64, device="cuda", requires_grad=True)
+    PhysicsLoss.apply(a0 * (1 + s), dev).sum().backward()
+    h = 1e-6
+    lp = dev.loss_value(a0 * (1 + h))[0][0, 5].item()
+    lm = dev.loss_value(a0 * (1 - h))[0][0, 5].item()
+    fd = (lp - lm) / (2 * h)
+    assert abs(s.grad.item() - fd) < 1e-6 * max(1.0, abs(fd)), (s.grad.item(), fd)
