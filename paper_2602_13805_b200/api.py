@@ -173,7 +173,6 @@ def loss_total(alpha: np.ndarray, ctx: LossContext) -> LossBreakdown:
 
 
 # ---------------------------------------------------------------------------- network
-@dataclass
 class PhysicsLoss(torch.autograd.Function):
     """The PDF physics loss as a differentiable torch op: the
     per-scene total of losses.py:215-247 for spectral coefficients alpha_hat
@@ -200,6 +199,7 @@ class PhysicsLoss(torch.autograd.Function):
         return g * grad_out.to(g.real.dtype)[:, None, None], None
 
 
+@dataclass
 class NetworkParams:
     weights: list
     biases: list
