@@ -68,7 +68,7 @@ struct pdf_ctx {
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
-  void *khat, *twP, *twM, *J, *E_, *gJ, *gE, *grows, *alpha0, *alpha_hat, *galpha;
+  void *khat, *twP, *twM, *hs, *J, *E_, *gJ, *gE, *grows, *alpha0, *alpha_hat, *galpha;
   void *x0, *cout, *h1, *h2, *gy, *gz2, *gz1, *ab;
   double *norms, *dloss, *part, *bd, *pix;
   void *spec, *gpart, *dpart;
@@ -91,6 +91,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->khat = w.take<C<T>>((size_t)c->P * c->P);
   c->twP = w.take<C<T>>(c->P);
   c->twM = w.take<C<T>>(c->M);
+  c->hs = w.take<C<T>>((size_t)d.R * c->M0);   // spectral receiver operator (pdf_aux.cuh)
   c->J = w.take<C<T>>(SN * img);
   c->E_ = w.take<C<T>>(SN * img);
   c->gJ = w.take<C<T>>(SN * img);
@@ -179,9 +180,9 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // config; kept as an option (PDF_SPLIT_PIXEL=1), covered by the sharded tests
   c->split = env_int("PDF_SPLIT_PIXEL", 0) && !d->joint;
   if (c->dgemm) {
-    const int npix = M * M;
+    const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
-    want = std::min(want, npix / DG_KC);
+    want = std::max(1, std::min(want, npix / DG_KC));
     c->dg_chunk = ((npix + want - 1) / want + DG_KC - 1) / DG_KC * DG_KC;
     c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
     const int ntp = ((d->n + 7) / 8) * ((d->R + 8 * DM_NTL - 1) / (8 * DM_NTL));
@@ -281,6 +282,7 @@ static ViewArgs<T> view_common(pdf_ctx* c) {
   ViewArgs<T> a = {};
   a.M = c->M; a.mf = c->d.mf; a.R = c->d.R; a.n = c->d.n; a.CS = c->CS;
   a.khat = (const C<T>*)c->khat; a.twP = (const C<T>*)c->twP; a.twM = (const C<T>*)c->twM;
+  a.hs = (const C<T>*)c->hs;
   return a;
 }
 
@@ -326,11 +328,14 @@ static int vl_conv(pdf_ctx* c, VLArgs<T>& a, int count, cudaStream_t st) {
   return PDF_OK;
 }
 
+// D = alpha_hat H^T - d over all views of a scene: the split-K GEMM runs over
+// the M0 spectral coefficients (H = G_S o expand, pdf_aux.cuh), not the M^2
+// pixels of J G_S^T
 template <typename T>
-static int data_term(pdf_ctx* c, cudaStream_t st) {
+static int data_term(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   DataArgs<T> g = {};
-  g.n = c->d.n; g.R = c->d.R; g.npix = c->M * c->M; g.chunk = c->dg_chunk; g.nchunks = c->dg_nchunks;
-  g.J = (const C<T>*)c->J; g.gs = (const C<T>*)c->d.gs_matrix; g.dpart = (C<T>*)c->dpart;
+  g.n = c->d.n; g.R = c->d.R; g.npix = c->M0; g.chunk = c->dg_chunk; g.nchunks = c->dg_nchunks;
+  g.J = (const C<T>*)alpha_hat; g.gs = (const C<T>*)c->hs; g.dpart = (C<T>*)c->dpart;
   g.data = (const C<T>*)c->d.data; g.mask = (const T*)c->d.mask; g.c_sca = c->c_sca;
   g.grows = (C<T>*)c->grows; g.dloss = c->dloss;
   g.nq = c->dg_nq;
@@ -353,7 +358,7 @@ static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
   a.E = (C<T>*)c->E_; a.norms = c->norms;
   TRY((vl_conv<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
-  return data_term<T>(c, st);
+  return data_term<T>(c, alpha_hat, st);
 }
 
 template <typename T>
@@ -362,6 +367,7 @@ static int vl_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, cons
   a.gE = (const C<T>*)c->gE; a.gJloc = (const C<T>*)c->gJ; a.gpart = (C<T>*)c->gpart;
   TRY((vl_conv<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st)));
   a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
+  a.grows = (const C<T>*)c->grows; a.hs = (const C<T>*)c->hs;
   a.fin = fin; a.do_fin = do_fin ? 1 : 0;
   void* args[] = {&a};
   cudaError_t e = plain_launch(vl_trunc_reduce_kernel<T>, dim3((c->M0 + 255) / 256, c->d.S * c->d.n), dim3(256), 0,
@@ -376,11 +382,11 @@ static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   ViewArgs<T> a = view_common<T>(c);
   a.alpha = (const C<T>*)alpha_hat;
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
-  a.gs = (const C<T>*)c->d.gs_matrix; a.data = (const C<T>*)c->d.data; a.mask = (const T*)c->d.mask;
+  a.data = (const C<T>*)c->d.data; a.mask = (const T*)c->d.mask;
   a.c_sca = c->c_sca; a.J = (C<T>*)c->J; a.E = (C<T>*)c->E_; a.norms = c->norms;
   a.grows = (C<T>*)c->grows; a.dloss = c->dloss; a.do_data = !c->dgemm;
   TRY((launch_view<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
-  return c->dgemm ? data_term<T>(c, st) : PDF_OK;
+  return c->dgemm ? data_term<T>(c, alpha_hat, st) : PDF_OK;
 }
 
 template <typename T, bool GRAD>
@@ -389,12 +395,12 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   p.M = c->M; p.n = c->d.n; p.R = c->d.R; p.CS = c->NPV; p.S = c->d.S;
   p.beta = (T)c->d.beta; p.l1 = (T)c->d.lambda1; p.l2 = (T)c->d.lambda2; p.l3 = (T)c->d.lambda3;
   p.tau = (T)c->d.tau_b;
-  p.J = (const C<T>*)c->J; p.E = (const C<T>*)c->E_; p.norms = c->norms; p.grows = (const C<T>*)c->grows;
-  p.gs = (const C<T>*)c->d.gs_matrix; p.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
+  p.J = (const C<T>*)c->J; p.E = (const C<T>*)c->E_; p.norms = c->norms;
+  p.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
   p.c_inc = c->c_inc; p.gJ = (C<T>*)c->gJ; p.gE = (C<T>*)c->gE; p.part = c->part;
   p.chi_out = (C<T>*)chi_out; p.err = c->err;
   dim3 grid(c->M / c->TX, c->M, c->d.S);
-  const size_t smem = GRAD ? pixel_smem_bytes<T>(c->d.n, c->d.R) : 0;
+  const size_t smem = 0;
   constexpr int epc = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
   if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
   void* args[] = {&p};
@@ -422,6 +428,7 @@ static int phys_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, do
   a.do_fin = fin ? 1 : 0;
   a.gE = (const C<T>*)c->gE; a.gJloc = (const C<T>*)c->gJ;
   a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
+  a.grows = (C<T>*)c->grows;
   return launch_view<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st);
 }
 
@@ -462,6 +469,18 @@ static cudaError_t fwd_mma_nt(int NT, dim3 grid, int CK, NetFwdArgs<double>& a, 
 
 static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
   const int MT = (c->rows + 7) / 8, S = c->d.S, N = a.N, K = a.K;
+  // latency regime (few scenes, <= 16 rows, K <= 1024): one n-tile per CTA,
+  // the input block resident in shared memory, one memory round trip
+  static const int xk = env_int("PDF_FWD_X", 1);
+  if (xk && MT <= 2 && K <= XW * XKB * 16 && (long long)S * ((N + 7) / 8) <= 4 * 148) {
+    const dim3 grid((N + 7) / 8, 1, S);
+    const size_t smem = fwd_x_smem_bytes(MT, K);
+    void* args[] = {&a};
+    cudaError_t e = MT == 1 ? plain_launch(net_fwd_x_kernel<1>, grid, dim3(XW * 32), smem, st, args)
+                            : plain_launch(net_fwd_x_kernel<2>, grid, dim3(XW * 32), smem, st, args);
+    if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net fwd (x): ") + cudaGetErrorString(e));
+    return PDF_OK;
+  }
   auto ctas = [&](int nt) { return (long long)((N + 64 * nt - 1) / (64 * nt)) * S; };
   // one n-tile per warp measured fastest in every regime (more CTAs and more
   // W bytes in flight per SM); PDF_FWD_NT=2/4 for experiments
@@ -545,11 +564,11 @@ static cudaError_t bwd_mma_launch(bool fused, dim3 grid, int CN, NetBwdArgs<doub
   if (fused) {
     auto k = net_bwd_mma_kernel<MT, KT, true, WB>;
     e = prep(k, smem);
-    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, CN, 1), args);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, a.gzprev ? CN : 1, 1), args);
   } else {
     auto k = net_bwd_mma_kernel<MT, KT, false, WB>;
     e = prep(k, smem);
-    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, CN, 1), args);
+    if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, a.gzprev ? CN : 1, 1), args);
   }
   return e;
 }
@@ -573,11 +592,17 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   if (kt_env == 1 || (kt_env == 2 && MT <= 4)) KT = kt_env;
   const int WB = S >= 4 ? BM_WARPS : 4;     // one scene: narrower CTAs, more of them
   const int CW = WB * 8 * KT;
+  // N split: a cluster of CN CTAs when g_h is reduced across it (DSMEM),
+  // plain CTAs for the first layer; CTA-count targets per SM in env for
+  // experiments
   static const int cap = env_int("PDF_BWD_CLUSTER", 16);
+  static const int tgt = env_int("PDF_BWD_TGT", 3), tgt1 = env_int("PDF_BWD_TGT1", 3);
   const long long base = (long long)((K + CW - 1) / CW) * S;
   const int nmax = (N + BM_NCH - 1) / BM_NCH;
+  const int cap_n = a.gzprev ? cap : 64;
+  const long long target = (long long)(a.gzprev ? tgt : tgt1) * 148;
   int CN = 1;
-  while (CN < cap && 2 * CN <= nmax && base * CN < 3 * 148) CN *= 2;
+  while (CN < cap_n && 2 * CN <= nmax && base * CN < target) CN *= 2;
   a.ns = ((N + CN - 1) / CN + BM_NCH - 1) / BM_NCH * BM_NCH;
   const dim3 grid((K + CW - 1) / CW, CN, S);
   cudaError_t e;
@@ -758,6 +783,19 @@ static int create_impl(pdf_ctx* c, void* ws, size_t bytes, cudaStream_t st) {
   permute_khat_kernel<T><<<(PP + 255) / 256, 256, 0, st>>>((const C<T>*)c->d.gd_kernel_hat, (C<T>*)c->khat, c->P,
                                                             c->large && c->E >= 4 ? 1 : 0);
   CK_CUDA(cudaGetLastError());
+  {
+    // H = G_S o expand (R x M0), two fixed-order contraction passes in float64
+    double2* t1 = nullptr;
+    const long long n1 = (long long)c->d.R * c->M * c->K;
+    CK_CUDA(cudaMallocAsync((void**)&t1, (size_t)n1 * sizeof(double2), st));
+    hs_rows_kernel<T><<<(unsigned)((n1 + 255) / 256), 256, 0, st>>>((const C<T>*)c->d.gs_matrix, t1, c->M, c->d.mf,
+                                                                    c->d.R);
+    const int n2 = c->d.R * c->M0;
+    hs_cols_kernel<T><<<(n2 + 255) / 256, 256, 0, st>>>(t1, (C<T>*)c->hs, c->M, c->d.mf, c->d.R);
+    const cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(t1, st);
+    CK_CUDA(e);
+  }
   CK_CUDA(cudaStreamSynchronize(st));
   return PDF_OK;
 }
@@ -1138,7 +1176,7 @@ static ShardArgs<T> shard_args(pdf_ctx* c, double* red1, double* red2) {
   a.beta = (T)c->d.beta; a.l1 = (T)c->d.lambda1; a.l2 = (T)c->d.lambda2; a.l3 = (T)c->d.lambda3;
   a.tau = (T)c->d.tau_b;
   a.J = (const C<T>*)c->J; a.E = (const C<T>*)c->E_; a.norms = c->norms; a.grows = (const C<T>*)c->grows;
-  a.gs = (const C<T>*)c->d.gs_matrix; a.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
+  a.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
   a.c_inc = c->c_inc; a.red1 = red1; a.red2 = red2; a.dloss = c->dloss; a.pix = c->pix; a.part = c->part;
   a.gJ = (C<T>*)c->gJ; a.gE = (C<T>*)c->gE; a.err = c->err;
   return a;

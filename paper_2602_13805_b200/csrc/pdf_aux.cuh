@@ -18,6 +18,75 @@ __device__ inline int khat_pos_freq(int pos, int P, int split) {
   return 2 * spectrum_slot_freq(r % 32, r / 32, E / 2) + h;
 }
 
+// ---------------------------------------------------------------------------
+// Spectral receiver operator H = G_S o expand (built once per geometry).
+// expand (spectral.py:68-79) is linear, J = sum_m alpha[m] phi_m with
+// phi_m(y, x) = exp(+2 pi i (f_u y + f_w x) / M) / M^2, so the data residual
+// of the loss (losses.py:229-232) is
+//     D[v][r] = sum_p J[v][p] G_S[r][p] = sum_m alpha[v][m] H[r][m],
+//     H[r][m] = sum_p G_S[r][p] phi_m(p)                (R x M0, slot order)
+// and its adjoint contribution to g_alpha (forward.py:303-306 followed by
+// truncate / (m1 m2), spectral.py:56-65, losses.py:288,306) is
+//     g_alpha[v][m] += sum_r g_rows[v][r] conj(H[r][m]).
+// The hot loop then never touches the R x M^2 receiver matrix.  Built in
+// float64 with fixed-order sums: stage 1 contracts x, stage 2 contracts y.
+__device__ __forceinline__ int spec_corner_freq(int u, int mf, int M) { return u < mf ? u : M - 2 * mf + u; }
+
+template <typename T>
+__global__ void hs_rows_kernel(const C<T>* gs, double2* t1, int M, int mf, int R) {
+  // t1[r][y][w] = sum_x G_S[r][y M + x] exp(+2 pi i f_w x / M)
+  const int K = 2 * mf;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)R * M * K) return;
+  const int w = (int)(idx % K), y = (int)((idx / K) % M), r = (int)(idx / ((long long)K * M));
+  const int f = spec_corner_freq(w, mf, M);
+  const C<T>* g = gs + (size_t)r * M * M + (size_t)y * M;
+  double sr = 0.0, si = 0.0;
+  for (int x = 0; x < M; ++x) {
+    double s, c;
+    sincospi(2.0 * (double)((f * x) % M) / (double)M, &s, &c);
+    const double gr = (double)g[x].x, gi = (double)g[x].y;
+    sr += gr * c - gi * s;
+    si += gr * s + gi * c;
+  }
+  t1[idx] = make_double2(sr, si);
+}
+
+template <typename T>
+__global__ void hs_cols_kernel(const double2* t1, C<T>* hs, int M, int mf, int R) {
+  // H[r][slot(u, w)] = sum_y t1[r][y][w] exp(+2 pi i f_u y / M) / M^2
+  const int K = 2 * mf, M0 = K * K;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * M0) return;
+  const int r = idx / M0, i = idx % M0, u = i / K, w = i % K;
+  const int f = spec_corner_freq(u, mf, M);
+  double sr = 0.0, si = 0.0;
+  for (int y = 0; y < M; ++y) {
+    double s, c;
+    sincospi(2.0 * (double)((f * y) % M) / (double)M, &s, &c);
+    const double2 v = t1[((size_t)r * M + y) * K + w];
+    sr += v.x * c - v.y * s;
+    si += v.x * s + v.y * c;
+  }
+  const double inv = 1.0 / ((double)M * (double)M);
+  const int slot = (((u / mf) * 2 + (w / mf)) * mf + (u % mf)) * mf + (w % mf);   // spectral.py:29-44
+  hs[(size_t)r * M0 + slot] = mk<T>((T)(sr * inv), (T)(si * inv));
+}
+
+// sum_r g_rows[r] conj(H[r][slot]) over receivers r0, r0 + rstep, ... (fixed order)
+template <typename T>
+__device__ __forceinline__ C<T> data_adjoint_at(const C<T>* grow, const C<T>* hs, int R, int M0, int slot, int r0,
+                                                int rstep) {
+  C<T> a0 = czero<T>(), a1 = czero<T>();
+  int r = r0;
+  for (; r + rstep < R; r += 2 * rstep) {
+    a0 = cadd<T>(a0, cmulc<T>(grow[r], hs[(size_t)r * M0 + slot]));
+    a1 = cadd<T>(a1, cmulc<T>(grow[r + rstep], hs[(size_t)(r + rstep) * M0 + slot]));
+  }
+  if (r < R) a0 = cadd<T>(a0, cmulc<T>(grow[r], hs[(size_t)r * M0 + slot]));
+  return cadd<T>(a0, a1);
+}
+
 template <typename T>
 __global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P, int split) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;

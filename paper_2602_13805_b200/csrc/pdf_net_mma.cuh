@@ -167,6 +167,112 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
 }
 
 // ---------------------------------------------------------------------------
+// Forward layer for one scene with few rows (the latency-bound regime):
+// CTA = one n-tile of 8 outputs, its XW warps split K.  The whole input
+// block x[rows][K] is staged into shared memory with cp.async and every W
+// fragment the warp needs (<= XKB k-blocks of 16) is requested into
+// registers at once, so the layer costs one memory round trip; the XW warp
+// partials are added in warp order through shared memory (no cluster).
+constexpr int XW = 8;
+constexpr int XKB = 8;                  // k-blocks per warp: K <= XW * XKB * 16 = 1024
+
+__host__ __device__ constexpr size_t fwd_x_smem_bytes(int MT, int K) {
+  const size_t xs = (size_t)8 * MT * (K + 2);
+  const size_t red = (size_t)XW * 8 * MT * 8;
+  return (xs + red) * sizeof(double);
+}
+
+template <int MT>
+__global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double> a) {
+  constexpr int RPM = 8 * MT, THR = XW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, N = a.N, rows = a.rows, XP = K + 2;
+  double* Xs = reinterpret_cast<double*>(smem_raw);     // [RPM][K + 2]
+  double* red = Xs + (size_t)RPM * XP;                  // [XW][RPM][8]
+  const int scene = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int n0 = blockIdx.x * 8, n = n0 + g;
+  const int kpw = ((K + XW * 16 - 1) / (XW * 16)) * 16;
+  const int kb = warp * kpw, ke = min(K, kb + kpw);
+  const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off + (size_t)(n < N ? n : 0) * K;
+  const double* __restrict__ X = a.in + scene * a.in_ss;
+  double b[XKB][4];
+  auto loadW = [&]() {
+#pragma unroll
+    for (int q = 0; q < XKB; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kk = kb + 16 * q + 4 * t + 2 * h;
+        double2 v = make_double2(0.0, 0.0);
+        if (n < N && kk < ke) v = *reinterpret_cast<const double2*>(W + kk);
+        b[q][2 * h] = v.x;
+        b[q][2 * h + 1] = v.y;
+      }
+  };
+  if (a.w_early) loadW();
+  pdl_wait();
+  if (!a.w_early) loadW();
+  if (a.step && tid == 0 && blockIdx.x == 0 && scene == 0) atomicAdd(a.step, 1);
+  const int seg = K / 2;
+  for (int i = tid; i < RPM * seg; i += THR) {
+    const int r = i / seg, s2 = i - r * seg;
+    const bool ok = r < rows;
+    cp_async16(Xs + (size_t)r * XP + 2 * s2, ok ? X + (size_t)r * K + 2 * s2 : X, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  pdl_trigger();
+  double acc[MT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < XKB; ++q) {
+    const int kk = kb + 16 * q;
+    if (kk < ke) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double* xr = Xs + (size_t)(8 * i + g) * XP + kk + 4 * t;
+        const double2 a01 = *reinterpret_cast<const double2*>(xr);
+        const double2 a23 = kk + 4 * t + 2 < ke ? *reinterpret_cast<const double2*>(xr + 2) : make_double2(0.0, 0.0);
+        const bool in0 = kk + 4 * t < ke;
+        const double av[4] = {in0 ? a01.x : 0.0, in0 ? a01.y : 0.0, a23.x, a23.y};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma(acc[i][0], acc[i][1], av[u], b[q][u]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) red[(warp * RPM + 8 * i + g) * 8 + 2 * t + c] = acc[i][c];
+  __syncthreads();
+  const double* bias = a.theta + scene * a.th_ss + a.b_off;
+  for (int e = tid; e < RPM * 8; e += THR) {
+    const int r = e >> 3, col = e & 7, gn = n0 + col;
+    if (gn >= N || r >= rows) continue;
+    double z = 0.0;
+#pragma unroll
+    for (int w = 0; w < XW; ++w) z += red[(w * RPM + r) * 8 + col];
+    z += bias[gn];
+    if (!a.final_layer) {
+      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+    } else {
+      const double yv = z * a.cout[(size_t)scene * N + gn];
+      const int half = N / 2;
+      const int f = gn < half ? gn : gn - half;
+      int view, m;
+      if (a.joint) { view = f / a.M0; m = f % a.M0; } else { view = r; m = f; }
+      const size_t off = ((size_t)scene * a.n + view) * a.M0 + m;
+      double* dst = reinterpret_cast<double*>(a.alpha_hat + off);
+      const double* src = reinterpret_cast<const double*>(a.alpha0 + off);
+      if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Backward layer + fused Adam on DMMA (network.py:201-219, 248-264):
 //   g_W[n][k] = sum_r g_z[r][n] h[r][k]     (MMA: M = n, N = k, K = r)
 //   g_h[r][k] = sum_n g_z[r][n] W_old[n][k] (MMA: M = r, N = k, K = n)
@@ -199,8 +305,10 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
   double* cpart = reinterpret_cast<double*>(ring + BM_D * 3 * KT * THR);   // [RPM][CW]
   __shared__ double bc_s[2];
   cg::cluster_group cluster = cg::this_cluster();
-  const int CN = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
+  // grid.y == CN: the whole y extent is one cluster when g_h is reduced
+  // across it, and plain CTAs otherwise (first layer: no g_h)
+  const int CN = (int)gridDim.y;
+  const int rank = (int)blockIdx.y;
   const int scene = blockIdx.z;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;

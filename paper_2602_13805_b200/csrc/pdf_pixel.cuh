@@ -6,7 +6,9 @@
 //   P = E + beta J, S = R P - beta J, ||S||^2               losses.py:225-227
 //   bound / tv / bridge values and chi-gradients            losses.py:115-195
 //   reverse pass (losses.py:279-300):
-//     g_S = 2S/c_inc, g_P = conj(R) g_S, g_J = beta (g_P - g_S) + G_S^H g_rows
+//     g_S = 2S/c_inc, g_P = conj(R) g_S, g_J = beta (g_P - g_S)
+//     (the G_S^H g_rows part of g_J enters g_alpha through the spectral
+//     receiver operator in the view backward, pdf_aux.cuh)
 //     g_chi = g_reg + conj(beta/(beta chi+1)^2) sum_i conj(P_i) g_S_i
 //     g_num = g_chi/den, g_den = -Re(conj(g_chi) chi)/den
 //     g_J += E g_num, g_E = g_P + conj(g_num) J + 2 g_den E
@@ -16,9 +18,8 @@
 // access is a coalesced row segment.  The regulariser stencils need chi on a
 // one-pixel halo, which the CTA recomputes (rows y-1..y+1) instead of a
 // separate launch; the stencil terms of rows y-1 and y are computed once per
-// halo pixel by parallel threads.  The G_S columns of the tile and the
-// scene's g_rows are staged in shared memory with cp.async while the halo is
-// processed.  All cross-view sums are fixed-order (deterministic).
+// halo pixel by parallel threads.  All cross-view sums are fixed-order
+// (deterministic).
 #pragma once
 #include "pdf_common.cuh"
 #include "pdf_dmma.cuh"
@@ -32,8 +33,6 @@ struct PixelArgs {
   const C<T>* J;        // [S*n][M][M]
   const C<T>* E;        // [S*n][M][M]
   const double* norms;  // [S*n][CS]
-  const C<T>* grows;    // [S*n][R]
-  const C<T>* gs;       // [R][M*M]
   const C<T>* rfixed;   // [S][M][M] or null
   const double* c_inc;  // [S]
   C<T>* gJ;             // [S*n][M][M]  (g_J local part)
@@ -46,12 +45,6 @@ struct PixelArgs {
 constexpr double EPS_TV = 1e-12;   // losses.py:29
 constexpr int PIX_TX = 32;         // max tile width
 constexpr int PIX_NW = 8;          // warps per CTA
-
-template <typename T>
-__host__ __device__ inline size_t pixel_smem_bytes(int n, int R) {
-  // gs tile [R][TX] + g_rows [n][R] (float32), or + G_S^H g_rows [n][TX] (float64, DMMA)
-  return ((size_t)R * PIX_TX + (size_t)n * (sizeof(T) == 8 ? PIX_TX : R)) * sizeof(C<T>);
-}
 
 template <typename T>
 __device__ __forceinline__ T amag(C<T> z) { return sqrt_<T>(cabs2<T>(z)); }
@@ -72,11 +65,8 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   __shared__ C<T> pgr[PIX_NW][PIX_TX];
   __shared__ double red[PIX_NW][4];
   __shared__ double eps_s;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C<T>* gsS = reinterpret_cast<C<T>*>(smem_raw);     // [R][TX]
-  C<T>* grS = gsS + (size_t)a.R * PIX_TX;             // [n][R] (float32) or G_S^H g_rows [n][TX] (float64)
 
-  const int M = a.M, n = a.n, R = a.R;
+  const int M = a.M, n = a.n;
   const int TX = M < PIX_TX ? M : PIX_TX;
   const int NH = 3 * (TX + 2);
   const int WW = TX + 2;
@@ -86,24 +76,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   const size_t img = (size_t)M * M;
   const size_t vbase = (size_t)scene * n;
 
-  if constexpr (GRAD) {
-    // stage this tile's G_S columns and the scene's g_rows (consumed at the end)
-    constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
-    const int segs = TX / EPC;
-    for (int i = tid; i < R * segs; i += blockDim.x) {
-      const int r = i / segs, sg = i % segs;
-      cp_async16(gsS + r * PIX_TX + sg * EPC, a.gs + (size_t)r * img + (size_t)y * M + x0 + sg * EPC, true);
-    }
-    cp_async_commit();
-  }
-  pdl_wait();   // J, E, norms, g_rows come from the previous kernel
-  if constexpr (GRAD && sizeof(T) != 8) {
-    constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
-    const int gseg = (n * R) / EPC;
-    for (int i = tid; i < gseg; i += blockDim.x)
-      cp_async16(grS + i * EPC, a.grows + vbase * R + i * EPC, true);
-    cp_async_commit();
-  }
+  pdl_wait();   // J, E, norms come from the previous kernel
 
   if (warp == 0) {
     const double mx = warp_max_view_power(a.norms + vbase * a.CS, n, a.CS);
@@ -245,18 +218,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
       gnum[tid] = mk<T>(gchi.x / den, gchi.y / den);
       gden[tid] = -(gchi.x * chi.x + gchi.y * chi.y) / den;   // -Re(conj(g_chi) chi)/den
     }
-    cp_async_wait<0>();
     __syncthreads();
-    if constexpr (sizeof(T) == 8) {
-      // G_S^H g_rows for the tile (forward.py:303-306) as a complex GEMM on
-      // the FP64 tensor cores: [n views] x [R] x [TX pixels]
-      const C<T>* gsT = gsS;
-      const C<T>* grG = a.grows + vbase * R;
-      cgemm_dmma(n, TX, R, [&](int v, int r) { return grG[(size_t)v * R + r]; },
-                 [&](int r, int xl) { return conj_<T>(gsT[r * PIX_TX + xl]); },
-                 [&](int v, int xl, C<T> val) { grS[v * PIX_TX + xl] = val; });
-      __syncthreads();
-    }
     if (lane < TX) {
       const size_t pix = (size_t)y * M + x0 + lane;
       const C<T> R_ = Rs[lane];
@@ -271,20 +233,6 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
         const C<T> gS = cscale<T>(Sr, gsc);
         const C<T> gP = cmul<T>(conj_<T>(R_), gS);
         C<T> gj = cscale<T>(csub<T>(gP, gS), beta);
-        // G_S^H g_rows at this pixel (forward.py:303-306), shared-memory operands
-        if constexpr (sizeof(T) == 8) {
-          gj = cadd<T>(gj, grS[i * PIX_TX + lane]);
-        } else {
-          const C<T>* gr = grS + (size_t)i * R;
-          C<T> acc0 = czero<T>(), acc1 = czero<T>();
-          int r = 0;
-          for (; r + 1 < R; r += 2) {
-            acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
-            acc1 = cadd<T>(acc1, cmulc<T>(gr[r + 1], gsS[(r + 1) * PIX_TX + lane]));
-          }
-          if (r < R) acc0 = cadd<T>(acc0, cmulc<T>(gr[r], gsS[r * PIX_TX + lane]));
-          gj = cadd<T>(gj, cadd<T>(acc0, acc1));
-        }
         gj = cadd<T>(gj, cmul<T>(e, gn));
         C<T> ge = cadd<T>(gP, cmul<T>(conj_<T>(gn), j));
         ge = cadd<T>(ge, cscale<T>(e, T(2) * gd));

@@ -30,7 +30,6 @@ struct ShardArgs {
   const C<T>* E;
   const double* norms;  // [S*n][CS]
   const C<T>* grows;    // [S*n][R]
-  const C<T>* gs;       // [R][M*M]
   const C<T>* rfixed;   // [S][M*M] or null
   const double* c_inc;
   double* red1;         // [S][3*M*M + 1] doubles: num (re,im interleaved), den, pmax
@@ -266,10 +265,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) shard_pixel_b_kernel(ShardArgs<T>
     const C<T> gS = cscale<T>(Sr, gsc);
     const C<T> gP = cmul<T>(conj_<T>(R_), gS);
     C<T> gj = cscale<T>(csub<T>(gP, gS), beta);
-    const C<T>* gr = a.grows + ((size_t)scene * n + i) * R;
-    C<T> acc = czero<T>();
-    for (int r = 0; r < R; ++r) acc = cadd<T>(acc, cmulc<T>(gr[r], a.gs[(size_t)r * img + pix]));
-    gj = cadd<T>(gj, acc);
+    // (G_S^H g_rows enters g_alpha through H in the view backward, pdf_aux.cuh)
     gj = cadd<T>(gj, cmul<T>(e, gn));
     C<T> ge = cadd<T>(gP, cmul<T>(conj_<T>(gn), j));
     ge = cadd<T>(ge, cscale<T>(e, T(2) * gd));

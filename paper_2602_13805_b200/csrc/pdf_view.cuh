@@ -4,10 +4,12 @@
 //
 //   VIEW_FWD  : alpha -> J = expand(alpha) (spectral.py:68-79)
 //               E = E_inc + G_D J          (forward.py:140-146, losses.py:220)
-//               D = J G_S^T - d (masked), ||D||^2, g_rows (losses.py:229-232,285-287)
+//               D = J G_S^T - d = alpha H^T - d (masked), ||D||^2, g_rows
+//               (losses.py:229-232,285-287; H = G_S o expand, pdf_aux.cuh)
 //               ||E_i||^2 partials for eps_reg (cie.py:42-50)
 //   VIEW_BWD  : g_J = g_J_local + G_D^H g_E   (forward.py:149-151, losses.py:303)
 //               g_alpha = truncate(g_J)/(m1 m2) (spectral.py:56-65, losses.py:306)
+//                         + g_rows conj(H)      (the G_S^H g_rows part of g_J)
 //               optionally scattered straight into the network's output
 //               gradient rows (network.py:575-582)
 //   VIEW_APPLY: y = G_D x or G_D^H x on dense images (init path, tests)
@@ -20,6 +22,7 @@
 //   B: per column  FFT, x K^, inverse FFT -> DSMEM scatter by row owner
 //   C: inverse row FFTs of my rows, crop to M columns
 #pragma once
+#include "pdf_aux.cuh"
 #include "pdf_common.cuh"
 #include "pdf_dmma.cuh"
 #include "pdf_pixel.cuh"
@@ -38,7 +41,7 @@ struct ViewArgs {
   const C<T>* alpha;  // [S*n][M0]
   const C<T>* einc;   // [S or 1][n][M][M]
   long long einc_scene_stride;   // elements; 0 = shared across scenes
-  const C<T>* gs;     // [R][M*M]
+  const C<T>* hs;     // [R][M0] spectral receiver operator (pdf_aux.cuh)
   const C<T>* data;   // [S][n][R]
   const T* mask;      // [S][n][R] or null
   const double* c_sca;  // [S]
@@ -47,7 +50,7 @@ struct ViewArgs {
   double* norms;      // [S*n][CS]
   C<T>* grows;        // [S*n][R]
   double* dloss;      // [S*n]
-  int do_data;        // 0: the data term runs as a separate GEMM (data_gemm_kernel)
+  int do_data;        // 0: the data term runs as a separate GEMM over the scene's views (data_mma_kernel)
   // BWD
   const C<T>* gE;     // [S*n][M][M]
   const C<T>* gJloc;  // [S*n][M][M]
@@ -228,32 +231,41 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   }
 
   // Split cluster barrier: the arrive releases my stage-A scatter; the data
-  // term (local rows, G_S from L2) then runs while the other CTAs finish
-  // theirs, and the wait acquires everyone's scatter before stage B.
+  // term (receivers rank, rank + CS, ...; H rows from L2) then runs while the
+  // other CTAs finish theirs, and the wait acquires everyone's scatter.
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (MODE == VIEW_FWD && a.do_data) {
-    // partial data residual over my pixels: sum_p J[p] G_S[r, p]
-    const size_t p0 = (size_t)y0 * M;
-    const int np = rp * M;
-    for (int r = warp; r < a.R; r += nw) {
-      const C<T>* g = a.gs + (size_t)r * img + p0;
-      C<T> acc = czero<T>();
-      C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
+    // D[r] = sum_m alpha[m] H[r][m] - d[r] (masked), g_rows = 2 D mask / c_sca
+    const C<T>* al = a.alpha + (size_t)v * M0;
+    const double csca = a.c_sca[scene];
+    double dl = 0.0;
+    for (int r = rank + CS * warp; r < a.R; r += CS * nw) {
+      const C<T>* h = a.hs + (size_t)r * M0;
+      C<T> acc = czero<T>(), acc1 = czero<T>();
       int i = lane;
-      for (; i + 96 < np; i += 128) {   // four independent chains, loads in flight together
-        acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
-        acc1 = cadd<T>(acc1, cmul<T>(s.rows[i + 32], g[i + 32]));
-        acc2 = cadd<T>(acc2, cmul<T>(s.rows[i + 64], g[i + 64]));
-        acc3 = cadd<T>(acc3, cmul<T>(s.rows[i + 96], g[i + 96]));
+      for (; i + 32 < M0; i += 64) {
+        acc = cadd<T>(acc, cmul<T>(al[i], h[i]));
+        acc1 = cadd<T>(acc1, cmul<T>(al[i + 32], h[i + 32]));
       }
-      for (; i < np; i += 32) acc = cadd<T>(acc, cmul<T>(s.rows[i], g[i]));
-      acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
+      if (i < M0) acc = cadd<T>(acc, cmul<T>(al[i], h[i]));
+      acc = cadd<T>(acc, acc1);
       acc.x = warp_sum<T>(acc.x);
       acc.y = warp_sum<T>(acc.y);
       if (lane == 0) {
-        C<T>* rx = cluster.map_shared_rank(xch, 0);
-        rx[rank * a.R + r] = acc;
+        const size_t di = (size_t)v * a.R + r;
+        C<T> d = csub<T>(acc, a.data[di]);
+        const T mk_ = a.mask ? a.mask[di] : T(1);
+        d = cscale<T>(d, mk_);
+        dl += (double)cabs2<T>(d);
+        a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
       }
+    }
+    if (lane == 0) red[16 + warp] = dl;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[16 + w];
+      cluster.map_shared_rank(red, 0)[40 + rank] = t;   // published by the cluster.sync after stage B
     }
   }
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -287,24 +299,10 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   }
   cluster.sync();   // also publishes the data partials (written before this arrive) to rank 0
 
-  if (MODE == VIEW_FWD && a.do_data) {
-    if (rank == 0) {
-      // D = sum of partials - d, masked; g_rows = 2 D mask / c_sca
-      double part = 0.0;
-      const double csca = a.c_sca[scene];
-      for (int r = tid; r < a.R; r += blockDim.x) {
-        C<T> acc = czero<T>();
-        for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * a.R + r]);
-        const size_t di = (size_t)v * a.R + r;
-        C<T> d = csub<T>(acc, a.data[di]);
-        T mk_ = a.mask ? a.mask[di] : T(1);
-        d = cscale<T>(d, mk_);
-        part += (double)cabs2<T>(d);
-        a.grows[di] = cscale<T>(d, T(2.0 / csca) * mk_);
-      }
-      double tot = block_sum_d<T>(part, red);
-      if (tid == 0) a.dloss[v] = tot;
-    }
+  if (MODE == VIEW_FWD && a.do_data && rank == 0 && tid == 0) {
+    double t = 0.0;
+    for (int c = 0; c < CS; ++c) t += red[40 + c];
+    a.dloss[v] = t;
   }
 
   // ---------------- stage C: inverse row FFTs, crop ------------------------
@@ -385,13 +383,30 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
     cluster.sync();
     const T inv = T(1) / (T(M) * T(M));
-    for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {
-      C<T> acc = czero<T>();
-      for (int c = 0; c < CS; ++c) {
-        const C<T>* other = cluster.map_shared_rank(xch, c);
-        acc = cadd<T>(acc, other[i]);
+    // G_S^H g_rows through H: outputs i = rank + CS*(o + 32 q) of this rank,
+    // warp w sums receivers w, w + nw, ... into dadj, added in warp order
+    // scratch: bufA, bufB and rows are contiguous and free after stage B
+    C<T>* dadj = s.bufA;   // [nwd][32]
+    const int nwd = min(nw, (int)(((size_t)M * cpp + (size_t)rp * Pp + (size_t)rp * M) / 32));
+    const C<T>* grow = a.grows + (size_t)v * a.R;
+    const int nout = (M0 - rank + CS - 1) / CS;
+    for (int ob = 0; ob < nout; ob += 32) {
+      const int o = ob + lane, i = rank + CS * o;
+      if (o < nout && warp < nwd) {
+        const int slot = corner_slot(i / K, i % K, mf);
+        dadj[warp * 32 + lane] = data_adjoint_at<T>(grow, a.hs, a.R, M0, slot, warp, nwd);
       }
-      acc = cscale<T>(acc, inv);
+      __syncthreads();
+      if (warp == 0 && o < nout) {
+        C<T> acc = czero<T>();
+        for (int c = 0; c < CS; ++c) {
+          const C<T>* other = cluster.map_shared_rank(xch, c);
+          acc = cadd<T>(acc, other[i]);
+        }
+        acc = cscale<T>(acc, inv);
+        C<T> dsum = czero<T>();
+        for (int w = 0; w < nwd; ++w) dsum = cadd<T>(dsum, dadj[w * 32 + lane]);
+        acc = cadd<T>(acc, dsum);
       const int u = i / K, w = i % K;
       const int slot = corner_slot(u, w, mf);
       if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
@@ -405,6 +420,8 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
         gyrow[re] = acc.x * co[re];
         gyrow[re + D0 / 2] = acc.y * co[re + D0 / 2];
       }
+      }
+      __syncthreads();
     }
     cluster.sync();
   }

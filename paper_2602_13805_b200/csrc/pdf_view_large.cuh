@@ -59,6 +59,8 @@ struct VLArgs {
   T* gy;
   const T* cout;
   int joint;
+  const C<T>* grows;           // [S*n][R] data-residual gradient rows
+  const C<T>* hs;              // [R][M0] spectral receiver operator (pdf_aux.cuh)
   FinalizeArgs fin;
   int do_fin;
 };
@@ -373,8 +375,9 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   }
 }
 
-// g_alpha = sum of the truncation partials / (m1 m2), scattered into the
-// network's output-gradient rows; (view 0, block 0) of each scene finalises
+// g_alpha = sum of the truncation partials / (m1 m2) + g_rows conj(H) (the
+// G_S^H g_rows part of g_J, pdf_aux.cuh), scattered into the network's
+// output-gradient rows; (view 0, block 0) of each scene finalises
 // the loss breakdown (losses.py:36-49)
 template <typename T>
 __global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
@@ -391,6 +394,7 @@ __global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
   acc = cscale<T>(acc, T(1) / (T(M) * T(M)));
   const int u = i / K, w = i % K;
   const int slot = vl_corner_slot(u, w, mf);
+  acc = cadd<T>(acc, data_adjoint_at<T>(a.grows + (size_t)v * a.R, a.hs, a.R, M0, slot, 0, 1));
   if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
   if (a.gy) {
     const int D0 = 2 * M0 * (a.joint ? a.n : 1);

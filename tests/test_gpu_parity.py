@@ -174,7 +174,9 @@ def test_cfg1_trajectory(cfg1_setup, g_cfg1, use_graph):
 
 
 def test_batched_equals_single(cfg1_setup, g_cfg1):
-    """S scenes in one launch == S separate single-scene runs (bitwise)."""
+    """S scenes in one launch == S separate single-scene runs.  Kernel shapes
+    (and so float64 summation orders) are chosen per batch size, so the
+    comparison is to 1e-9 relative; rerun determinism is bitwise (below)."""
     from paper_2602_13805_b200.api import BatchReconstructor
     g = g_cfg1
     rng = np.random.default_rng(0)
@@ -185,8 +187,8 @@ def test_batched_equals_single(cfg1_setup, g_cfg1):
     r1 = BatchReconstructor(cfg1_setup.cfg, 1, e_inc=cfg1_setup.e_inc)
     for s in range(3):
         one = r1.run([datas[s]], seeds=[seeds[s]], k_iters=20)[0]
-        assert np.array_equal(one.chi_cco.values, batch[s].chi_cco.values)
-        assert [b.total for b in one.trace] == [b.total for b in batch[s].trace]
+        np.testing.assert_allclose(one.chi_cco.values, batch[s].chi_cco.values, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose([b.total for b in one.trace], [b.total for b in batch[s].trace], rtol=1e-9)
 
 
 def test_deterministic_rerun(cfg1_setup, g_cfg1):
