@@ -556,31 +556,37 @@ static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, 
 }
 
 // DMMA backward layer (float64)
-template <int MT, int KT, int WB>
+template <int MT, int KT, int WB, int D>
 static cudaError_t bwd_mma_launch(bool fused, dim3 grid, int CN, NetBwdArgs<double>& a, cudaStream_t st) {
-  const size_t smem = bwd_mma_smem_bytes(MT, KT, WB);
+  const size_t smem = bwd_mma_smem_bytes(MT, KT, WB, D);
   void* args[] = {&a};
   cudaError_t e;
   if (fused) {
-    auto k = net_bwd_mma_kernel<MT, KT, true, WB>;
+    auto k = net_bwd_mma_kernel<MT, KT, true, WB, D>;
     e = prep(k, smem);
     if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, a.gzprev ? CN : 1, 1), args);
   } else {
-    auto k = net_bwd_mma_kernel<MT, KT, false, WB>;
+    auto k = net_bwd_mma_kernel<MT, KT, false, WB, D>;
     e = prep(k, smem);
     if (e == cudaSuccess) e = launch_cluster(k, grid, dim3(WB * 32), smem, st, dim3(1, a.gzprev ? CN : 1, 1), args);
   }
   return e;
 }
 
+// D = n-tiles in flight per lane: 6 with one k-tile per warp (more bytes in
+// flight where few warps stream), 3 with two (batches: two CTAs per SM)
 template <int MT>
-static cudaError_t bwd_mma_kt(int KT, int WB, bool fused, dim3 grid, int CN, NetBwdArgs<double>& a,
+static cudaError_t bwd_mma_kt(int KT, int WB, int D, bool fused, dim3 grid, int CN, NetBwdArgs<double>& a,
                               cudaStream_t st) {
   if constexpr (MT <= 4) {
-    if (KT == 2) return WB == 8 ? bwd_mma_launch<MT, 2, 8>(fused, grid, CN, a, st)
-                                : bwd_mma_launch<MT, 2, 4>(fused, grid, CN, a, st);
+    if (KT == 2) return WB == 8 ? bwd_mma_launch<MT, 2, 8, 3>(fused, grid, CN, a, st)
+                                : bwd_mma_launch<MT, 2, 4, 3>(fused, grid, CN, a, st);
   }
-  return WB == 8 ? bwd_mma_launch<MT, 1, 8>(fused, grid, CN, a, st) : bwd_mma_launch<MT, 1, 4>(fused, grid, CN, a, st);
+  if (D == 6)
+    return WB == 8 ? bwd_mma_launch<MT, 1, 8, 6>(fused, grid, CN, a, st)
+                   : bwd_mma_launch<MT, 1, 4, 6>(fused, grid, CN, a, st);
+  return WB == 8 ? bwd_mma_launch<MT, 1, 8, 3>(fused, grid, CN, a, st)
+                 : bwd_mma_launch<MT, 1, 4, 3>(fused, grid, CN, a, st);
 }
 
 static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStream_t st) {
@@ -590,7 +596,11 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   int KT = 1;
   if (MT <= 4 && (long long)((K + 63) / 64) * S >= 2 * 148) KT = 2;
   if (kt_env == 1 || (kt_env == 2 && MT <= 4)) KT = kt_env;
-  const int WB = S >= 4 ? BM_WARPS : 4;     // one scene: narrower CTAs, more of them
+  static const int wb_env = env_int("PDF_BWD_WB", 0), d_env = env_int("PDF_BWD_D", 3);
+  // 8 warps per CTA in every regime (measured: cfg2 96.8 -> 93.7 us/iter,
+  // cfg5 backward 795 -> 671 us against 4-warp CTAs for one scene)
+  const int WB = wb_env ? wb_env : BM_WARPS;
+  const int D = KT == 1 ? d_env : 3;
   const int CW = WB * 8 * KT;
   // N split: a cluster of CN CTAs when g_h is reduced across it (DSMEM),
   // plain CTAs for the first layer; CTA-count targets per SM in env for
@@ -607,16 +617,16 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   const dim3 grid((K + CW - 1) / CW, CN, S);
   cudaError_t e;
   switch (MT) {
-    case 1: e = bwd_mma_kt<1>(KT, WB, fused, grid, CN, a, st); break;
-    case 2: e = bwd_mma_kt<2>(KT, WB, fused, grid, CN, a, st); break;
-    case 3: e = bwd_mma_kt<3>(KT, WB, fused, grid, CN, a, st); break;
-    case 4: e = bwd_mma_kt<4>(KT, WB, fused, grid, CN, a, st); break;
-    case 5: e = bwd_mma_kt<5>(KT, WB, fused, grid, CN, a, st); break;
-    case 6: e = bwd_mma_kt<6>(KT, WB, fused, grid, CN, a, st); break;
-    case 7: e = bwd_mma_kt<7>(KT, WB, fused, grid, CN, a, st); break;
-    case 8: e = bwd_mma_kt<8>(KT, WB, fused, grid, CN, a, st); break;
-    case 9: e = bwd_mma_kt<9>(KT, WB, fused, grid, CN, a, st); break;
-    case 10: e = bwd_mma_kt<10>(KT, WB, fused, grid, CN, a, st); break;
+    case 1: e = bwd_mma_kt<1>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 2: e = bwd_mma_kt<2>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 3: e = bwd_mma_kt<3>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 4: e = bwd_mma_kt<4>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 5: e = bwd_mma_kt<5>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 6: e = bwd_mma_kt<6>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 7: e = bwd_mma_kt<7>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 8: e = bwd_mma_kt<8>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 9: e = bwd_mma_kt<9>(KT, WB, D, fused, grid, CN, a, st); break;
+    case 10: e = bwd_mma_kt<10>(KT, WB, D, fused, grid, CN, a, st); break;
     default: return fail(PDF_EINVAL, "rows");
   }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net bwd (dmma): ") + cudaGetErrorString(e));

@@ -288,20 +288,23 @@ __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double
 constexpr int BM_WARPS = 8;              // warps per CTA for batches (4 for one scene: more CTAs)
 constexpr int BM_NCH = 32;              // n per staged g_z chunk (4 n-tiles)
 constexpr int BM_GP = BM_NCH + 4;       // pitch: conflict-free fragment reads in both products
-constexpr int BM_D = 3;                 // n-tiles in flight per lane (<= BM_NCH / 8 with two chunk buffers)
+// D (template): n-tiles in flight per lane; g_z chunk buffers: 2 for D <= 4,
+// 3 for D <= 8 (the refill may stage the chunk after next)
+__host__ __device__ constexpr int bm_ngb(int D) { return D > 4 ? 3 : 2; }
 
-__host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT, int WB) {
-  return ((size_t)2 * 8 * MT * BM_GP + (size_t)BM_D * 3 * KT * WB * 32 * 2 +
+__host__ __device__ constexpr size_t bwd_mma_smem_bytes(int MT, int KT, int WB, int D) {
+  return ((size_t)bm_ngb(D) * 8 * MT * BM_GP + (size_t)D * 3 * KT * WB * 32 * 2 +
           (size_t)8 * MT * WB * 8 * KT) * sizeof(double);
 }
 
-template <int MT, int KT, bool FUSED, int WB>
+template <int MT, int KT, bool FUSED, int WB, int BM_D>
 __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double> a) {
+  constexpr int NGB = bm_ngb(BM_D);
   constexpr int RPM = 8 * MT, SEG = BM_NCH / 2, KC = 8 * KT, CW = WB * KC;
   constexpr int THR = WB * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Gs = reinterpret_cast<double*>(smem_raw);              // 2 x [RPM][BM_GP]  g_z[r][c0 + i]
-  double2* ring = reinterpret_cast<double2*>(Gs + 2 * RPM * BM_GP);   // [BM_D][3][KT][THR]
+  double2* ring = reinterpret_cast<double2*>(Gs + NGB * RPM * BM_GP);   // [BM_D][3][KT][THR]
   double* cpart = reinterpret_cast<double*>(ring + BM_D * 3 * KT * THR);   // [RPM][CW]
   __shared__ double bc_s[2];
   cg::cluster_group cluster = cg::this_cluster();
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
 
   auto stage_gz = [&](int c) {          // chunk c of this rank (no commit)
     const int n0 = nb + c * BM_NCH;
-    double* dst = Gs + (c & 1) * RPM * BM_GP;
+    double* dst = Gs + (c % NGB) * RPM * BM_GP;
     for (int i = tid; i < RPM * SEG; i += THR) {
       const int r = i / SEG, sg = i % SEG, gn = n0 + 2 * sg;
       const bool ok = r < rows && gn < ne;
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < KT; ++j) gh[i][j][0] = gh[i][j][1] = 0.0;
-  if (ntl > 0) stage_gz(0);
+  for (int c = 0; 4 * c < BM_D && 4 * c < ntl; ++c) stage_gz(c);
   cp_async_commit();
 
   int errbits = 0;
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
     const int c = it >> 2, nt = (it & 3) * 8;
     if ((it & 3) == 0) __syncthreads();   // chunk c visible to all; chunk c-1 no longer read
     else __syncwarp();
-    const double* G = Gs + (c & 1) * RPM * BM_GP;
+    const double* G = Gs + (c % NGB) * RPM * BM_GP;
     const double ibc1 = bc_s[0], ibc2 = bc_s[1];
     const int sl = it % BM_D;
     // bias of chunk c (network.py:213,217), by the first column tile

@@ -75,6 +75,9 @@ struct ViewSmem {
   C<T>* bufB;   // (M/CS) * (P + 1)
   C<T>* rows;   // (M/CS) * M
   C<T>* small;  // M0 + (M/CS)*K : A (spectral grid) then V / U
+  C<T>* khs;    // (P/CS) * P : my K^ columns (constant: prefetched before the dependency wait)
+  C<T>* pre;    // (M/CS) * M : FWD: my E_inc rows (constant, prefetched); BWD: my g_J local rows
+  C<T>* dsum;   // 32 * nw + M0/CS + 1 : BWD data-adjoint scratch and per-output sums
   // followed by xch: max(CS*R, M0) partial-sum exchange (read remotely)
 };
 
@@ -84,7 +87,12 @@ __host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) 
   const int rp = M / CS;
   size_t a = (size_t)M0 + (size_t)rp * K;
   size_t xch = (size_t)CS * R > (size_t)M0 ? (size_t)CS * R : (size_t)M0;
-  size_t n = (size_t)P + M + (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M + a + xch;
+  // 8-CTA clusters (latency regime, one CTA per SM) also stage the constant
+  // K^ columns and the E_inc / g_J-local rows; 4-CTA clusters (batches) keep
+  // two CTAs per SM and read them from L2 in place
+  const size_t stage = CS == 8 ? (size_t)(P / CS) * P + (size_t)rp * M : 0;
+  size_t pre = stage + (size_t)32 * 8 + (size_t)M0 / CS + 1;
+  size_t n = (size_t)P + M + (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M + a + pre + xch;
   return n * sizeof(C<T>) + 64 * sizeof(double);
 }
 
@@ -135,15 +143,50 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   s.bufB = p; p += (size_t)rp * Pp;
   s.rows = p; p += (size_t)rp * M;
   s.small = p; p += (size_t)M0 + (size_t)rp * K;
+  constexpr bool PRE = CS == 8;   // staged constants (view_smem_bytes)
+  s.khs = p; p += PRE ? (size_t)cp * P : 0;
+  s.pre = p; p += PRE ? (size_t)rp * M : 0;
+  s.dsum = p; p += (size_t)32 * 8 + M0 / CS + 1;
   C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)M0 ? (size_t)CS * a.R : (size_t)M0);
   double* red = reinterpret_cast<double*>(p);
 
   for (int i = tid; i < P; i += blockDim.x) s.tw[i] = a.twP[i];
   for (int i = tid; i < M; i += blockDim.x) s.twm[i] = a.twM[i];
-  const size_t img = (size_t)M * M;
   __syncthreads();
   LaneTw<T, E> ltw;
   ltw.load(s.tw, lane);
+  // constants: my K^ columns (and E_inc rows) stream in while the previous
+  // kernel drains
+  const size_t img = (size_t)M * M;
+  constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
+  if constexpr (PRE && MODE != VIEW_APPLY) {
+    const C<T>* src = a.khat + (size_t)rank * cp * P;
+    for (int i = tid; i < cp * P / EPC; i += blockDim.x) cp_async16(s.khs + i * EPC, src + i * EPC, true);
+  }
+  if constexpr (PRE && MODE == VIEW_FWD) {
+    const C<T>* src = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img + (size_t)y0 * M;
+    for (int i = tid; i < rp * M / EPC; i += blockDim.x) cp_async16(s.pre + i * EPC, src + i * EPC, true);
+  }
+  cp_async_commit();
+  if constexpr (MODE == VIEW_BWD) {
+    // G_S^H g_rows through H (pdf_aux.cuh) for my outputs i = rank + CS*o:
+    // g_rows was finalised two launches back (view_fwd / data term), so this
+    // runs before the dependency wait; warp w sums receivers w, w + nw, ...
+    const C<T>* grow = a.grows + (size_t)v * a.R;
+    const int nout = (M0 - rank + CS - 1) / CS;
+    C<T>* scr = s.dsum + M0 / CS + 1;   // [nw][32]
+    for (int ob = 0; ob < nout; ob += 32) {
+      const int o = ob + lane, i = rank + CS * o;
+      if (o < nout) scr[warp * 32 + lane] = data_adjoint_at<T>(grow, a.hs, a.R, M0, corner_slot(i / K, i % K, mf), warp, nw);
+      __syncthreads();
+      if (warp == 0 && o < nout) {
+        C<T> d = czero<T>();
+        for (int w = 0; w < nw; ++w) d = cadd<T>(d, scr[w * 32 + lane]);
+        s.dsum[o] = d;
+      }
+      __syncthreads();
+    }
+  }
   pdl_wait();   // everything below reads the previous kernel's outputs
 
   // ---------------- stage 0: my input rows -> s.rows ----------------------
@@ -200,6 +243,12 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
     __syncthreads();
   } else if constexpr (MODE == VIEW_BWD) {
+    // my g_E rows (conjugated) now; my g_J local rows stream in for stage C
+    if constexpr (PRE) {
+      const C<T>* gl = a.gJloc + (size_t)v * img + (size_t)y0 * M;
+      for (int i = tid; i < rp * M / EPC; i += blockDim.x) cp_async16(s.pre + i * EPC, gl + i * EPC, true);
+      cp_async_commit();
+    }
     const C<T>* g = a.gE + (size_t)v * img + (size_t)y0 * M;
     for (int i = tid; i < rp * M; i += blockDim.x) s.rows[i] = conj_<T>(g[i]);
     __syncthreads();
@@ -268,6 +317,8 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       cluster.map_shared_rank(red, 0)[40 + rank] = t;   // published by the cluster.sync after stage B
     }
   }
+  cp_async_wait<0>();   // K^ columns, E_inc / g_J local rows (own copies: a CTA barrier follows)
+  __syncthreads();
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
   // ---------------- stage B: columns: FFT, x K^, inverse FFT ---------------
@@ -279,14 +330,16 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       const int row = lane + 32 * k;
       x[k] = (k < KH && lane_ok) ? s.bufA[(size_t)row * cpp + cc] : czero<T>();
     }
-    // the kernel spectrum column is fetched before the FFT so its latency hides
-    const C<T>* kh = a.khat + (size_t)posc * P;
-    C<T> kv[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) kv[q] = kh[q * 32 + lane];
     warp_fft_fwd<T, E>(x, ltw, lane);
+    if constexpr (PRE && MODE != VIEW_APPLY) {
+      const C<T>* kh = s.khs + (size_t)cc * P;
 #pragma unroll
-    for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kv[q]);
+      for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kh[q * 32 + lane]);
+    } else {
+      const C<T>* kh = a.khat + (size_t)posc * P;
+#pragma unroll
+      for (int q = 0; q < E; ++q) x[q] = cmul<T>(x[q], kh[q * 32 + lane]);
+    }
     warp_fft_inv<T, E>(x, ltw, lane);
 #pragma unroll
     for (int k = 0; k < KH; ++k) {
@@ -318,13 +371,14 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       if (!lane_ok) break;
       const int col = lane + 32 * k;
       if constexpr (MODE == VIEW_FWD) {
-        const C<T>* ei = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img +
-                         (size_t)(y0 + yl) * M + col;
-        C<T> e = cadd<T>(*ei, x[k]);
+        const C<T> ei = PRE ? s.pre[yl * M + col]
+                            : a.einc[(size_t)scene * a.einc_scene_stride + (size_t)view * img + (size_t)(y0 + yl) * M + col];
+        C<T> e = cadd<T>(ei, x[k]);
         a.E[rowoff + col] = e;
         nrm += (double)cabs2<T>(e);
       } else if constexpr (MODE == VIEW_BWD) {
-        s.rows[yl * M + col] = cadd<T>(a.gJloc[rowoff + col], conj_<T>(x[k]));
+        const C<T> gl = PRE ? s.pre[yl * M + col] : a.gJloc[rowoff + col];
+        s.rows[yl * M + col] = cadd<T>(gl, conj_<T>(x[k]));
       } else {
         a.y[rowoff + col] = a.conj_out ? conj_<T>(x[k]) : x[k];
       }
@@ -383,30 +437,14 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
     cluster.sync();
     const T inv = T(1) / (T(M) * T(M));
-    // G_S^H g_rows through H: outputs i = rank + CS*(o + 32 q) of this rank,
-    // warp w sums receivers w, w + nw, ... into dadj, added in warp order
-    // scratch: bufA, bufB and rows are contiguous and free after stage B
-    C<T>* dadj = s.bufA;   // [nwd][32]
-    const int nwd = min(nw, (int)(((size_t)M * cpp + (size_t)rp * Pp + (size_t)rp * M) / 32));
-    const C<T>* grow = a.grows + (size_t)v * a.R;
-    const int nout = (M0 - rank + CS - 1) / CS;
-    for (int ob = 0; ob < nout; ob += 32) {
-      const int o = ob + lane, i = rank + CS * o;
-      if (o < nout && warp < nwd) {
-        const int slot = corner_slot(i / K, i % K, mf);
-        dadj[warp * 32 + lane] = data_adjoint_at<T>(grow, a.hs, a.R, M0, slot, warp, nwd);
+    for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {
+      C<T> acc = czero<T>();
+      for (int c = 0; c < CS; ++c) {
+        const C<T>* other = cluster.map_shared_rank(xch, c);
+        acc = cadd<T>(acc, other[i]);
       }
-      __syncthreads();
-      if (warp == 0 && o < nout) {
-        C<T> acc = czero<T>();
-        for (int c = 0; c < CS; ++c) {
-          const C<T>* other = cluster.map_shared_rank(xch, c);
-          acc = cadd<T>(acc, other[i]);
-        }
-        acc = cscale<T>(acc, inv);
-        C<T> dsum = czero<T>();
-        for (int w = 0; w < nwd; ++w) dsum = cadd<T>(dsum, dadj[w * 32 + lane]);
-        acc = cadd<T>(acc, dsum);
+      acc = cscale<T>(acc, inv);
+      acc = cadd<T>(acc, s.dsum[(i - rank) / CS]);
       const int u = i / K, w = i % K;
       const int slot = corner_slot(u, w, mf);
       if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
@@ -420,8 +458,6 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
         gyrow[re] = acc.x * co[re];
         gyrow[re + D0 / 2] = acc.y * co[re + D0 / 2];
       }
-      }
-      __syncthreads();
     }
     cluster.sync();
   }
