@@ -215,10 +215,10 @@ def algorithmic_work(dev, phase: str):
     if phase in ("view_fwd", "view_bwd"):
         fft = 2 * 5 * P * P * lg + 6 * P * P                  # forward + inverse padded 2-D FFT, x K^
         spec = 8 * (M * K * K + M * M * K)                     # corner-sparse DFT contraction
-        gs = 8 * M * M * R if phase == "view_fwd" else 0       # data GEMM row
-        return "fp64", S * n * (fft + spec + gs)
+        data = 8 * K * K * R                                   # D = alpha H^T row / g_rows conj(H) (H = G_S o expand)
+        return "fp64", S * n * (fft + spec + data)
     if phase == "pixel":
-        return "hbm", S * (4 * n * M * M * cs + R * M * M * cs)
+        return "hbm", S * 4 * n * M * M * cs                   # J, E read; g_J, g_E written
     layer = {"fwd_l1": (H, D0), "fwd_l2": (H, H), "fwd_l3": (D0, H),
              "bwd_l1": (H, D0), "bwd_l2": (H, H), "bwd_l3": (D0, H)}.get(phase)
     if layer is None:
@@ -269,7 +269,7 @@ def large_leg(args, d: Dist):
                     "final_loss_total": float(tr[-1, 0, 5])})
         peaks = json.load(open(os.path.join(HERE, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(HERE, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-        pr = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), 36.2, peaks["hbm_gbs"])
+        pr = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), 36.2, peaks["hbm_gbs"], m0=4 * dev.mf ** 2)
         pr["frac"] = pr["t_roof_us_per_scene_iter"] * k / (1e6 * secs)
         pr["fp64_peak_note"] = "36.2 TFLOP/s (pdf_fp64_probe on this pool)"
         out["path_roofline"] = pr
@@ -301,15 +301,19 @@ def large_leg(args, d: Dist):
     return out
 
 
-PHASE_KERNEL = {"view_fwd": "view_kernel<double, 4, 0>", "view_bwd": "view_kernel<double, 4, 1>",
-                "pixel": "pixel_kernel<double, 1>", "fwd_l1": "net_fwd_mma_kernel", "fwd_l2": "net_fwd_mma_kernel",
-                "fwd_l3": "net_fwd_mma_kernel", "bwd_l1": "net_bwd_mma_kernel", "bwd_l2": "net_bwd_mma_kernel",
-                "bwd_l3": "net_bwd_mma_kernel"}
+PHASE_KERNEL = {"view_fwd": "view_kernel<double, 4, 0", "view_bwd": "view_kernel<double, 4, 1",
+                "pixel": "pixel_kernel<double, 1>", "fwd_l1": "net_fwd_", "fwd_l2": "net_fwd_",
+                "fwd_l3": "net_fwd_", "bwd_l1": "net_bwd_", "bwd_l2": "net_bwd_", "bwd_l3": "net_bwd_"}
+# network layers share one kernel name: the launches of a layer kernel come in
+# forward (l1, l2, l3) / backward (l3, l2, l1) order
+LAYER_POS = {"fwd_l1": 0, "fwd_l2": 1, "fwd_l3": 2, "bwd_l3": 0, "bwd_l2": 1, "bwd_l1": 2}
 
 
 def ncu_traffic(phase: str):
     """Mean DRAM bytes (read + write) per launch of the phase's kernel from the
-    committed ncu launch list of this bench command (profiles/), else None."""
+    committed ncu launch list of this bench command (profiles/), else None.
+    ncu flushes caches before each launch (cold), and a kernel's writes still
+    in L2 when it ends are not counted."""
     import glob
     import gzip
     import csv
@@ -327,25 +331,35 @@ def ncu_traffic(phase: str):
         per = {}
         for r in rows[hi + 1:]:
             if key in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                per[r[idi]] = per.get(r[idi], 0.0) + float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
-        return {"bytes_per_launch": float(np.mean(list(per.values()))), "launches": len(per),
-                "source": os.path.relpath(files[-1], HERE)} if per else None
+                per[int(r[idi])] = per.get(int(r[idi]), 0.0) + float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        ids = sorted(per)
+        if phase in LAYER_POS:
+            ids = ids[LAYER_POS[phase]::3]
+        vals = [per[i] for i in ids]
+        return {"bytes_per_launch": float(np.mean(vals)), "launches": len(vals),
+                "source": os.path.relpath(files[-1], HERE)} if vals else None
     except Exception:
         return None
 
 
-def path_roofline(M: int, n: int, R: int, np_params: int, fp64_tflops: float, hbm_gbs: float) -> dict:
+def path_roofline(M: int, n: int, R: int, np_params: int, fp64_tflops: float, hbm_gbs: float,
+                  m0: int | None = None) -> dict:
     """SURVEY 8(d) path roofline per scene-iteration, restated for float64:
     F_phys = n [20 P^2 log2 P^2 + 12 P^2 + 10 M^2 log2 M^2 + 16 M^2 R] flop at the
     FP64 peak, B_net = 56 Np bytes (W read forward, W/m/v read + written by the
-    fused backward/Adam) at the HBM peak."""
+    fused backward/Adam) at the HBM peak.  This implementation contracts the
+    data term over the M0 spectral coefficients (H = G_S o expand),
+    so the bound of the work it executes replaces 16 M^2 R by 16 M0 R; `frac`
+    uses that (smaller, stricter) bound, F_phys_reference_flop is SURVEY's."""
     P = 2 * M
-    f = n * (20 * P * P * np.log2(P * P) + 12 * P * P + 10 * M * M * np.log2(M * M) + 16 * M * M * R)
+    base = 20 * P * P * np.log2(P * P) + 12 * P * P + 10 * M * M * np.log2(M * M)
+    f_ref = n * (base + 16 * M * M * R)
+    f = n * (base + 16 * (m0 if m0 else M * M) * R)
     b = 56.0 * np_params
     t_phys = f / (fp64_tflops * 1e12)
     t_net = b / (hbm_gbs * 1e9)
-    return {"F_phys_flop": float(f), "B_net_bytes": b, "t_phys_us": 1e6 * t_phys, "t_net_us": 1e6 * t_net,
-            "t_roof_us_per_scene_iter": 1e6 * (t_phys + t_net)}
+    return {"F_phys_flop": float(f), "F_phys_reference_flop": float(f_ref), "B_net_bytes": b,
+            "t_phys_us": 1e6 * t_phys, "t_net_us": 1e6 * t_net, "t_roof_us_per_scene_iter": 1e6 * (t_phys + t_net)}
 
 
 def run_ours(args, d: Dist):
@@ -429,7 +443,7 @@ def run_ours(args, d: Dist):
         achieved = work / launch_s / 1e12
         roof = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak_tflops, "peak_source": "pdf_fp64_probe DFMA kernel (measured live)"}
-    proof = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), fp64_peak_tflops, peaks["hbm_gbs"])
+    proof = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), fp64_peak_tflops, peaks["hbm_gbs"], m0=4 * dev.mf ** 2)
     proof["frac"] = proof["t_roof_us_per_scene_iter"] / (1e3 * ms_step / k)
     roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom],
                  "traffic": ncu_traffic(dom), "share_of_step": share[dom]})
@@ -484,7 +498,7 @@ def run_ours(args, d: Dist):
         phb = devb.profile_phases(thb, mb, vb, 0, 3)
         devb.check_errors()
         rels = [o.rel_error for o in outb]
-        proof_b = path_roofline(devb.M, devb.n, devb.R, int(devb.n_params), fp64_peak_tflops, peaks["hbm_gbs"])
+        proof_b = path_roofline(devb.M, devb.n, devb.R, int(devb.n_params), fp64_peak_tflops, peaks["hbm_gbs"], m0=4 * devb.mf ** 2)
         proof_b["frac"] = proof_b["t_roof_us_per_scene_iter"] * S * k / (1e6 * tdev)
         batched = {"workload": f"cfg4: {S * d.world} scenes of 1-4 random ellipses (seed = scene index), "
                                f"{S} per GPU, {k} iterations each",
