@@ -142,6 +142,13 @@ int pdf_apply_cco(pdf_ctx* ctx, const void* chi, void* out, int32_t count, doubl
 int pdf_profile_train(pdf_ctx* ctx, void* theta, void* m, void* v, int32_t t0, int32_t iters, float* ms,
                       void* stream);
 int pdf_fp64_probe(double* gflops, void* stream);
+/* timeline of the replayed training graph: pdf_timeline_reset(on = 1) makes the next captured
+ * graph of pdf_train stamp slot = iteration * PDF_NPHASES + phase into its kernels and clears the
+ * stamps (on = 0: off, recapture without; on = 2: clear the stamps only); after one replay pdf_timeline_read copies [PDF_TL_SLOTS][3] globaltimer ns (first CTA
+ * entry, first CTA past the dependency wait, last CTA exit; unused: UINT64_MAX / 0). */
+#define PDF_TL_SLOTS 128
+int pdf_timeline_reset(pdf_ctx* ctx, int32_t on, void* stream);
+int pdf_timeline_read(uint64_t* out_host, void* stream);
 
 /* incidence sharding (one large scene, views split over ranks).
  * The context is created for this rank's views only (desc.n = own views, c_inc / c_sca

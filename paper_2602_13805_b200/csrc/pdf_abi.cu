@@ -21,6 +21,9 @@
 using namespace pdf;
 
 static thread_local std::string g_err;
+// timeline slot (+1) stamped into the hot-loop kernel arguments while a
+// timeline capture is on (pdf_timeline); 0 otherwise
+static thread_local int g_tl_cur = 0, g_tl_iter = 0;
 static int env_int(const char* name, int dflt);
 // programmatic dependent launch for the hot-loop kernels (PDF_PDL=0 disables)
 static const int g_pdl = env_int("PDF_PDL", 1);
@@ -65,6 +68,7 @@ struct pdf_ctx {
   // spectrum chunk, data-GEMM pixel chunking
   int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks, dg_nq;
   int split;         // pixel stage as numden / pixel_a / pixel_b (pdf_shard.cuh) in the training loop
+  int xbwd;          // split network backward in the training loop (net_gh_x / net_adam_x)
   long long Np;
   size_t csz, rsz;   // complex / real element size
   // workspace
@@ -81,6 +85,7 @@ struct pdf_ctx {
   void *g_theta = nullptr, *g_m = nullptr, *g_v = nullptr, *g_trace = nullptr;
   cudaStream_t g_stream = nullptr;
   int g_iters = 0;
+  int tl_on = 0;
 };
 
 template <typename T>
@@ -179,6 +184,9 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // measured slower than the fused pixel kernel (with its DMMA G_S^H) on every
   // config; kept as an option (PDF_SPLIT_PIXEL=1), covered by the sharded tests
   c->split = env_int("PDF_SPLIT_PIXEL", 0) && !d->joint;
+  // latency regime: g_h and g_W + Adam as separate fully parallel launches
+  c->xbwd = env_int("PDF_BWD_X", 1) && d->dtype == PDF_F64 && c->rows <= 16 && c->D0 <= XW * 4 * GX_STEPS &&
+            c->H <= XW * 4 * GX_STEPS && (long long)d->S * (c->H / 8) <= 4 * 148;
   if (c->dgemm) {
     const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
@@ -280,6 +288,7 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
 template <typename T>
 static ViewArgs<T> view_common(pdf_ctx* c) {
   ViewArgs<T> a = {};
+  a.tl = g_tl_cur;
   a.M = c->M; a.mf = c->d.mf; a.R = c->d.R; a.n = c->d.n; a.CS = c->CS;
   a.khat = (const C<T>*)c->khat; a.twP = (const C<T>*)c->twP; a.twM = (const C<T>*)c->twM;
   a.hs = (const C<T>*)c->hs;
@@ -392,6 +401,7 @@ static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
 template <typename T, bool GRAD>
 static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   PixelArgs<T> p = {};
+  p.tl = g_tl_cur;
   p.M = c->M; p.n = c->d.n; p.R = c->d.R; p.CS = c->NPV; p.S = c->d.S;
   p.beta = (T)c->d.beta; p.l1 = (T)c->d.lambda1; p.l2 = (T)c->d.lambda2; p.l3 = (T)c->d.lambda3;
   p.tau = (T)c->d.tau_b;
@@ -516,6 +526,7 @@ template <typename T>
 static int net_fwd_layer(pdf_ctx* c, const T* in, int K, int N, const T* theta, long long woff, long long boff,
                          T* out, int final_layer, int* step, cudaStream_t st) {
   NetFwdArgs<T> a = {};
+  a.tl = g_tl_cur;
   a.rows = c->rows; a.K = K; a.N = N;
   a.in = in; a.in_ss = (long long)c->rows * K;
   a.theta = theta; a.th_ss = c->Np; a.w_off = woff; a.b_off = boff;
@@ -637,6 +648,7 @@ template <typename T>
 static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T* theta, long long woff,
                          long long boff, T* m, T* v, T* grad, int fused, T* gzprev, cudaStream_t st) {
   NetBwdArgs<T> a = {};
+  a.tl = g_tl_cur;
   a.rows = c->rows; a.K = K; a.N = N;
   a.gz = gz; a.gz_ss = (long long)c->rows * N;
   a.hin = hin; a.hin_ss = (long long)c->rows * K;
@@ -722,6 +734,57 @@ static int split_finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st
   return PDF_OK;
 }
 
+// split network backward (latency regime, float64): g_h of layers 3 and 2,
+// then g_W + Adam of all layers in one launch
+static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, int N, const double* theta,
+                      long long woff, double* gzprev, cudaStream_t st) {
+  NetBwdArgs<double> a = {};
+  a.tl = g_tl_cur;
+  a.rows = c->rows; a.K = K; a.N = N;
+  a.gz = gz; a.gz_ss = (long long)c->rows * N;
+  a.hin = hin; a.hin_ss = (long long)c->rows * K;
+  a.theta = const_cast<double*>(theta); a.th_ss = c->Np; a.w_off = woff;
+  a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
+  const int MT = (c->rows + 7) / 8;
+  const dim3 grid((K + 7) / 8, 1, c->d.S);
+  const size_t smem = gh_x_smem_bytes(MT, N);
+  void* args[] = {&a};
+  cudaError_t e = MT == 1 ? plain_launch(net_gh_x_kernel<1>, grid, dim3(XW * 32), smem, st, args)
+                          : plain_launch(net_gh_x_kernel<2>, grid, dim3(XW * 32), smem, st, args);
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net g_h (x): ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
+static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStream_t st) {
+  const long long H = c->H, D0 = c->D0, R = c->rows;
+  const double* gzs[3] = {(const double*)c->gz1, (const double*)c->gz2, (const double*)c->gy};
+  const double* hins[3] = {(const double*)c->x0, (const double*)c->h1, (const double*)c->h2};
+  const long long Ns[3] = {H, H, D0}, Ks[3] = {D0, H, H};
+  const Offs o = offsets(c);
+  const long long wo[3] = {o.w1, o.w2, o.w3}, bo[3] = {o.b1, o.b2, o.b3};
+  NetAdamArgs a = {};
+  a.tl = g_tl_cur;
+  long long items = 0;
+  for (int l = 0; l < 3; ++l) {
+    AdamLayer& L = a.L[l];
+    L.gz = gzs[l]; L.hin = hins[l]; L.gz_ss = R * Ns[l]; L.hin_ss = R * Ks[l];
+    L.w_off = wo[l]; L.b_off = bo[l]; L.N = (int)Ns[l]; L.K = (int)Ks[l];
+    L.strips = (int)((Ks[l] / 8 + AX_ST - 1) / AX_ST);
+    L.w_items = (int)(Ns[l] / 8) * L.strips;
+    L.b_items = (int)((Ns[l] + 31) / 32);
+    items += L.w_items + L.b_items;
+  }
+  a.rows = c->rows; a.theta = theta; a.m = m; a.v = v; a.th_ss = c->Np; a.step = c->step;
+  a.lr = c->d.lr; a.b1 = c->d.adam_b1; a.b2 = c->d.adam_b2; a.eps = c->d.adam_eps; a.err = c->err;
+  const dim3 grid((unsigned)((items + 7) / 8), c->d.S);
+  void* args[] = {&a};
+  const int MT = (c->rows + 7) / 8;
+  cudaError_t e = MT == 1 ? plain_launch(net_adam_x_kernel<1>, grid, dim3(256), 0, st, args)
+                          : plain_launch(net_adam_x_kernel<2>, grid, dim3(256), 0, st, args);
+  if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net adam (x): ") + cudaGetErrorString(e));
+  return PDF_OK;
+}
+
 template <typename T>
 static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, double* bd, double* trace, int fused,
                      cudaStream_t st, cudaEvent_t* ev = nullptr) {
@@ -729,7 +792,11 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   // PDF_SKIP_PHASES (bitmask, measurement experiments only) drops kernels.
   static const int skip = env_int("PDF_SKIP_PHASES", 0);
   int ph = 0;
-  auto mark = [&]() { if (ev) cudaEventRecord(ev[ph], st); ++ph; };
+  auto mark = [&]() {
+    if (ev) cudaEventRecord(ev[ph], st);
+    ++ph;
+    g_tl_cur = c->tl_on && ph <= PDF_NPHASES ? g_tl_iter * PDF_NPHASES + ph : 0;
+  };
   auto run = [&]() { return !(skip >> ph & 1); };
   const Offs o = offsets(c);
   const T* thc = (const T*)theta;
@@ -753,6 +820,20 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   mark();
   if (run() && c->split) TRY(split_finalize(c, bd, trace, st));
   mark();   // finalize is fused into view_bwd unless the pixel stage is split
+  if constexpr (sizeof(T) == 8) {
+    if (fused && c->xbwd) {
+      // split backward: phases bwd_l3 / bwd_l2 = g_h of layers 3 / 2, bwd_l1 = g_W + Adam (all layers)
+      if (run()) TRY(gh_x_layer(c, (const double*)c->gy, (const double*)c->h2, c->H, c->D0, (const double*)theta,
+                                o.w3, (double*)c->gz2, st));
+      mark();
+      if (run()) TRY(gh_x_layer(c, (const double*)c->gz2, (const double*)c->h1, c->H, c->H, (const double*)theta,
+                                o.w2, (double*)c->gz1, st));
+      mark();
+      if (run()) TRY(adam_x_all(c, (double*)theta, (double*)m, (double*)v, st));
+      mark();
+      return PDF_OK;
+    }
+  }
   if (run()) TRY(net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, (T*)m, (T*)v,
                                   (T*)grad, fused, (T*)c->gz2, st));
   mark();
@@ -967,8 +1048,11 @@ static int train_impl(pdf_ctx* c, void* theta, void* m, void* v, int t0, int k, 
     cudaGraph_t g;
     CK_CUDA(cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal));
     int r = PDF_OK;
-    for (int i = 0; i < G && r == PDF_OK; ++i)
+    for (int i = 0; i < G && r == PDF_OK; ++i) {
+      g_tl_iter = i;
       r = iteration<T>(c, theta, m, v, nullptr, nullptr, tr, 1, c->g_stream);
+    }
+    g_tl_cur = 0;
     cudaError_t e = cudaStreamEndCapture(c->g_stream, &g);
     if (r != PDF_OK) return r;
     if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("capture: ") + cudaGetErrorString(e));
@@ -980,6 +1064,30 @@ static int train_impl(pdf_ctx* c, void* theta, void* m, void* v, int t0, int k, 
   int done = 0;
   for (; done + G <= k; done += G) CK_CUDA(cudaGraphLaunch(c->gexec, st));
   for (; done < k; ++done) TRY(iteration<T>(c, theta, m, v, nullptr, nullptr, tr, 1, st));
+  return PDF_OK;
+}
+
+extern "C" int pdf_timeline_reset(pdf_ctx* c, int32_t on, void* stream) {
+  if (!c) return fail(PDF_EINVAL, "null ctx");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (on != 2) {   // 2: clear the stamps only (keep the captured graph)
+    c->tl_on = on ? 1 : 0;
+    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }   // recapture with / without slots
+  }
+  std::vector<unsigned long long> init(PDF_TL_SLOTS * 3);
+  for (int i = 0; i < PDF_TL_SLOTS; ++i) { init[3 * i] = init[3 * i + 1] = ~0ULL; init[3 * i + 2] = 0; }
+  CK_CUDA(cudaMemcpyToSymbolAsync(g_tl, init.data(), init.size() * sizeof(unsigned long long), 0,
+                                  cudaMemcpyHostToDevice, st));
+  CK_CUDA(cudaStreamSynchronize(st));
+  return PDF_OK;
+}
+
+extern "C" int pdf_timeline_read(uint64_t* out, void* stream) {
+  if (!out) return fail(PDF_EINVAL, "null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK_CUDA(cudaMemcpyFromSymbolAsync(out, g_tl, PDF_TL_SLOTS * 3 * sizeof(unsigned long long), 0,
+                                    cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaStreamSynchronize(st));
   return PDF_OK;
 }
 

@@ -66,6 +66,18 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // earlier (weights, Adam moments, operators, constants); pdl_trigger() lets
 // the next kernel start its own prologue.  Both are no-ops without PDL.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// Measurement timeline (pdf_timeline; off unless a launch carries a slot):
+// per slot the first CTA entry, the first CTA past the dependency wait and
+// the last CTA exit, in globaltimer nanoseconds.
+constexpr int TL_SLOTS = 128;   // = PDF_TL_SLOTS (pdf_abi.h)
+__device__ unsigned long long g_tl[TL_SLOTS][3];
+__device__ __forceinline__ void tl_mark(int slot1, int k) {
+  if (slot1 <= 0 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (k < 2) atomicMin(&g_tl[slot1 - 1][k], t); else atomicMax(&g_tl[slot1 - 1][2], t);
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // numerically stable logistic, scipy.special.expit semantics

@@ -45,6 +45,7 @@ struct NetFwdArgs {
   int n, M0, joint;
   int* step;                          // incremented once (train mode) or null
   int w_early;                        // weights final two launches back: prefetch before pdl_wait
+  int tl;                             // timeline slot + 1 (0: off)
 };
 
 template <typename T, int RB> struct FwdShape {
@@ -209,6 +210,7 @@ struct NetBwdArgs {
   T lr, b1, b2, eps;
   T* gzprev; long long gzp_ss;        // [S][rows][K] or null (first layer)
   int* err;                           // [S]
+  int tl;                             // timeline slot + 1 (0: off)
 };
 
 // Adam in the reference's operation order (network.py:252-257).  The bias

@@ -95,10 +95,11 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
   double b[4][NT][4];
   // W1 is written by the launch right before (Adam of the previous
   // iteration); W2, W3 two or more launches back and may stream early
-  if (!a.w_early) pdl_wait();
+  tl_mark(a.tl, 0);
+  if (!a.w_early) { pdl_wait(); tl_mark(a.tl, 1); }
 #pragma unroll
   for (int q = 0; q < 4; ++q) loadB(kb + 16 * q, b[q]);
-  if (a.w_early) pdl_wait();
+  if (a.w_early) { pdl_wait(); tl_mark(a.tl, 1); }
   if (a.step && tid == 0 && blockIdx.x == 0 && rank == 0 && scene == 0) atomicAdd(a.step, 1);
   if (kb < ke) stage(kb, 0);
   int s = 0;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
     const int gn = blockIdx.x * FM_WARPS * NT * 8 + wo;
     if (gn >= N || r >= rows) continue;
     double z = 0.0;
+#pragma unroll 8
     for (int c = 0; c < CK; ++c) z += cluster.map_shared_rank(part, c)[e];
     z += bias[gn];
     if (!a.final_layer) {
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
     }
   }
   cluster.sync();
+  tl_mark(a.tl, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -210,8 +213,10 @@ __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double
         b[q][2 * h + 1] = v.y;
       }
   };
+  tl_mark(a.tl, 0);
   if (a.w_early) loadW();
   pdl_wait();
+  tl_mark(a.tl, 1);
   if (!a.w_early) loadW();
   if (a.step && tid == 0 && blockIdx.x == 0 && scene == 0) atomicAdd(a.step, 1);
   const int seg = K / 2;
@@ -270,6 +275,7 @@ __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double
       if (gn < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
     }
   }
+  tl_mark(a.tl, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -361,12 +367,20 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
     }
   }
   // W, m, v are final since the previous iteration: the first BM_D n-tiles
-  // are requested before the dependency wait
+  // (and this CTA's first bias entries) are requested before the dependency wait
+  const bool bias_lane = blockIdx.x == 0 && tid < BM_NCH;
+  double* thb = FUSED ? a.theta + scene * a.th_ss + a.b_off : nullptr;
+  double* mbb = FUSED ? a.m + scene * a.th_ss + a.b_off : nullptr;
+  double* vbb = FUSED ? a.v + scene * a.th_ss + a.b_off : nullptr;
+  double bp = 0.0, bm = 0.0, bv = 0.0;
+  if (FUSED && bias_lane && nb + tid < ne) { bp = thb[nb + tid]; bm = mbb[nb + tid]; bv = vbb[nb + tid]; }
+  tl_mark(a.tl, 0);
   for (int it = 0; it < BM_D; ++it) {
     if (it < ntl) stage_w(it);
     cp_async_commit();
   }
   pdl_wait();
+  tl_mark(a.tl, 1);
   // h as B fragments of the g_W product: hf[j][s] = h[4s + t][kw0 + 8j + g]
   double hf[KT][RPM / 4];
 #pragma unroll
@@ -396,22 +410,22 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
     const double* G = Gs + (c % NGB) * RPM * BM_GP;
     const double ibc1 = bc_s[0], ibc2 = bc_s[1];
     const int sl = it % BM_D;
-    // bias of chunk c (network.py:213,217), by the first column tile
-    if ((it & 3) == 0 && blockIdx.x == 0 && tid < BM_NCH && nb + c * BM_NCH + tid < ne) {
-      double gb = 0.0;
-      for (int r = 0; r < rows; ++r) gb += G[r * BM_GP + tid];
+    // bias of chunk c (network.py:213,217), by the first column tile; its
+    // p, m, v were loaded one chunk ahead (no global round trip in the loop)
+    if ((it & 3) == 0 && bias_lane) {
       const int gn = nb + c * BM_NCH + tid;
-      if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
-      if constexpr (FUSED) {
-        double* th = a.theta + scene * a.th_ss + a.b_off;
-        double* mb = a.m + scene * a.th_ss + a.b_off;
-        double* vb = a.v + scene * a.th_ss + a.b_off;
-        double p = th[gn], m1 = mb[gn], v1 = vb[gn];
-        adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
-        if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
-        th[gn] = p; mb[gn] = m1; vb[gn] = v1;
-      } else {
-        a.grad[scene * a.th_ss + a.b_off + gn] = gb;
+      if (gn < ne) {
+        double gb = 0.0;
+        for (int r = 0; r < rows; ++r) gb += G[r * BM_GP + tid];
+        if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
+        if constexpr (FUSED) {
+          adam_one<double>(bp, bm, bv, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+          if (!isfinite(bp)) errbits |= ERR_NONFINITE_PARAM;
+          thb[gn] = bp; mbb[gn] = bm; vbb[gn] = bv;
+          if (gn + BM_NCH < ne) { bp = thb[gn + BM_NCH]; bm = mbb[gn + BM_NCH]; bv = vbb[gn + BM_NCH]; }
+        } else {
+          a.grad[scene * a.th_ss + a.b_off + gn] = gb;
+        }
       }
     }
     // g_W: NA independent accumulators break the dependent DMMA chain over the rows
@@ -488,7 +502,8 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
       const int r = e / CW, cl = e % CW, gk = blockIdx.x * CW + cl;
       if (gk >= K) continue;
       double sum = 0.0;
-      for (int q = 0; q < CN; ++q) sum += cluster.map_shared_rank(cpart, q)[e];
+#pragma unroll 8
+      for (int q = 0; q < CN; ++q) sum += cluster.map_shared_rank(cpart, q)[e];   // loads in flight together
       const double hv = hin[(size_t)r * K + gk];
       a.gzprev[scene * a.gzp_ss + (size_t)r * K + gk] = sum * (1.0 - hv * hv);
     }
@@ -496,6 +511,210 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
   } else {
     cp_async_wait<0>();
   }
+  tl_mark(a.tl, 2);
+}
+
+}  // namespace pdf
+
+namespace pdf {
+
+// ---------------------------------------------------------------------------
+// Split network backward for the latency regime (one or a few scenes, <= 16
+// rows, widths <= 1024).  The fused layer kernel above walks n-tiles serially
+// per warp and reduces g_h across a cluster; here the two products of a layer
+// become separate, fully parallel launches:
+//   net_gh_x_kernel   g_h = g_z W_old, g_z' = g_h (1 - h^2)  (network.py:210-212)
+//                     for layers 3 and 2, on the critical path;
+//   net_adam_x_kernel g_W = g_z^T h, g_b = sum_r g_z, Adam in place
+//                     (network.py:201-219, 248-264) for all three layers in
+//                     one launch, every W / m / v fragment requested at once.
+// W_old is read by the g_h launches before the Adam launch rewrites it.
+constexpr int GX_STEPS = 32;            // n-steps of 4 per warp: N <= XW * 4 * GX_STEPS = 1024
+
+__host__ __device__ constexpr size_t gh_x_smem_bytes(int MT, int N) {
+  return ((size_t)8 * MT * (N + 2) + (size_t)XW * 8 * MT * 8) * sizeof(double);
+}
+
+// CTA = one k-tile of 8 outputs of g_h; its XW warps split the n reduction
+template <int MT>
+__global__ void __launch_bounds__(XW * 32, 1) net_gh_x_kernel(NetBwdArgs<double> a) {
+  constexpr int RPM = 8 * MT, THR = XW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int K = a.K, N = a.N, rows = a.rows, GP = N + 2;
+  double* Gz = reinterpret_cast<double*>(smem_raw);   // [RPM][N + 2]
+  double* red = Gz + (size_t)RPM * GP;                 // [XW][RPM][8]
+  const int scene = blockIdx.z;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int k0 = blockIdx.x * 8;
+  const int npw = ((N + XW * 4 - 1) / (XW * 4)) * 4;
+  const int nb = warp * npw, ne = min(N, nb + npw);
+  const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  tl_mark(a.tl, 0);
+  // B fragments (W_old is final since the previous iteration): lane holds W[n + t][k0 + g]
+  double b[GX_STEPS];
+  const bool kok = k0 + g < K;
+#pragma unroll
+  for (int q = 0; q < GX_STEPS; ++q) {
+    const int n = nb + 4 * q + t;
+    b[q] = (kok && n < ne) ? W[(size_t)n * K + k0 + g] : 0.0;
+  }
+  pdl_wait();
+  tl_mark(a.tl, 1);
+  const double* __restrict__ gz = a.gz + scene * a.gz_ss;
+  const int seg = N / 2;
+  for (int i = tid; i < RPM * seg; i += THR) {
+    const int r = i / seg, s2 = i - r * seg;
+    const bool ok = r < rows;
+    cp_async16(Gz + (size_t)r * GP + 2 * s2, ok ? gz + (size_t)r * N + 2 * s2 : gz, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  pdl_trigger();
+  double acc[MT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+  for (int q = 0; q < GX_STEPS; ++q) {
+    const int n = nb + 4 * q;
+    if (n < ne) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double av = n + t < ne ? Gz[(size_t)(8 * i + g) * GP + n + t] : 0.0;
+        dmma(acc[i][0], acc[i][1], av, b[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) red[(warp * RPM + 8 * i + g) * 8 + 2 * t + c] = acc[i][c];
+  __syncthreads();
+  const double* __restrict__ hin = a.hin + scene * a.hin_ss;
+  for (int e = tid; e < RPM * 8; e += THR) {
+    const int r = e >> 3, col = e & 7, k = k0 + col;
+    if (k >= K || r >= rows) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < XW; ++w) s += red[(w * RPM + r) * 8 + col];
+    const double hv = hin[(size_t)r * K + k];
+    a.gzprev[scene * a.gzp_ss + (size_t)r * K + k] = s * (1.0 - hv * hv);
+  }
+  tl_mark(a.tl, 2);
+}
+
+struct AdamLayer {
+  const double* gz;       // [S][rows][N]
+  const double* hin;      // [S][rows][K]
+  long long gz_ss, hin_ss, w_off, b_off;
+  int N, K, strips;       // strips of AX_ST k-tiles per n-tile
+  int w_items, b_items;   // weight items (n-tile x strip) and bias items (32 outputs)
+};
+
+struct NetAdamArgs {
+  AdamLayer L[3];
+  int rows;
+  double* theta; double* m; double* v; long long th_ss;
+  const int* step;
+  double lr, b1, b2, eps;
+  int* err;
+  int tl;
+};
+
+constexpr int AX_ST = 4;   // k-tiles per weight item
+
+// One warp per item; every load of an item is issued before any use.
+template <int MT>
+__global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
+  constexpr int RPM = 8 * MT, NS = RPM / 4;
+  __shared__ double bc_s[2];
+  const int scene = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  int item = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  tl_mark(a.tl, 0);
+  int li = 0;
+  while (li < 3 && item >= a.L[li].w_items + a.L[li].b_items) { item -= a.L[li].w_items + a.L[li].b_items; ++li; }
+  const bool active = li < 3;
+  const AdamLayer& L = a.L[active ? li : 0];
+  const int K = L.K, N = L.N, rows = a.rows;
+  double* __restrict__ th = a.theta + scene * a.th_ss;
+  double* __restrict__ mm = a.m + scene * a.th_ss;
+  double* __restrict__ vv = a.v + scene * a.th_ss;
+  const bool witem = active && item < L.w_items;
+  // weight item: n-tile nt, k-tiles kt0 .. kt0 + AX_ST - 1
+  const int nt = witem ? item / L.strips : 0, kt0 = witem ? (item % L.strips) * AX_ST : 0;
+  const int n = nt * 8 + g;
+  double2 wp[AX_ST], wm[AX_ST], wv[AX_ST];
+  double hb[AX_ST][NS];
+  bool tok[AX_ST];
+  // W, m, v (final since the previous iteration) and h (the forward's) before the wait
+#pragma unroll
+  for (int j = 0; j < AX_ST; ++j) {
+    const int kk = (kt0 + j) * 8 + 2 * t;
+    tok[j] = witem && kk < K;
+    const size_t o = tok[j] ? L.w_off + (size_t)n * K + kk : 0;
+    wp[j] = tok[j] ? *reinterpret_cast<const double2*>(th + o) : make_double2(0.0, 0.0);
+    wm[j] = tok[j] ? *reinterpret_cast<const double2*>(mm + o) : make_double2(0.0, 0.0);
+    wv[j] = tok[j] ? *reinterpret_cast<const double2*>(vv + o) : make_double2(0.0, 0.0);
+    const int kb = (kt0 + j) * 8 + g;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int r = 4 * s + t;
+      hb[j][s] = (witem && r < rows && kb < K) ? L.hin[scene * L.hin_ss + (size_t)r * K + kb] : 0.0;
+    }
+  }
+  if (tid == 0) {
+    const double tt = (double)*a.step;
+    bc_s[0] = 1.0 / (1.0 - pow(a.b1, tt));
+    bc_s[1] = 1.0 / (1.0 - pow(a.b2, tt));
+  }
+  pdl_wait();
+  tl_mark(a.tl, 1);
+  __syncthreads();
+  const double ibc1 = bc_s[0], ibc2 = bc_s[1];
+  int errbits = 0;
+  if (witem) {
+    const double* gz = L.gz + scene * L.gz_ss;
+    double ga[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int r = 4 * s + t;
+      ga[s] = r < rows ? gz[(size_t)r * N + n] : 0.0;   // A[g][t] = g_z[4s + t][n0 + g]
+    }
+#pragma unroll
+    for (int j = 0; j < AX_ST; ++j) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) dmma(d0, d1, ga[s], hb[j][s]);
+      if (!tok[j]) continue;
+      if (!isfinite(d0) || !isfinite(d1)) errbits |= ERR_NONFINITE_GRAD;
+      adam_one<double>(wp[j].x, wm[j].x, wv[j].x, d0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+      adam_one<double>(wp[j].y, wm[j].y, wv[j].y, d1, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+      if (!isfinite(wp[j].x) || !isfinite(wp[j].y)) errbits |= ERR_NONFINITE_PARAM;
+      const size_t o = L.w_off + (size_t)n * K + (kt0 + j) * 8 + 2 * t;
+      *reinterpret_cast<double2*>(th + o) = wp[j];
+      *reinterpret_cast<double2*>(mm + o) = wm[j];
+      *reinterpret_cast<double2*>(vv + o) = wv[j];
+    }
+  } else if (active) {
+    // bias item: outputs 32 * item + lane (network.py:213,217)
+    const int bn = (item - L.w_items) * 32 + lane;
+    if (bn < N) {
+      const double* gz = L.gz + scene * L.gz_ss;
+      double gb = 0.0;
+      for (int r = 0; r < rows; ++r) gb += gz[(size_t)r * N + bn];
+      if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
+      const size_t o = L.b_off + bn;
+      double p = th[o], m1 = mm[o], v1 = vv[o];
+      adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+      if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
+      th[o] = p; mm[o] = m1; vv[o] = v1;
+    }
+  }
+  if (errbits) atomicOr(&a.err[scene], errbits);
+  tl_mark(a.tl, 2);
 }
 
 }  // namespace pdf

@@ -40,6 +40,7 @@ struct PixelArgs {
   double* part;         // [S][ntiles][4]  state, bound, tv, bridge
   C<T>* chi_out;        // [S][M][M] or null
   int* err;             // [S]
+  int tl;               // timeline slot + 1 (0: off)
 };
 
 constexpr double EPS_TV = 1e-12;   // losses.py:29
@@ -76,7 +77,9 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   const size_t img = (size_t)M * M;
   const size_t vbase = (size_t)scene * n;
 
+  tl_mark(a.tl, 0);
   pdl_wait();   // J, E, norms come from the previous kernel
+  tl_mark(a.tl, 1);
 
   if (warp == 0) {
     const double mx = warp_max_view_power(a.norms + vbase * a.CS, n, a.CS);
@@ -255,6 +258,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     const int tile = y * tilesx + blockIdx.x;
     a.part[((size_t)scene * (tilesx * M) + tile) * 4 + tid] = s;
   }
+  tl_mark(a.tl, 2);
 }
 
 // breakdown per scene: [state, data, bound, tv, bridge, total] (losses.py:36-49)

@@ -65,6 +65,7 @@ struct ViewArgs {
   const C<T>* x;
   C<T>* y;
   int conj_in, conj_out;
+  int tl;             // timeline slot + 1 (0: off)
 };
 
 template <typename T>
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   ltw.load(s.tw, lane);
   // constants: my K^ columns (and E_inc rows) stream in while the previous
   // kernel drains
+  tl_mark(a.tl, 0);
   const size_t img = (size_t)M * M;
   constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
   if constexpr (PRE && MODE != VIEW_APPLY) {
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
   }
   pdl_wait();   // everything below reads the previous kernel's outputs
+  tl_mark(a.tl, 1);
 
   // ---------------- stage 0: my input rows -> s.rows ----------------------
   if constexpr (MODE == VIEW_FWD) {
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
     cluster.sync();
   }
+  tl_mark(a.tl, 2);
 }
 
 }  // namespace pdf

@@ -192,6 +192,29 @@ class DeviceProblem:
                                            _stream()))
         return {name: float(ms[i]) for i, name in enumerate(N.PHASES)}
 
+    def timeline(self, theta, m, v, t0: int = 0) -> list:
+        """One replay of the 10-iteration training graph with per-kernel
+        globaltimer stamps: [(iteration, phase, entry_ns, waited_ns, exit_ns)]
+        relative to the first entry (measurement only)."""
+        st = _stream()
+        N.check(self.lib.pdf_timeline_reset(self.ctx, 1, st))
+        self.train(theta, m, v, t0, 10)          # capture with slots + one replay
+        torch.cuda.synchronize()
+        N.check(self.lib.pdf_timeline_reset(self.ctx, 2, st))   # clear the stamps, keep the graph
+        self.train(theta, m, v, t0 + 10, 10)
+        torch.cuda.synchronize()
+        buf = (ct.c_uint64 * (128 * 3))()
+        N.check(self.lib.pdf_timeline_read(buf, st))
+        N.check(self.lib.pdf_timeline_reset(self.ctx, 0, st))
+        rows = []
+        for sl in range(128):
+            e, w, x = buf[3 * sl], buf[3 * sl + 1], buf[3 * sl + 2]
+            if x == 0:
+                continue
+            rows.append((sl // len(N.PHASES), sl % len(N.PHASES), e, w, x))
+        t0ns = min(r[2] for r in rows) if rows else 0
+        return [(i, N.PHASES[p], e - t0ns, w - t0ns, x - t0ns) for i, p, e, w, x in rows]
+
     # ------------------------------------------------------------------ primitives
     def apply_gd(self, x: torch.Tensor, adjoint: bool = False) -> torch.Tensor:
         x = x.to(self.cdt).contiguous()
