@@ -757,11 +757,13 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
 
 static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStream_t st) {
   const long long H = c->H, D0 = c->D0, R = c->rows;
-  const double* gzs[3] = {(const double*)c->gz1, (const double*)c->gz2, (const double*)c->gy};
-  const double* hins[3] = {(const double*)c->x0, (const double*)c->h1, (const double*)c->h2};
-  const long long Ns[3] = {H, H, D0}, Ks[3] = {D0, H, H};
   const Offs o = offsets(c);
-  const long long wo[3] = {o.w1, o.w2, o.w3}, bo[3] = {o.b1, o.b2, o.b3};
+  // launch order: layer 3 (g_z = g_y, three launches old), layer 2 (g_z2 from
+  // the g_h launch two back), layer 1 (g_z1 from the launch right before: waits)
+  const double* gzs[3] = {(const double*)c->gy, (const double*)c->gz2, (const double*)c->gz1};
+  const double* hins[3] = {(const double*)c->h2, (const double*)c->h1, (const double*)c->x0};
+  const long long Ns[3] = {D0, H, H}, Ks[3] = {H, H, D0};
+  const long long wo[3] = {o.w3, o.w2, o.w1}, bo[3] = {o.b3, o.b2, o.b1};
   NetAdamArgs a = {};
   a.tl = g_tl_cur;
   long long items = 0;
@@ -769,14 +771,15 @@ static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStrea
     AdamLayer& L = a.L[l];
     L.gz = gzs[l]; L.hin = hins[l]; L.gz_ss = R * Ns[l]; L.hin_ss = R * Ks[l];
     L.w_off = wo[l]; L.b_off = bo[l]; L.N = (int)Ns[l]; L.K = (int)Ks[l];
-    L.strips = (int)((Ks[l] / 8 + AX_ST - 1) / AX_ST);
-    L.w_items = (int)(Ns[l] / 8) * L.strips;
-    L.b_items = (int)((Ns[l] + 31) / 32);
-    items += L.w_items + L.b_items;
+    L.nblk = (int)((Ns[l] + AX_NB - 1) / AX_NB);
+    L.strips = (int)((Ks[l] + AX_ST * 8 - 1) / (AX_ST * 8));
+    L.items = L.nblk * L.strips + (int)((Ns[l] + 255) / 256);
+    L.wait = l == 2;
+    items += L.items;
   }
   a.rows = c->rows; a.theta = theta; a.m = m; a.v = v; a.th_ss = c->Np; a.step = c->step;
   a.lr = c->d.lr; a.b1 = c->d.adam_b1; a.b2 = c->d.adam_b2; a.eps = c->d.adam_eps; a.err = c->err;
-  const dim3 grid((unsigned)((items + 7) / 8), c->d.S);
+  const dim3 grid((unsigned)items, c->d.S);
   void* args[] = {&a};
   const int MT = (c->rows + 7) / 8;
   cudaError_t e = MT == 1 ? plain_launch(net_adam_x_kernel<1>, grid, dim3(256), 0, st, args)

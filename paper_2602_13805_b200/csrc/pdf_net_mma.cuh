@@ -608,12 +608,14 @@ struct AdamLayer {
   const double* gz;       // [S][rows][N]
   const double* hin;      // [S][rows][K]
   long long gz_ss, hin_ss, w_off, b_off;
-  int N, K, strips;       // strips of AX_ST k-tiles per n-tile
-  int w_items, b_items;   // weight items (n-tile x strip) and bias items (32 outputs)
+  int N, K;
+  int nblk, strips;       // 64-output n-blocks x 32-input k-strips (one CTA each)
+  int items;              // nblk * strips weight CTAs + bias CTAs (256 outputs each)
+  int wait;               // g_z written by the launch right before: wait for it
 };
 
 struct NetAdamArgs {
-  AdamLayer L[3];
+  AdamLayer L[3];         // in launch order (layers whose g_z is older first)
   int rows;
   double* theta; double* m; double* v; long long th_ss;
   const int* step;
@@ -622,93 +624,101 @@ struct NetAdamArgs {
   int tl;
 };
 
-constexpr int AX_ST = 4;   // k-tiles per weight item
+constexpr int AX_ST = 4;          // k-tiles per strip (32 inputs)
+constexpr int AX_NB = XW * 8;     // outputs per n-block (one n-tile per warp)
 
-// One warp per item; every load of an item is issued before any use.
+// CTA = (n-block, k-strip) of one layer: warp w updates n-tile w of the
+// block over the strip's four k-tiles.  W, m, v fragments go to registers,
+// the strip's h columns and the block's g_z columns to shared memory, all
+// requested at once; layers whose g_z is two or more launches old do not
+// wait for the previous kernel at all.
 template <int MT>
 __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
   constexpr int RPM = 8 * MT, NS = RPM / 4;
+  constexpr int HP = AX_ST * 8 + 2, GP = AX_NB + 2;   // pitches (conflict-free fragment reads)
+  __shared__ __align__(16) double hS[RPM * HP];
+  __shared__ __align__(16) double gS[RPM * GP];
   __shared__ double bc_s[2];
   const int scene = blockIdx.y;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  int item = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
   tl_mark(a.tl, 0);
-  int li = 0;
-  while (li < 3 && item >= a.L[li].w_items + a.L[li].b_items) { item -= a.L[li].w_items + a.L[li].b_items; ++li; }
-  const bool active = li < 3;
-  const AdamLayer& L = a.L[active ? li : 0];
+  int item = blockIdx.x, li = 0;
+  while (li < 2 && item >= a.L[li].items) { item -= a.L[li].items; ++li; }
+  const AdamLayer L = a.L[li];
   const int K = L.K, N = L.N, rows = a.rows;
   double* __restrict__ th = a.theta + scene * a.th_ss;
   double* __restrict__ mm = a.m + scene * a.th_ss;
   double* __restrict__ vv = a.v + scene * a.th_ss;
-  const bool witem = active && item < L.w_items;
-  // weight item: n-tile nt, k-tiles kt0 .. kt0 + AX_ST - 1
-  const int nt = witem ? item / L.strips : 0, kt0 = witem ? (item % L.strips) * AX_ST : 0;
-  const int n = nt * 8 + g;
-  double2 wp[AX_ST], wm[AX_ST], wv[AX_ST];
-  double hb[AX_ST][NS];
-  bool tok[AX_ST];
-  // W, m, v (final since the previous iteration) and h (the forward's) before the wait
-#pragma unroll
-  for (int j = 0; j < AX_ST; ++j) {
-    const int kk = (kt0 + j) * 8 + 2 * t;
-    tok[j] = witem && kk < K;
-    const size_t o = tok[j] ? L.w_off + (size_t)n * K + kk : 0;
-    wp[j] = tok[j] ? *reinterpret_cast<const double2*>(th + o) : make_double2(0.0, 0.0);
-    wm[j] = tok[j] ? *reinterpret_cast<const double2*>(mm + o) : make_double2(0.0, 0.0);
-    wv[j] = tok[j] ? *reinterpret_cast<const double2*>(vv + o) : make_double2(0.0, 0.0);
-    const int kb = (kt0 + j) * 8 + g;
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const int r = 4 * s + t;
-      hb[j][s] = (witem && r < rows && kb < K) ? L.hin[scene * L.hin_ss + (size_t)r * K + kb] : 0.0;
-    }
-  }
+  const double* __restrict__ gz = L.gz + scene * L.gz_ss;
   if (tid == 0) {
     const double tt = (double)*a.step;
     bc_s[0] = 1.0 / (1.0 - pow(a.b1, tt));
     bc_s[1] = 1.0 / (1.0 - pow(a.b2, tt));
   }
-  pdl_wait();
-  tl_mark(a.tl, 1);
-  __syncthreads();
-  const double ibc1 = bc_s[0], ibc2 = bc_s[1];
   int errbits = 0;
-  if (witem) {
-    const double* gz = L.gz + scene * L.gz_ss;
+  const int wc = L.nblk * L.strips;
+  if (item < wc) {
+    const int nb = item / L.strips, k0 = (item % L.strips) * AX_ST * 8;
+    const int n = nb * AX_NB + warp * 8 + g;
+    // W, m, v (final since the previous iteration) and the strip's h (the forward's)
+    double2 wp[AX_ST], wm[AX_ST], wv[AX_ST];
+    bool tok[AX_ST];
+#pragma unroll
+    for (int j = 0; j < AX_ST; ++j) {
+      const int kk = k0 + j * 8 + 2 * t;
+      tok[j] = n < N && kk < K;
+      const size_t o = tok[j] ? L.w_off + (size_t)n * K + kk : 0;
+      wp[j] = tok[j] ? *reinterpret_cast<const double2*>(th + o) : make_double2(0.0, 0.0);
+      wm[j] = tok[j] ? *reinterpret_cast<const double2*>(mm + o) : make_double2(0.0, 0.0);
+      wv[j] = tok[j] ? *reinterpret_cast<const double2*>(vv + o) : make_double2(0.0, 0.0);
+    }
+    const double* hin = L.hin + scene * L.hin_ss;
+    for (int i = tid; i < RPM * AX_ST * 4; i += blockDim.x) {     // 16-byte pieces: [r][16]
+      const int r = i / (AX_ST * 4), sg = i % (AX_ST * 4), kk = k0 + 2 * sg;
+      const bool ok = r < rows && kk < K;
+      cp_async16(hS + r * HP + 2 * sg, ok ? hin + (size_t)r * K + kk : hin, ok);
+    }
+    if (L.wait) { pdl_wait(); tl_mark(a.tl, 1); }
+    for (int i = tid; i < RPM * AX_NB / 2; i += blockDim.x) {
+      const int r = i / (AX_NB / 2), sg = i % (AX_NB / 2), nn = nb * AX_NB + 2 * sg;
+      const bool ok = r < rows && nn < N;
+      cp_async16(gS + r * GP + 2 * sg, ok ? gz + (size_t)r * N + nn : gz, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const double ibc1 = bc_s[0], ibc2 = bc_s[1];
     double ga[NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const int r = 4 * s + t;
-      ga[s] = r < rows ? gz[(size_t)r * N + n] : 0.0;   // A[g][t] = g_z[4s + t][n0 + g]
-    }
+    for (int s = 0; s < NS; ++s) ga[s] = gS[(4 * s + t) * GP + warp * 8 + g];   // A[g][t] = g_z[4s + t][n]
 #pragma unroll
     for (int j = 0; j < AX_ST; ++j) {
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int s = 0; s < NS; ++s) dmma(d0, d1, ga[s], hb[j][s]);
+      for (int s = 0; s < NS; ++s) dmma(d0, d1, ga[s], hS[(4 * s + t) * HP + j * 8 + g]);   // B[t][g] = h[4s + t][k]
       if (!tok[j]) continue;
       if (!isfinite(d0) || !isfinite(d1)) errbits |= ERR_NONFINITE_GRAD;
       adam_one<double>(wp[j].x, wm[j].x, wv[j].x, d0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
       adam_one<double>(wp[j].y, wm[j].y, wv[j].y, d1, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
       if (!isfinite(wp[j].x) || !isfinite(wp[j].y)) errbits |= ERR_NONFINITE_PARAM;
-      const size_t o = L.w_off + (size_t)n * K + (kt0 + j) * 8 + 2 * t;
+      const size_t o = L.w_off + (size_t)n * K + k0 + j * 8 + 2 * t;
       *reinterpret_cast<double2*>(th + o) = wp[j];
       *reinterpret_cast<double2*>(mm + o) = wm[j];
       *reinterpret_cast<double2*>(vv + o) = wv[j];
     }
-  } else if (active) {
-    // bias item: outputs 32 * item + lane (network.py:213,217)
-    const int bn = (item - L.w_items) * 32 + lane;
+  } else {
+    // bias CTA: outputs 256 * (item - wc) + tid (network.py:213,217)
+    const int bn = (item - wc) * 256 + tid;
+    const size_t o = L.b_off + (bn < N ? bn : 0);
+    double p = th[o], m1 = mm[o], v1 = vv[o];
+    if (L.wait) { pdl_wait(); tl_mark(a.tl, 1); }
+    __syncthreads();
     if (bn < N) {
-      const double* gz = L.gz + scene * L.gz_ss;
       double gb = 0.0;
       for (int r = 0; r < rows; ++r) gb += gz[(size_t)r * N + bn];
       if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
-      const size_t o = L.b_off + bn;
-      double p = th[o], m1 = mm[o], v1 = vv[o];
-      adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+      adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, bc_s[0], bc_s[1]);
       if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
       th[o] = p; mm[o] = m1; vv[o] = v1;
     }
