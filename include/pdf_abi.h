@@ -145,7 +145,8 @@ int pdf_fp64_probe(double* gflops, void* stream);
 /* timeline of the replayed training graph: pdf_timeline_reset(on = 1) makes the next captured
  * graph of pdf_train stamp slot = iteration * PDF_NPHASES + phase into its kernels and clears the
  * stamps (on = 0: off, recapture without; on = 2: clear the stamps only); after one replay pdf_timeline_read copies [PDF_TL_SLOTS][3] globaltimer ns (first CTA
- * entry, first CTA past the dependency wait, last CTA exit; unused: UINT64_MAX / 0). */
+ * entry, first CTA past the dependency wait, last CTA exit; unused: UINT64_MAX / 0) followed by
+ * [PDF_TL_SLOTS][8] in-kernel stage stamps (last CTA reaching each stage; 0 = none). */
 #define PDF_TL_SLOTS 128
 int pdf_timeline_reset(pdf_ctx* ctx, int32_t on, void* stream);
 int pdf_timeline_read(uint64_t* out_host, void* stream);

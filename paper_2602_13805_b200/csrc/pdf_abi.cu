@@ -266,8 +266,11 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
   const size_t smem = view_smem_bytes<T>(c->M, c->d.mf, c->d.R, c->CS);
   void* args[] = {&a};
   cudaError_t e;
+  // 8 warps: 16-warp CTAs halve the column pass but need a whole SM's
+  // registers, so under PDL they wait for the previous kernel to drain
+  // (measured +8 us per view kernel at cfg2)
   static const int vt = env_int("PDF_VIEW_THREADS", 256);
-  const int nthr = std::min(vt, 256);
+  const int nthr = std::min(vt, VIEW_MAX_THREADS);
   dim3 grid(c->CS, count), block(nthr), cl(c->CS, 1, 1);
   switch (c->E * 100 + c->CS) {
 #define VCASE(EE, CC)                                               \
@@ -1081,6 +1084,9 @@ extern "C" int pdf_timeline_reset(pdf_ctx* c, int32_t on, void* stream) {
   for (int i = 0; i < PDF_TL_SLOTS; ++i) { init[3 * i] = init[3 * i + 1] = ~0ULL; init[3 * i + 2] = 0; }
   CK_CUDA(cudaMemcpyToSymbolAsync(g_tl, init.data(), init.size() * sizeof(unsigned long long), 0,
                                   cudaMemcpyHostToDevice, st));
+  std::vector<unsigned long long> zs(PDF_TL_SLOTS * TL_STAGES, 0ULL);
+  CK_CUDA(cudaMemcpyToSymbolAsync(g_tls, zs.data(), zs.size() * sizeof(unsigned long long), 0,
+                                  cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaStreamSynchronize(st));
   return PDF_OK;
 }
@@ -1089,6 +1095,9 @@ extern "C" int pdf_timeline_read(uint64_t* out, void* stream) {
   if (!out) return fail(PDF_EINVAL, "null output");
   cudaStream_t st = (cudaStream_t)stream;
   CK_CUDA(cudaMemcpyFromSymbolAsync(out, g_tl, PDF_TL_SLOTS * 3 * sizeof(unsigned long long), 0,
+                                    cudaMemcpyDeviceToHost, st));
+  CK_CUDA(cudaMemcpyFromSymbolAsync(out + PDF_TL_SLOTS * 3, g_tls,
+                                    PDF_TL_SLOTS * TL_STAGES * sizeof(unsigned long long), 0,
                                     cudaMemcpyDeviceToHost, st));
   CK_CUDA(cudaStreamSynchronize(st));
   return PDF_OK;

@@ -78,6 +78,15 @@ __device__ __forceinline__ void tl_mark(int slot1, int k) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   if (k < 2) atomicMin(&g_tl[slot1 - 1][k], t); else atomicMax(&g_tl[slot1 - 1][2], t);
 }
+// stage stamps inside a kernel: the last CTA to reach stage k (measurement)
+constexpr int TL_STAGES = 8;
+__device__ unsigned long long g_tls[TL_SLOTS][TL_STAGES];
+__device__ __forceinline__ void tl_stage(int slot1, int k) {
+  if (slot1 <= 0 || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  atomicMax(&g_tls[slot1 - 1][k], t);
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 // numerically stable logistic, scipy.special.expit semantics

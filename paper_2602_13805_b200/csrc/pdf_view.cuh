@@ -68,6 +68,8 @@ struct ViewArgs {
   int tl;             // timeline slot + 1 (0: off)
 };
 
+constexpr int VIEW_MAX_THREADS = 256;
+
 template <typename T>
 struct ViewSmem {
   C<T>* tw;     // P
@@ -92,7 +94,7 @@ __host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) 
   // K^ columns and the E_inc / g_J-local rows; 4-CTA clusters (batches) keep
   // two CTAs per SM and read them from L2 in place
   const size_t stage = CS == 8 ? (size_t)(P / CS) * P + (size_t)rp * M : 0;
-  size_t pre = stage + (size_t)32 * 8 + (size_t)M0 / CS + 1;
+  size_t pre = stage + (size_t)32 * (VIEW_MAX_THREADS / 32) + (size_t)M0 / CS + 1;
   size_t n = (size_t)P + M + (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M + a + pre + xch;
   return n * sizeof(C<T>) + 64 * sizeof(double);
 }
@@ -117,7 +119,7 @@ __device__ inline double block_sum_d(double v, double* red) {
 }
 
 template <typename T, int E, int MODE, int CSZ>
-__global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
+__global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int P = 32 * E;
   cg::cluster_group cluster = cg::this_cluster();
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   constexpr bool PRE = CS == 8;   // staged constants (view_smem_bytes)
   s.khs = p; p += PRE ? (size_t)cp * P : 0;
   s.pre = p; p += PRE ? (size_t)rp * M : 0;
-  s.dsum = p; p += (size_t)32 * 8 + M0 / CS + 1;
+  s.dsum = p; p += (size_t)32 * (VIEW_MAX_THREADS / 32) + M0 / CS + 1;
   C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)M0 ? (size_t)CS * a.R : (size_t)M0);
   double* red = reinterpret_cast<double*>(p);
 
@@ -264,6 +266,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     __syncthreads();
   }
 
+  tl_stage(a.tl, 0);
   // ---------------- stage A: row FFTs, scatter to column owners ------------
   for (int yl = warp; yl < rp; yl += nw) {
     C<T> x[E];
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   // Split cluster barrier: the arrive releases my stage-A scatter; the data
   // term (receivers rank, rank + CS, ...; H rows from L2) then runs while the
   // other CTAs finish theirs, and the wait acquires everyone's scatter.
+  tl_stage(a.tl, 1);
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (MODE == VIEW_FWD && a.do_data) {
     // D[r] = sum_m alpha[m] H[r][m] - d[r] (masked), g_rows = 2 D mask / c_sca
@@ -324,6 +328,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
   __syncthreads();
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
+  tl_stage(a.tl, 2);
   // ---------------- stage B: columns: FFT, x K^, inverse FFT ---------------
   for (int cc = warp; cc < cp; cc += nw) {
     const int posc = rank * cp + cc;
@@ -353,6 +358,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
       rb[(size_t)yl * Pp + posc] = x[k];
     }
   }
+  tl_stage(a.tl, 3);
   cluster.sync();   // also publishes the data partials (written before this arrive) to rank 0
 
   if (MODE == VIEW_FWD && a.do_data && rank == 0 && tid == 0) {
@@ -361,6 +367,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     a.dloss[v] = t;
   }
 
+  tl_stage(a.tl, 4);
   // ---------------- stage C: inverse row FFTs, crop ------------------------
   double nrm = 0.0;
   for (int yl = warp; yl < rp; yl += nw) {
@@ -388,6 +395,7 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
     }
   }
 
+  tl_stage(a.tl, 5);
   pdl_trigger();
   if constexpr (MODE == VIEW_FWD) {
     double tot = block_sum_d<T>(nrm, red);
@@ -438,7 +446,9 @@ __global__ void __launch_bounds__(256) view_kernel(ViewArgs<T> a) {
         mine[i] = acc;
       }
     }
+    tl_stage(a.tl, 6);
     cluster.sync();
+    tl_stage(a.tl, 7);
     const T inv = T(1) / (T(M) * T(M));
     for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {
       C<T> acc = czero<T>();

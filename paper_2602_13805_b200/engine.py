@@ -203,7 +203,7 @@ class DeviceProblem:
         N.check(self.lib.pdf_timeline_reset(self.ctx, 2, st))   # clear the stamps, keep the graph
         self.train(theta, m, v, t0 + 10, 10)
         torch.cuda.synchronize()
-        buf = (ct.c_uint64 * (128 * 3))()
+        buf = (ct.c_uint64 * (128 * 3 + 128 * 8))()
         N.check(self.lib.pdf_timeline_read(buf, st))
         N.check(self.lib.pdf_timeline_reset(self.ctx, 0, st))
         rows = []
@@ -211,9 +211,11 @@ class DeviceProblem:
             e, w, x = buf[3 * sl], buf[3 * sl + 1], buf[3 * sl + 2]
             if x == 0:
                 continue
-            rows.append((sl // len(N.PHASES), sl % len(N.PHASES), e, w, x))
+            stages = [buf[384 + 8 * sl + k] for k in range(8)]
+            rows.append((sl // len(N.PHASES), sl % len(N.PHASES), e, w, x, stages))
         t0ns = min(r[2] for r in rows) if rows else 0
-        return [(i, N.PHASES[p], e - t0ns, w - t0ns, x - t0ns) for i, p, e, w, x in rows]
+        return [(i, N.PHASES[p], e - t0ns, w - t0ns, x - t0ns, [s - t0ns if s else None for s in st_])
+                for i, p, e, w, x, st_ in rows]
 
     # ------------------------------------------------------------------ primitives
     def apply_gd(self, x: torch.Tensor, adjoint: bool = False) -> torch.Tensor:

@@ -44,16 +44,18 @@ def main():
     rows = dev.timeline(th, m, v, 20)
     dev.check_errors()
     it0 = {}
-    for i, p, e, w, x in rows:
+    for i, p, e, w, x, _ in rows:
         it0.setdefault(i, e)
-    per = {}
+    per, stg = {}, {}
     prev_exit = {}
-    for i, p, e, w, x in sorted(rows, key=lambda r: (r[0], r[2])):
+    for i, p, e, w, x, st in sorted(rows, key=lambda r: (r[0], r[2])):
         if 2 <= i <= 9:
             base = it0[i]
             gap = (w - prev_exit[i]) if i in prev_exit else float("nan")
             per.setdefault(p, []).append(((e - base) / 1e3, (w - base) / 1e3, (x - base) / 1e3, gap / 1e3,
                                           (x - w) / 1e3))
+            if any(s is not None for s in st):
+                stg.setdefault(p, []).append([(s - w) / 1e3 if s is not None else np.nan for s in st])
         prev_exit[i] = x
     iters = sorted(it0)
     period = np.diff([it0[i] for i in iters]).mean() / 1e3 if len(iters) > 1 else float("nan")
@@ -64,6 +66,9 @@ def main():
         mv = np.nanmean(np.array(vals), axis=0)
         print(f"{p:9s} {mv[0]:8.2f} {mv[1]:8.2f} {mv[2]:8.2f} {mv[3]:14.2f} {mv[4]:12.2f}")
         out[p] = [round(float(x), 2) for x in mv]
+    for p, vals in stg.items():
+        mv = np.nanmean(np.array(vals, dtype=float), axis=0)
+        print(f"{p:9s} stages (us after the wait release, last CTA): " + " ".join(f"{v:6.2f}" for v in mv))
     print(json.dumps(out))
 
 
