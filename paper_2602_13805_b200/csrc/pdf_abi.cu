@@ -76,6 +76,8 @@ struct pdf_ctx {
   void *x0, *cout, *h1, *h2, *gy, *gz2, *gz1, *ab;
   double *norms, *dloss, *part, *bd, *pix;
   void *spec, *gpart, *dpart;
+  double* ghp;       // split backward: g_h slice partials [S][GH_NSL][rows][H]
+  int* ticket;       // split backward: per k-block tickets [S][H / 64 + 1]
   double *red1, *red2;   // split pixel stage scratch (local reductions)
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
@@ -122,6 +124,8 @@ static void plan(pdf_ctx* c, Ws& w) {
     c->spec = c->gpart = nullptr;
   }
   c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
+  c->ghp = c->xbwd ? w.take<double>((size_t)d.S * GH_NSL * c->rows * c->H) : nullptr;
+  c->ticket = c->xbwd ? w.take<int>((size_t)d.S * (c->H / GT_KB + 1)) : nullptr;
   c->red1 = c->split ? w.take<double>((size_t)d.S * (3 * img + 1)) : nullptr;
   c->red2 = c->split ? w.take<double>((size_t)d.S * (2 * img + 2)) : nullptr;
   c->dloss = w.take<double>(SN);
@@ -185,8 +189,9 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // config; kept as an option (PDF_SPLIT_PIXEL=1), covered by the sharded tests
   c->split = env_int("PDF_SPLIT_PIXEL", 0) && !d->joint;
   // latency regime: g_h and g_W + Adam as separate fully parallel launches
-  c->xbwd = env_int("PDF_BWD_X", 1) && d->dtype == PDF_F64 && c->rows <= 16 && c->D0 <= XW * 4 * GX_STEPS &&
-            c->H <= XW * 4 * GX_STEPS && (long long)d->S * (c->H / 8) <= 4 * 148;
+  // (measured: cfg2 -4 us, cfg3 167 -> 150 us per iteration, cfg5 unchanged)
+  c->xbwd = env_int("PDF_BWD_X", 1) && d->dtype == PDF_F64 && c->rows <= 80 &&
+            (long long)d->S * (c->H / 8) <= 4 * 148;
   if (c->dgemm) {
     const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
@@ -739,8 +744,48 @@ static int split_finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st
 
 // split network backward (latency regime, float64): g_h of layers 3 and 2,
 // then g_W + Adam of all layers in one launch
+template <int MT>
+static cudaError_t gh_t_launch(dim3 grid, GhArgs& a, cudaStream_t st) {
+  const size_t smem = gh_t_smem_bytes(MT);
+  void* args[] = {&a};
+  return plain_launch(net_gh_t_kernel<MT>, grid, dim3(XW * 32), smem, st, args);
+}
+
 static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, int N, const double* theta,
                       long long woff, double* gzprev, cudaStream_t st) {
+  const int MT = (c->rows + 7) / 8;
+  if (MT > 2 || N > XW * 4 * GX_STEPS) {
+    // tiled: all rows x 64 outputs per CTA, n split into slices (~2 CTAs per SM)
+    GhArgs g = {};
+    g.tl = g_tl_cur;
+    g.rows = c->rows; g.K = K; g.N = N;
+    const int kbs = (K + GT_KB - 1) / GT_KB;
+    int nsl = 1;
+    while (nsl < GH_NSL && (long long)kbs * nsl * c->d.S < 2 * 148 && N / (2 * nsl) >= 2 * GT_NC) nsl *= 2;
+    g.nsl = nsl;
+    g.ns = ((N + nsl - 1) / nsl + GT_NC - 1) / GT_NC * GT_NC;
+    g.gz = gz; g.gz_ss = (long long)c->rows * N;
+    g.hin = hin; g.hin_ss = (long long)c->rows * K;
+    g.theta = theta; g.th_ss = c->Np; g.w_off = woff;
+    g.gzprev = gzprev; g.gzp_ss = (long long)c->rows * K;
+    g.part = c->ghp; g.ticket = c->ticket;
+    const dim3 grid(kbs, nsl, c->d.S);
+    cudaError_t e;
+    switch (MT) {
+      case 1: e = gh_t_launch<1>(grid, g, st); break;
+      case 2: e = gh_t_launch<2>(grid, g, st); break;
+      case 3: e = gh_t_launch<3>(grid, g, st); break;
+      case 4: e = gh_t_launch<4>(grid, g, st); break;
+      case 5: e = gh_t_launch<5>(grid, g, st); break;
+      case 6: e = gh_t_launch<6>(grid, g, st); break;
+      case 7: e = gh_t_launch<7>(grid, g, st); break;
+      case 8: e = gh_t_launch<8>(grid, g, st); break;
+      case 9: e = gh_t_launch<9>(grid, g, st); break;
+      default: e = gh_t_launch<10>(grid, g, st); break;
+    }
+    if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net g_h (tiled): ") + cudaGetErrorString(e));
+    return PDF_OK;
+  }
   NetBwdArgs<double> a = {};
   a.tl = g_tl_cur;
   a.rows = c->rows; a.K = K; a.N = N;
@@ -748,7 +793,6 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
   a.hin = hin; a.hin_ss = (long long)c->rows * K;
   a.theta = const_cast<double*>(theta); a.th_ss = c->Np; a.w_off = woff;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
-  const int MT = (c->rows + 7) / 8;
   const dim3 grid((K + 7) / 8, 1, c->d.S);
   const size_t smem = gh_x_smem_bytes(MT, N);
   void* args[] = {&a};
@@ -785,8 +829,14 @@ static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStrea
   const dim3 grid((unsigned)items, c->d.S);
   void* args[] = {&a};
   const int MT = (c->rows + 7) / 8;
-  cudaError_t e = MT == 1 ? plain_launch(net_adam_x_kernel<1>, grid, dim3(256), 0, st, args)
-                          : plain_launch(net_adam_x_kernel<2>, grid, dim3(256), 0, st, args);
+  const size_t smem = adam_x_smem_bytes(MT);
+  cudaError_t e;
+  switch (MT) {
+#define ACASE(MM) case MM: e = plain_launch(net_adam_x_kernel<MM>, grid, dim3(256), smem, st, args); break;
+    ACASE(1) ACASE(2) ACASE(3) ACASE(4) ACASE(5) ACASE(6) ACASE(7) ACASE(8) ACASE(9)
+    default: e = plain_launch(net_adam_x_kernel<10>, grid, dim3(256), smem, st, args); break;
+#undef ACASE
+  }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net adam (x): ") + cudaGetErrorString(e));
   return PDF_OK;
 }
@@ -876,6 +926,7 @@ static int create_impl(pdf_ctx* c, void* ws, size_t bytes, cudaStream_t st) {
   CK_CUDA(cudaMemcpyAsync(c->c_sca, c->c_sca_h.data(), c->d.S * sizeof(double), cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaMemsetAsync(c->err, 0, c->d.S * sizeof(int), st));
   CK_CUDA(cudaMemsetAsync(c->step, 0, 2 * sizeof(int), st));
+  if (c->ticket) CK_CUDA(cudaMemsetAsync(c->ticket, 0, (size_t)c->d.S * (c->H / GT_KB + 1) * sizeof(int), st));
   const int PP = c->P * c->P;
   permute_khat_kernel<T><<<(PP + 255) / 256, 256, 0, st>>>((const C<T>*)c->d.gd_kernel_hat, (C<T>*)c->khat, c->P,
                                                             c->large && c->E >= 4 ? 1 : 0);

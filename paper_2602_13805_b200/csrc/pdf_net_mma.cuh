@@ -632,12 +632,18 @@ constexpr int AX_NB = XW * 8;     // outputs per n-block (one n-tile per warp)
 // the strip's h columns and the block's g_z columns to shared memory, all
 // requested at once; layers whose g_z is two or more launches old do not
 // wait for the previous kernel at all.
+constexpr int AX_HP = AX_ST * 8 + 4, AX_GP = AX_NB + 4;   // pitches = 4 mod 16: conflict-free fragment reads
+__host__ __device__ constexpr size_t adam_x_smem_bytes(int MT) {
+  return (size_t)8 * MT * (AX_HP + AX_GP) * sizeof(double);
+}
+
 template <int MT>
 __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
   constexpr int RPM = 8 * MT, NS = RPM / 4;
-  constexpr int HP = AX_ST * 8 + 2, GP = AX_NB + 2;   // pitches (conflict-free fragment reads)
-  __shared__ __align__(16) double hS[RPM * HP];
-  __shared__ __align__(16) double gS[RPM * GP];
+  constexpr int HP = AX_HP, GP = AX_GP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* hS = reinterpret_cast<double*>(smem_raw);   // [RPM][HP]
+  double* gS = hS + RPM * HP;                          // [RPM][GP]
   __shared__ double bc_s[2];
   const int scene = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -692,11 +698,18 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
     double ga[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) ga[s] = gS[(4 * s + t) * GP + warp * 8 + g];   // A[g][t] = g_z[4s + t][n]
+    // NA accumulator pairs per tile break the dependent DMMA chain over rows
+    constexpr int NA = NS >= 12 ? 3 : (NS >= 4 ? 2 : 1);
 #pragma unroll
     for (int j = 0; j < AX_ST; ++j) {
-      double d0 = 0.0, d1 = 0.0;
+      double e0[NA], e1[NA];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) dmma(d0, d1, ga[s], hS[(4 * s + t) * HP + j * 8 + g]);   // B[t][g] = h[4s + t][k]
+      for (int q = 0; q < NA; ++q) e0[q] = e1[q] = 0.0;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) dmma(e0[s % NA], e1[s % NA], ga[s], hS[(4 * s + t) * HP + j * 8 + g]);   // B[t][g] = h[4s + t][k]
+      double d0 = e0[0], d1 = e1[0];
+#pragma unroll
+      for (int q = 1; q < NA; ++q) { d0 += e0[q]; d1 += e1[q]; }
       if (!tok[j]) continue;
       if (!isfinite(d0) || !isfinite(d1)) errbits |= ERR_NONFINITE_GRAD;
       adam_one<double>(wp[j].x, wm[j].x, wv[j].x, d0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
@@ -724,6 +737,123 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
     }
   }
   if (errbits) atomicOr(&a.err[scene], errbits);
+  tl_mark(a.tl, 2);
+}
+
+// g_h = g_z W_old for many rows or wide layers (network.py:210-212): CTA =
+// all rows x 64 outputs (one 8-wide k-tile per warp), n reduction in chunks
+// of 32 staged with cp.async (double-buffered), split over grid.y slices;
+// the slice partials are added in slice order by the last CTA of each
+// k-block (atomic ticket, self-resetting), which applies (1 - h^2).
+constexpr int GT_NC = 32, GT_KB = XW * 8;
+constexpr int GH_NSL = 16;   // max n slices
+constexpr int GT_GP = GT_NC + 4, GT_WP = GT_KB + 4;   // pitches = 4 mod 16
+__host__ __device__ constexpr size_t gh_t_smem_bytes(int MT) {
+  return ((size_t)2 * 8 * MT * GT_GP + (size_t)2 * GT_NC * GT_WP) * sizeof(double);
+}
+
+struct GhArgs {
+  int rows, K, N, nsl, ns;          // ns: n per slice (multiple of GT_NC)
+  const double* gz; long long gz_ss;
+  const double* hin; long long hin_ss;
+  const double* theta; long long th_ss, w_off;
+  double* gzprev; long long gzp_ss;
+  double* part;                      // [S][nsl][rows][K]
+  int* ticket;                       // [S][K / GT_KB]
+  int tl;
+};
+
+template <int MT>
+__global__ void __launch_bounds__(XW * 32) net_gh_t_kernel(GhArgs a) {
+  constexpr int RPM = 8 * MT, THR = XW * 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Gs = reinterpret_cast<double*>(smem_raw);   // [2][RPM][GT_GP]
+  double* Ws = Gs + 2 * RPM * GT_GP;                   // [2][GT_NC][GT_WP]
+  __shared__ int last_s;
+  const int K = a.K, N = a.N, rows = a.rows;
+  const int scene = blockIdx.z, sl = blockIdx.y, kb = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int k0 = kb * GT_KB;
+  const int n0 = sl * a.ns, n1 = min(N, n0 + a.ns);
+  const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
+  const double* __restrict__ gz = a.gz + scene * a.gz_ss;
+  tl_mark(a.tl, 0);
+  auto stage_w = [&](int c, int b) {
+    const int nc = n0 + c * GT_NC;
+    double* dst = Ws + b * GT_NC * GT_WP;
+    for (int i = tid; i < GT_NC * GT_KB / 2; i += THR) {
+      const int r = i / (GT_KB / 2), sg = i % (GT_KB / 2), n = nc + r, k = k0 + 2 * sg;
+      const bool ok = n < n1 && k < K;
+      cp_async16(dst + r * GT_WP + 2 * sg, ok ? W + (size_t)n * K + k : W, ok);
+    }
+  };
+  auto stage_g = [&](int c, int b) {
+    const int nc = n0 + c * GT_NC;
+    double* dst = Gs + b * RPM * GT_GP;
+    for (int i = tid; i < RPM * GT_NC / 2; i += THR) {
+      const int r = i / (GT_NC / 2), sg = i % (GT_NC / 2), n = nc + 2 * sg;
+      const bool ok = r < rows && n < n1;
+      cp_async16(dst + r * GT_GP + 2 * sg, ok ? gz + (size_t)r * N + n : gz, ok);
+    }
+  };
+  const int nch = (n1 - n0 + GT_NC - 1) / GT_NC;
+  // W_old is final since the previous iteration: the first chunk before the wait
+  if (nch > 0) stage_w(0, 0);
+  pdl_wait();
+  tl_mark(a.tl, 1);
+  if (nch > 0) stage_g(0, 0);
+  cp_async_commit();
+  double acc[MT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) { stage_w(c + 1, (c + 1) & 1); stage_g(c + 1, (c + 1) & 1); }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* G = Gs + (c & 1) * RPM * GT_GP;
+    const double* Wc = Ws + (c & 1) * GT_NC * GT_WP;
+#pragma unroll
+    for (int q = 0; q < GT_NC / 4; ++q) {
+      const double bv = Wc[(4 * q + t) * GT_WP + warp * 8 + g];      // B[t][g] = W[n + t][k + g]
+#pragma unroll
+      for (int i = 0; i < MT; ++i) dmma(acc[i][0], acc[i][1], G[(8 * i + g) * GT_GP + 4 * q + t], bv);
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+  // slice partial -> global, then the last CTA of this k-block reduces
+  double* P = a.part + ((size_t)scene * a.nsl + sl) * rows * K;
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int r = 8 * i + g, k = k0 + warp * 8 + 2 * t + cc;
+      if (r < rows && k < K) P[(size_t)r * K + k] = acc[i][cc];
+    }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int* tk = a.ticket + (size_t)scene * gridDim.x + kb;
+    const int prev = atomicAdd(tk, 1);
+    last_s = prev == a.nsl - 1;
+    if (last_s) *tk = 0;   // ready for the next launch
+  }
+  __syncthreads();
+  if (last_s) {
+    __threadfence();
+    const double* __restrict__ hin = a.hin + scene * a.hin_ss;
+    for (int e = tid; e < rows * GT_KB; e += THR) {
+      const int r = e / GT_KB, k = k0 + e % GT_KB;
+      if (k >= K) continue;
+      double s = 0.0;
+      for (int q = 0; q < a.nsl; ++q)
+        s += __ldcg(a.part + (((size_t)scene * a.nsl + q) * rows + r) * K + k);
+      const double hv = hin[(size_t)r * K + k];
+      a.gzprev[scene * a.gzp_ss + (size_t)r * K + k] = s * (1.0 - hv * hv);
+    }
+  }
   tl_mark(a.tl, 2);
 }
 
