@@ -136,3 +136,40 @@ def test_cfg5_trajectory_gate(cfg5):
     np.testing.assert_allclose(tr[:3, 5], g["trace"][:3, 5], rtol=1e-9)
     assert abs(res.rel_error - float(g["rel_error"])) < 1e-3, (res.rel_error, float(g["rel_error"]))
     print(f"cfg5: rel_error {res.rel_error:.6f} vs reference {float(g['rel_error']):.6f}")
+
+
+@pytest.mark.parametrize("n", [12, 36, 72])
+def test_train_step_split_backward_matches_oracle(tiny_setup, n):
+    """Fused training steps (split backward: g_h kernels + one Adam launch over
+    all layers) against the oracle's grad_loss + Adam sequence (network.py:
+    183-264) for 12 / 36 / 72 network rows."""
+    from oracle import pdf_oracle as O
+    from conftest import oracle_ops
+    from paper_2602_13805_b200.engine import DeviceProblem
+    rng = np.random.default_rng(100 + n)
+    m, R = 16, tiny_setup.ops.gs_matrix.shape[0]
+    phi = 2 * np.pi * np.arange(n) / n
+    xy = np.linspace(-0.7, 0.7, m)
+    e_inc = np.exp(1j * 2 * np.pi * (np.cos(phi)[:, None, None] * xy[None, None, :]
+                                     + np.sin(phi)[:, None, None] * xy[None, :, None]))
+    data = 0.3 * (rng.standard_normal((n, R)) + 1j * rng.standard_normal((n, R)))
+    alpha0 = 0.05 * (rng.standard_normal((n, 36)) + 1j * rng.standard_normal((n, 36)))
+    params = O.init_net(36, np.random.default_rng(2))
+    flat = O.flat(params) + 0.02 * rng.standard_normal(O.flat(params).size)
+    ctx = O.Context(data, e_inc, oracle_ops(tiny_setup), 3, 6.0, LAM, 0.5)
+    dev = DeviceProblem(tiny_setup.ops, e_inc, data, mf=3, beta=6.0, lambdas=LAM, tau_b=0.5)
+    dev.net_setup(torch.as_tensor(alpha0[None], device="cuda"))
+    th = torch.as_tensor(flat[None], device="cuda").contiguous()
+    mm, vv = torch.zeros_like(th), torch.zeros_like(th)
+    steps = 3
+    trace = torch.zeros(steps, 1, 6, dtype=torch.float64, device="cuda")
+    dev.train(th, mm, vv, 0, steps, trace, use_graph=False)
+    torch.cuda.synchronize()
+    dev.check_errors()
+    want = flat.copy()
+    st = O.Adam(m=np.zeros_like(flat), v=np.zeros_like(flat))
+    for k in range(steps):
+        g, parts = O.grad_loss(O.unflat(want, params), alpha0, ctx)
+        assert abs(trace[k, 0, 5].item() - parts["total"]) < 1e-9 * abs(parts["total"])
+        want = O.adam_update(st, want, g)
+    assert np.abs(th[0].cpu().numpy() - want).max() < 1e-9
