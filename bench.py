@@ -226,6 +226,13 @@ def algorithmic_work(dev, phase: str):
     N_, K_ = layer
     if phase.startswith("fwd"):
         return "hbm", S * es * (N_ * K_ + rows * K_ + rows * N_)
+    if getattr(dev, "split_bwd", False):
+        # split backward: bwd_l3 / bwd_l2 = g_h kernels (W_old read, g_z and h read,
+        # g_z' written); bwd_l1 = g_W + Adam of all layers (W, m, v read + written)
+        if phase in ("bwd_l3", "bwd_l2"):
+            return "hbm", S * es * (N_ * K_ + rows * (N_ + 2 * K_))
+        weights = H * D0 + H * H + D0 * H
+        return "hbm", S * es * (6 * (weights + 2 * H + D0) + rows * (2 * H + D0) * 2)
     return "hbm", S * es * (6 * N_ * K_ + rows * (K_ + 2 * N_))
 
 

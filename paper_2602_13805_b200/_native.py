@@ -30,7 +30,7 @@ EXPORTS = (
     "pdf_net_dims", "pdf_loss_grad", "pdf_loss_value", "pdf_net_setup", "pdf_net_forward",
     "pdf_grad_loss", "pdf_adam_step", "pdf_set_norms", "pdf_train", "pdf_apply_gd", "pdf_gs_forward", "pdf_gs_adjoint",
     "pdf_expand", "pdf_truncate", "pdf_apply_cco", "pdf_get_error", "pdf_profile_train", "pdf_fp64_probe",
-    "pdf_timeline_reset", "pdf_timeline_read",
+    "pdf_timeline_reset", "pdf_timeline_read", "pdf_ctx_paths",
     "pdf_net_setup_sharded", "pdf_shard_buffer_sizes", "pdf_shard_step_a", "pdf_shard_step_b", "pdf_shard_step_c",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
@@ -92,6 +92,7 @@ def lib():
         "pdf_profile_train": (ct.c_int, [vp, vp, vp, vp, i32, i32, ct.POINTER(ct.c_float), vp]),
         "pdf_fp64_probe": (ct.c_int, [dp, vp]),
         "pdf_timeline_reset": (ct.c_int, [vp, i32, vp]),
+        "pdf_ctx_paths": (ct.c_int, [vp, ct.POINTER(i32)]),
         "pdf_timeline_read": (ct.c_int, [ct.POINTER(ct.c_uint64), vp]),
         "pdf_net_setup_sharded": (ct.c_int, [vp, vp, i32, i32, vp]),
         "pdf_shard_buffer_sizes": (ct.c_int, [vp, ct.POINTER(i64), ct.POINTER(i64)]),

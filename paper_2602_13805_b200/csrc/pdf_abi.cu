@@ -972,6 +972,13 @@ extern "C" int pdf_ctx_destroy(pdf_ctx* c) {
   return PDF_OK;
 }
 
+extern "C" int pdf_ctx_paths(const pdf_ctx* c, int32_t* paths) {
+  if (!c || !paths) return fail(PDF_EINVAL, "null argument");
+  *paths = (c->large ? PDF_PATH_LARGE_GRID : 0) | (c->dgemm ? PDF_PATH_DATA_GEMM : 0) |
+           (c->xbwd ? PDF_PATH_SPLIT_BWD : 0);
+  return PDF_OK;
+}
+
 extern "C" int pdf_net_dims(const pdf_ctx* c, int32_t* rows, int32_t* d0, int32_t* hidden, int64_t* np) {
   if (!c) return fail(PDF_EINVAL, "null ctx");
   if (rows) *rows = c->rows;
