@@ -10,7 +10,7 @@ import ctypes as ct
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpdfb200.so")
+LIB_PATH = os.environ.get("PDF_LIB_PATH") or os.path.join(_HERE, "libpdfb200.so")   # override: A/B measurements only
 
 ABI_VERSION = 1
 PDF_F64, PDF_F32 = 0, 1
@@ -101,6 +101,8 @@ def lib():
         "pdf_shard_step_c": (ct.c_int, [vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("PDF_LIB_PATH") and not hasattr(L, name):
+            continue   # A/B against an older build
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

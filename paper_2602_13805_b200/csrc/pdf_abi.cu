@@ -27,6 +27,8 @@ static thread_local int g_tl_cur = 0, g_tl_iter = 0;
 static int env_int(const char* name, int dflt);
 // programmatic dependent launch for the hot-loop kernels (PDF_PDL=0 disables)
 static const int g_pdl = env_int("PDF_PDL", 1);
+// set around launches that must fully follow their stream predecessor (side-stream branches)
+static thread_local int g_pdl_off = 0;
 
 // cluster caps (tunable for experiments: PDF_NET_CLUSTER, PDF_VIEW_CLUSTER)
 static int env_int(const char* name, int dflt) {
@@ -78,6 +80,13 @@ struct pdf_ctx {
   void *spec, *gpart, *dpart;
   double* ghp;       // split backward: g_h slice partials [S][GH_NSL][rows][H]
   int* ticket;       // split backward: per k-block tickets [S][H / 64 + 1]
+  // captured training graph with the Adam of layers 2 / 3 on a side branch:
+  // activations and the Adam-t snapshot alternate between two buffers per iteration
+  void *h1b, *h2b;
+  int *tsnap, *tsnap_b;
+  int capturing = 0, pend = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_g3 = nullptr, ev_g2 = nullptr, ev_a2 = nullptr;
   double *red1, *red2;   // split pixel stage scratch (local reductions)
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
@@ -126,6 +135,10 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
   c->ghp = c->xbwd ? w.take<double>((size_t)d.S * GH_NSL * c->rows * c->H) : nullptr;
   c->ticket = c->xbwd ? w.take<int>((size_t)d.S * (c->H / GT_KB + 1)) : nullptr;
+  c->h1b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
+  c->h2b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
+  c->tsnap = c->xbwd ? w.take<int>(1) : nullptr;
+  c->tsnap_b = c->xbwd ? w.take<int>(1) : nullptr;
   c->red1 = c->split ? w.take<double>((size_t)d.S * (3 * img + 1)) : nullptr;
   c->red2 = c->split ? w.take<double>((size_t)d.S * (2 * img + 2)) : nullptr;
   c->dloss = w.take<double>(SN);
@@ -236,7 +249,7 @@ static cudaError_t launch_cluster(F kern, dim3 grid, dim3 block, size_t smem, cu
   attr[0].val.clusterDim.y = cluster.y;
   attr[0].val.clusterDim.z = cluster.z;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = g_pdl;
+  attr[1].val.programmaticStreamSerializationAllowed = g_pdl && !g_pdl_off;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
@@ -260,7 +273,7 @@ static cudaError_t plain_launch(K kern, dim3 grid, dim3 block, size_t smem, cuda
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl && !g_pdl_off;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelExC(&cfg, (const void*)kern, args);
@@ -752,7 +765,7 @@ static cudaError_t gh_t_launch(dim3 grid, GhArgs& a, cudaStream_t st) {
 }
 
 static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, int N, const double* theta,
-                      long long woff, double* gzprev, cudaStream_t st) {
+                      long long woff, double* gzprev, int* snap, cudaStream_t st) {
   const int MT = (c->rows + 7) / 8;
   if (MT > 2 || N > XW * 4 * GX_STEPS) {
     // tiled: all rows x 64 outputs per CTA, n split into slices (~2 CTAs per SM)
@@ -768,7 +781,7 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
     g.hin = hin; g.hin_ss = (long long)c->rows * K;
     g.theta = theta; g.th_ss = c->Np; g.w_off = woff;
     g.gzprev = gzprev; g.gzp_ss = (long long)c->rows * K;
-    g.part = c->ghp; g.ticket = c->ticket;
+    g.part = c->ghp; g.ticket = c->ticket;   // (the side-branch fork, which needs the t snapshot, uses gh_x only)
     const dim3 grid(kbs, nsl, c->d.S);
     cudaError_t e;
     switch (MT) {
@@ -793,6 +806,7 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
   a.hin = hin; a.hin_ss = (long long)c->rows * K;
   a.theta = const_cast<double*>(theta); a.th_ss = c->Np; a.w_off = woff;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
+  a.step = c->step; a.snap = snap;
   const dim3 grid((K + 7) / 8, 1, c->d.S);
   const size_t smem = gh_x_smem_bytes(MT, N);
   void* args[] = {&a};
@@ -802,7 +816,9 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
   return PDF_OK;
 }
 
-static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStream_t st) {
+// layers: bit l of `mask` selects network layer l + 1; tsnap: Adam t snapshot or null (*step)
+static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStream_t st, int mask = 7,
+                      const int* tsnap = nullptr) {
   const long long H = c->H, D0 = c->D0, R = c->rows;
   const Offs o = offsets(c);
   // launch order: layer 3 (g_z = g_y, three launches old), layer 2 (g_z2 from
@@ -820,11 +836,12 @@ static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStrea
     L.w_off = wo[l]; L.b_off = bo[l]; L.N = (int)Ns[l]; L.K = (int)Ks[l];
     L.nblk = (int)((Ns[l] + AX_NB - 1) / AX_NB);
     L.strips = (int)((Ks[l] + AX_ST * 8 - 1) / (AX_ST * 8));
-    L.items = L.nblk * L.strips + (int)((Ns[l] + 255) / 256);
+    const int layer = 3 - l;   // entries in launch order 3, 2, 1
+    L.items = (mask >> (layer - 1) & 1) ? L.nblk * L.strips + (int)((Ns[l] + 255) / 256) : 0;
     L.wait = l == 2;
     items += L.items;
   }
-  a.rows = c->rows; a.theta = theta; a.m = m; a.v = v; a.th_ss = c->Np; a.step = c->step;
+  a.rows = c->rows; a.theta = theta; a.m = m; a.v = v; a.th_ss = c->Np; a.step = c->step; a.tsnap = tsnap;
   a.lr = c->d.lr; a.b1 = c->d.adam_b1; a.b2 = c->d.adam_b2; a.eps = c->d.adam_eps; a.err = c->err;
   const dim3 grid((unsigned)items, c->d.S);
   void* args[] = {&a};
@@ -857,10 +874,22 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   const Offs o = offsets(c);
   const T* thc = (const T*)theta;
   T* th = (T*)theta;
+  // captured graph: the Adam of layers 3 / 2 runs on a side branch that
+  // overlaps the next iteration's first layers; h1 / h2 (read by it) and the
+  // Adam-t snapshot alternate between two buffers
+  // (measured: cfg2 88.1 -> 84.6 us; with 36 rows the side branch slows the
+  // main chain, cfg3 150 -> 194 us: rows <= 16 only)
+  const bool fork = sizeof(T) == 8 && c->capturing && fused && c->xbwd && c->rows <= 16 &&
+                    c->H <= XW * 4 * GX_STEPS && c->D0 <= XW * 4 * GX_STEPS;
+  if (fork) { std::swap(c->h1, c->h1b); std::swap(c->h2, c->h2b); std::swap(c->tsnap, c->tsnap_b); }
   mark();
   if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->x0, c->D0, c->H, thc, o.w1, o.b1, (T*)c->h1, 0,
                                   fused ? c->step : nullptr, st));
   mark();
+  if (fork && c->pend) {   // W2 / W3 of the previous iteration's side branch
+    CK_CUDA(cudaStreamWaitEvent(st, c->ev_a2, 0));
+    c->pend = 0;
+  }
   if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h1, c->H, c->H, thc, o.w2, o.b2, (T*)c->h2, 0, nullptr, st));
   mark();
   if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h2, c->H, c->D0, thc, o.w3, o.b3, nullptr, 1, nullptr, st));
@@ -880,12 +909,32 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
     if (fused && c->xbwd) {
       // split backward: phases bwd_l3 / bwd_l2 = g_h of layers 3 / 2, bwd_l1 = g_W + Adam (all layers)
       if (run()) TRY(gh_x_layer(c, (const double*)c->gy, (const double*)c->h2, c->H, c->D0, (const double*)theta,
-                                o.w3, (double*)c->gz2, st));
+                                o.w3, (double*)c->gz2, fork ? c->tsnap : nullptr, st));
+      if (fork) CK_CUDA(cudaEventRecord(c->ev_g3, st));
       mark();
       if (run()) TRY(gh_x_layer(c, (const double*)c->gz2, (const double*)c->h1, c->H, c->H, (const double*)theta,
-                                o.w2, (double*)c->gz1, st));
+                                o.w2, (double*)c->gz1, nullptr, st));
+      if (fork) CK_CUDA(cudaEventRecord(c->ev_g2, st));
       mark();
-      if (run()) TRY(adam_x_all(c, (double*)theta, (double*)m, (double*)v, st));
+      if (fork) {
+        // critical path: W1 (the next forward starts with it); side: W3 after
+        // g_h3, W2 after g_h2 (full dependencies, no PDL)
+        if (run()) TRY(adam_x_all(c, (double*)theta, (double*)m, (double*)v, st, 1, c->tsnap));
+        CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_g3, 0));
+        g_pdl_off = 1;
+        int r1 = run() ? adam_x_all(c, (double*)theta, (double*)m, (double*)v, c->side, 4, c->tsnap) : PDF_OK;
+        cudaError_t e1 = cudaStreamWaitEvent(c->side, c->ev_g2, 0);
+        int r2 = run() && r1 == PDF_OK ? adam_x_all(c, (double*)theta, (double*)m, (double*)v, c->side, 2, c->tsnap)
+                                       : PDF_OK;
+        g_pdl_off = 0;
+        TRY(r1);
+        TRY(r2);
+        CK_CUDA(e1);
+        CK_CUDA(cudaEventRecord(c->ev_a2, c->side));
+        c->pend = 1;
+      } else {
+        if (run()) TRY(adam_x_all(c, (double*)theta, (double*)m, (double*)v, st));
+      }
       mark();
       return PDF_OK;
     }
@@ -968,6 +1017,8 @@ extern "C" int pdf_ctx_destroy(pdf_ctx* c) {
   if (!c) return PDF_OK;
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : {c->ev_g3, c->ev_g2, c->ev_a2}) if (e) cudaEventDestroy(e);
   delete c;
   return PDF_OK;
 }
@@ -1109,13 +1160,26 @@ static int train_impl(pdf_ctx* c, void* theta, void* m, void* v, int t0, int k, 
     // capture on a private stream (the caller's may be the legacy default
     // stream, which cannot capture); the graph is then launched on `st`
     if (!c->g_stream) CK_CUDA(cudaStreamCreateWithFlags(&c->g_stream, cudaStreamNonBlocking));
+    if (c->xbwd && !c->side) {
+      CK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      CK_CUDA(cudaEventCreateWithFlags(&c->ev_g3, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&c->ev_g2, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&c->ev_a2, cudaEventDisableTiming));
+    }
     cudaGraph_t g;
     CK_CUDA(cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal));
     int r = PDF_OK;
+    c->capturing = env_int("PDF_ADAM_FORK", 1);
+    c->pend = 0;
     for (int i = 0; i < G && r == PDF_OK; ++i) {
       g_tl_iter = i;
       r = iteration<T>(c, theta, m, v, nullptr, nullptr, tr, 1, c->g_stream);
     }
+    if (c->pend) {   // join the last side branch before the capture ends
+      cudaStreamWaitEvent(c->g_stream, c->ev_a2, 0);
+      c->pend = 0;
+    }
+    c->capturing = 0;
     g_tl_cur = 0;
     cudaError_t e = cudaStreamEndCapture(c->g_stream, &g);
     if (r != PDF_OK) return r;

@@ -211,6 +211,7 @@ struct NetBwdArgs {
   T* gzprev; long long gzp_ss;        // [S][rows][K] or null (first layer)
   int* err;                           // [S]
   int tl;                             // timeline slot + 1 (0: off)
+  int* snap;                          // split backward: *snap = *step (Adam t of this iteration) or null
 };
 
 // Adam in the reference's operation order (network.py:252-257).  The bias

@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(XW * 32, 1) net_gh_x_kernel(NetBwdArgs<double>
   const int nb = warp * npw, ne = min(N, nb + npw);
   const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
   tl_mark(a.tl, 0);
+  if (a.snap && tid == 0 && blockIdx.x == 0 && scene == 0) *a.snap = *a.step;
   // B fragments (W_old is final since the previous iteration): lane holds W[n + t][k0 + g]
   double b[GX_STEPS];
   const bool kok = k0 + g < K;
@@ -619,6 +620,7 @@ struct NetAdamArgs {
   int rows;
   double* theta; double* m; double* v; long long th_ss;
   const int* step;
+  const int* tsnap;       // Adam t snapshot of this iteration (side-stream launches) or null
   double lr, b1, b2, eps;
   int* err;
   int tl;
@@ -658,7 +660,7 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
   double* __restrict__ vv = a.v + scene * a.th_ss;
   const double* __restrict__ gz = L.gz + scene * L.gz_ss;
   if (tid == 0) {
-    const double tt = (double)*a.step;
+    const double tt = (double)(a.tsnap ? *a.tsnap : *a.step);
     bc_s[0] = 1.0 / (1.0 - pow(a.b1, tt));
     bc_s[1] = 1.0 / (1.0 - pow(a.b2, tt));
   }

@@ -112,7 +112,8 @@ class DeviceProblem:
         N.check(self.lib.pdf_net_dims(self.ctx, ct.byref(rows), ct.byref(d0), ct.byref(hid), ct.byref(npar)))
         self.rows, self.d0, self.hidden, self.n_params = rows.value, d0.value, hid.value, npar.value
         paths = ct.c_int32()
-        N.check(self.lib.pdf_ctx_paths(self.ctx, ct.byref(paths)))
+        if hasattr(self.lib, "pdf_ctx_paths"):
+            N.check(self.lib.pdf_ctx_paths(self.ctx, ct.byref(paths)))
         self.large_grid, self.data_gemm, self.split_bwd = (bool(paths.value & b) for b in (1, 2, 4))
         self.bd = torch.zeros(S, 6, dtype=torch.float64, device=dev)
 
