@@ -87,23 +87,45 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   }
 
   // ---- per-warp partial num/den on the halo --------------------------------
-  for (int h = lane; h < NH; h += 32) {
-    const int hy = y - 1 + h / WW, hx = x0 - 1 + h % WW;
-    C<T> num = czero<T>();
-    T den = T(0);
-    if (hy >= 0 && hy < M && hx >= 0 && hx < M) {
-      const size_t pix = (size_t)hy * M + hx;
-      for (int i = warp; i < n; i += nw) {
-        const C<T> j = a.J[(vbase + i) * img + pix];
-        const C<T> e = a.E[(vbase + i) * img + pix];
-        num = cadd<T>(num, cmulc<T>(j, e));
-        den += cabs2<T>(e);
+  // halo entries h = lane + 32 q (NH <= 3 (32 + 2) < 128): the four entries'
+  // loads of one view are in flight together; per entry the views are summed
+  // in increasing order
+  {
+    constexpr int QH = 4;
+    C<T> num[QH];
+    T den[QH];
+    size_t pix[QH];
+    bool ok[QH];
+#pragma unroll
+    for (int q = 0; q < QH; ++q) {
+      const int h = lane + 32 * q;
+      const int hy = y - 1 + h / WW, hx = x0 - 1 + h % WW;
+      ok[q] = h < NH && hy >= 0 && hy < M && hx >= 0 && hx < M;
+      pix[q] = ok[q] ? (size_t)hy * M + hx : 0;
+      num[q] = czero<T>();
+      den[q] = T(0);
+    }
+    for (int i = warp; i < n; i += nw) {
+      C<T> j[QH], e[QH];
+#pragma unroll
+      for (int q = 0; q < QH; ++q) {
+        j[q] = ok[q] ? a.J[(vbase + i) * img + pix[q]] : czero<T>();
+        e[q] = ok[q] ? a.E[(vbase + i) * img + pix[q]] : czero<T>();
+      }
+#pragma unroll
+      for (int q = 0; q < QH; ++q) {
+        num[q] = cadd<T>(num[q], cmulc<T>(j[q], e[q]));
+        den[q] += cabs2<T>(e[q]);
       }
     }
-    pnum[warp][h] = num;
-    pden[warp][h] = den;
+#pragma unroll
+    for (int q = 0; q < QH; ++q) {
+      const int h = lane + 32 * q;
+      if (h < NH) { pnum[warp][h] = num[q]; pden[warp][h] = den[q]; }
+    }
   }
   __syncthreads();
+  tl_stage(a.tl, 0);
   const T eps = (T)eps_s;
   for (int h = tid; h < NH; h += blockDim.x) {
     C<T> num = czero<T>();
@@ -114,6 +136,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     if (h / WW == 1 && (h % WW) >= 1 && (h % WW) <= TX) dens[h % WW - 1] = den;
   }
   __syncthreads();
+  tl_stage(a.tl, 1);
 
   // ---- stencil terms at rows y-1, y (forward differences, losses.py:139-144)
   const T tau = a.tau;
@@ -141,6 +164,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     bsig[row][cix] = sig; bdamp[row][cix] = damp; bcx[row][cix] = cx; bcy[row][cix] = cy;
   }
   __syncthreads();
+  tl_stage(a.tl, 2);
 
   // ---- per-pixel scalar work ------------------------------------------------
   double vb = 0.0, vt = 0.0, vr = 0.0;
@@ -189,6 +213,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     Rs[tid] = R_;
   }
   __syncthreads();
+  tl_stage(a.tl, 3);
 
   // ---- state residual, R-chain partial ------------------------------------
   const T beta = a.beta;
@@ -211,6 +236,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   pdl_trigger();
   if (GRAD) {
     __syncthreads();
+    tl_stage(a.tl, 4);
     if (tid < TX) {
       C<T> gr = czero<T>();
       for (int w = 0; w < nw; ++w) gr = cadd<T>(gr, pgr[w][tid]);
@@ -222,6 +248,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
       gden[tid] = -(gchi.x * chi.x + gchi.y * chi.y) / den;   // -Re(conj(g_chi) chi)/den
     }
     __syncthreads();
+    tl_stage(a.tl, 5);
     if (lane < TX) {
       const size_t pix = (size_t)y * M + x0 + lane;
       const C<T> R_ = Rs[lane];
@@ -245,6 +272,7 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
     }
   }
 
+  tl_stage(a.tl, 6);
   // ---- loss partials (fixed order) ----------------------------------------
   vs = warp_sum<double>(vs);
   vb = warp_sum<double>(vb);
