@@ -316,7 +316,7 @@ PHASE_KERNEL = {"view_fwd": "view_kernel<double, 4, 0", "view_bwd": "view_kernel
 LAYER_POS = {"fwd_l1": 0, "fwd_l2": 1, "fwd_l3": 2, "bwd_l3": 0, "bwd_l2": 1, "bwd_l1": 2}
 
 
-def ncu_traffic(phase: str):
+def ncu_traffic(phase: str, split_bwd: bool = False):
     """Mean DRAM bytes (read + write) per launch of the phase's kernel from the
     committed ncu launch list of this bench command (profiles/), else None.
     ncu flushes caches before each launch (cold), and a kernel's writes still
@@ -326,6 +326,10 @@ def ncu_traffic(phase: str):
     import csv
     files = sorted(glob.glob(os.path.join(HERE, "profiles", "*_launches_cfg2.csv.gz")))
     key = PHASE_KERNEL.get(phase)
+    if split_bwd and phase in ("bwd_l3", "bwd_l2"):
+        key = "net_gh_"
+    elif split_bwd and phase == "bwd_l1":
+        key = "net_adam_x"
     if not files or not key:
         return None
     try:
@@ -340,9 +344,18 @@ def ncu_traffic(phase: str):
             if key in r[ki] and r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 per[int(r[idi])] = per.get(int(r[idi]), 0.0) + float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         ids = sorted(per)
-        if phase in LAYER_POS:
-            ids = ids[LAYER_POS[phase]::3]
-        vals = [per[i] for i in ids]
+        if split_bwd and phase in ("bwd_l3", "bwd_l2"):
+            ids = ids[(0 if phase == "bwd_l3" else 1)::2]          # g_h launches: layer 3, layer 2
+            vals = [per[i] for i in ids]
+        elif split_bwd and phase == "bwd_l1":
+            # one Adam launch over all layers, or three (layer 1 + the side branch's 3 / 2) in the graph
+            n3 = len(ids) // 3 if len(ids) % 3 == 0 and "net_adam_x" in key else 0
+            vals = [per[ids[3 * q]] + per[ids[3 * q + 1]] + per[ids[3 * q + 2]] for q in range(n3)] if n3 else \
+                [per[i] for i in ids]
+        else:
+            if phase in LAYER_POS:
+                ids = ids[LAYER_POS[phase]::3]
+            vals = [per[i] for i in ids]
         return {"bytes_per_launch": float(np.mean(vals)), "launches": len(vals),
                 "source": os.path.relpath(files[-1], HERE)} if vals else None
     except Exception:
@@ -453,7 +466,7 @@ def run_ours(args, d: Dist):
     proof = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), fp64_peak_tflops, peaks["hbm_gbs"], m0=4 * dev.mf ** 2)
     proof["frac"] = proof["t_roof_us_per_scene_iter"] / (1e3 * ms_step / k)
     roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom],
-                 "traffic": ncu_traffic(dom), "share_of_step": share[dom]})
+                 "traffic": ncu_traffic(dom, getattr(dev, "split_bwd", False)), "share_of_step": share[dom]})
 
     # ---- e2e through the public API with host buffers (per step: H2D data, D2H results)
     res = rec.run([data[0]], seeds=[cfg.rng_seed], chi_trues=[chi_true[0]])   # warm (theta0 cache)
