@@ -203,8 +203,8 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   c->split = env_int("PDF_SPLIT_PIXEL", 0) && !d->joint;
   // latency regime: g_h and g_W + Adam as separate fully parallel launches
   // (measured: cfg2 -4 us, cfg3 167 -> 150 us per iteration, cfg5 unchanged)
-  c->xbwd = env_int("PDF_BWD_X", 1) && d->dtype == PDF_F64 && c->rows <= 80 &&
-            (long long)d->S * (c->H / 8) <= 4 * 148;
+  const int bx = env_int("PDF_BWD_X", 1);   // 2: force (experiments)
+  c->xbwd = bx && d->dtype == PDF_F64 && c->rows <= 80 && (bx == 2 || (long long)d->S * (c->H / 8) <= 4 * 148);
   if (c->dgemm) {
     const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
