@@ -626,7 +626,7 @@ static int bwd_mma_layer(pdf_ctx* c, NetBwdArgs<double>& a, bool fused, cudaStre
   // two k-tiles per warp (128-byte W row segments) when the batch fills the GPU
   static const int kt_env = env_int("PDF_BWD_KT", 0);
   int KT = 1;
-  if (MT <= 4 && (long long)((K + 63) / 64) * S >= 2 * 148) KT = 2;
+  // (two k-tiles per warp measured 1.2 % slower at 128 scenes: one everywhere; PDF_BWD_KT=2 for experiments)
   if (kt_env == 1 || (kt_env == 2 && MT <= 4)) KT = kt_env;
   static const int wb_env = env_int("PDF_BWD_WB", 0), d_env = env_int("PDF_BWD_D", 3);
   // 8 warps per CTA in every regime (measured: cfg2 96.8 -> 93.7 us/iter,
