@@ -21,7 +21,9 @@ reference.  Every numerical step runs in libpdfb200.so on the GPU.
 from __future__ import annotations
 
 import time
+import warnings
 from concurrent.futures import ThreadPoolExecutor
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -86,6 +88,32 @@ class LossBreakdown:
     def from_row(cls, row, weights) -> "LossBreakdown":
         st, da, bo, tv, br, tot = (float(x) for x in row)
         return cls(total=tot, state=st, data=da, bound=bo, tv=tv, bridge=br, weights=tuple(weights))
+
+
+class LossTrace(Sequence):
+    """Per-iteration LossBreakdown rows (reconstruct.py:217-220) backed by the
+    float64 trace array copied from the device; entries are built on access,
+    so a 500-iteration result costs no Python objects until it is read."""
+
+    def __init__(self, rows: np.ndarray, weights):
+        self._rows = np.ascontiguousarray(rows, dtype=np.float64).reshape(-1, 6)
+        self._w = tuple(weights)
+
+    def __len__(self) -> int:
+        return self._rows.shape[0]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        st, da, bo, tv, br, tot = self._rows[i].tolist()
+        return LossBreakdown(total=tot, state=st, data=da, bound=bo, tv=tv, bridge=br, weights=self._w)
+
+    def __eq__(self, other) -> bool:
+        return list(self) == list(other)
+
+    def as_array(self) -> np.ndarray:
+        """[k][6] rows in as_row() order (state, data, bound, tv, bridge, total)."""
+        return self._rows.copy()
 
 
 @dataclass
@@ -431,6 +459,33 @@ class BatchReconstructor:
                                  lr=config.learn_rate, dtype=dtype)
         self.m0_eff = self.basis.m0 * (self.e_inc.shape[0] if config.joint_views else 1)
 
+    def _initialise(self):
+        """bp_initialize + init_alpha + net_setup (reconstruct.py:52-153, network.py:88-104)
+        on the current data: ~70 small launches, replayed from a CUDA graph
+        captured on the first call (the data and normalisers are updated in
+        place by set_data, so the graph stays valid)."""
+        dev = self.dev
+        if not self.use_graph:
+            chi0, r0 = dev.bp_initialize(check=False)
+            alpha0 = dev.init_alpha(r0, check=False)
+            dev.net_setup(alpha0)
+            return chi0, alpha0
+        if getattr(self, "_init_graph", None) is None:
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):            # warm-up outside the capture
+                chi0, r0 = dev.bp_initialize(check=False)
+                dev.net_setup(dev.init_alpha(r0, check=False))
+            torch.cuda.current_stream().wait_stream(st)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                chi0, r0 = dev.bp_initialize(check=False)
+                alpha0 = dev.init_alpha(r0, check=False)
+                dev.net_setup(alpha0)
+            self._init_graph, self._init_out = g, (chi0, alpha0)
+        self._init_graph.replay()
+        return self._init_out
+
     def run(self, datas, seeds=None, chi_trues=None, k_iters: int | None = None) -> list:
         cfg = self.config
         t0 = time.perf_counter()
@@ -451,9 +506,7 @@ class BatchReconstructor:
             host = torch.empty((self.S, _flat_size(self.m0_eff)), dtype=torch.float64, pin_memory=True)
             pending = _theta0_async(seeds, self.m0_eff, host.numpy())
         dev.set_data(mats)
-        chi0, r0 = dev.bp_initialize()
-        alpha0 = dev.init_alpha(r0)
-        dev.net_setup(alpha0)
+        chi0, alpha0 = self._initialise()
         if pending is not None:
             for f in pending:
                 f.result()
@@ -469,6 +522,10 @@ class BatchReconstructor:
         ahat = dev.net_forward(theta)
         bd, chi = dev.loss_value(ahat, want_chi=True)
         chi_cco = dev.apply_cco(chi, cfg.cco) if cfg.use_cco else chi.clone()
+        if bool(dev.pole_flag):     # deferred checks of the initialisation (no host sync before the loop)
+            raise PoleError("beta*chi + 1 vanishes at some pixel")
+        if bool(dev.zero_grad_flag):
+            warnings.warn("zero initial gradient; starting from zero coefficients")
         dev.check_errors()
         chi0_h, chi_h, cco_h = chi0.cpu().numpy(), chi.cpu().numpy(), chi_cco.cpu().numpy()
         tr_h, bd_h = trace.cpu().numpy(), bd.cpu().numpy()
@@ -483,7 +540,7 @@ class BatchReconstructor:
             out.append(ReconstructionResult(
                 chi_hat=ComplexGrid(chi_h[s], cs), chi_cco=ComplexGrid(cco_h[s], cs),
                 chi0=ComplexGrid(chi0_h[s], cs),
-                trace=[LossBreakdown.from_row(tr_h[i, s], self.lambdas) for i in range(k)],
+                trace=LossTrace(tr_h[:k, s], self.lambdas),
                 final_loss=LossBreakdown.from_row(bd_h[s], self.lambdas), wall_time=wall, rel_error=rel))
         return out
 
@@ -541,7 +598,7 @@ def _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0):
     tr = trace.cpu().numpy()
     return ReconstructionResult(chi_hat=ComplexGrid(chi[0].cpu().numpy(), cs), chi_cco=ComplexGrid(cco_h, cs),
                                 chi0=ComplexGrid(chi0[0].cpu().numpy(), cs),
-                                trace=[LossBreakdown.from_row(tr[i, 0], lam) for i in range(k)],
+                                trace=LossTrace(tr[:k, 0], lam),
                                 final_loss=LossBreakdown.from_row(bd[0].cpu().numpy(), lam),
                                 wall_time=time.perf_counter() - t0, rel_error=rel)
 

@@ -111,6 +111,8 @@ class DeviceProblem:
         rows, d0, hid, npar = ct.c_int32(), ct.c_int32(), ct.c_int32(), ct.c_int64()
         N.check(self.lib.pdf_net_dims(self.ctx, ct.byref(rows), ct.byref(d0), ct.byref(hid), ct.byref(npar)))
         self.rows, self.d0, self.hidden, self.n_params = rows.value, d0.value, hid.value, npar.value
+        self.c_inc_d = torch.as_tensor(np.asarray(self.c_inc, float), device=dev)
+        self.c_sca_d = torch.as_tensor(np.asarray(self.c_sca, float), device=dev)
         paths = ct.c_int32()
         if hasattr(self.lib, "pdf_ctx_paths"):
             N.check(self.lib.pdf_ctx_paths(self.ctx, ct.byref(paths)))
@@ -182,6 +184,12 @@ class DeviceProblem:
         if np.any(np.asarray(c_sca) <= 0) or np.any(np.asarray(c_inc) <= 0):
             raise ZeroDataError("measured scattered / incident power is zero")
         self.c_inc, self.c_sca = np.asarray(c_inc, float), np.asarray(c_sca, float)
+        # device copies (read by init_alpha; updated in place so a captured graph sees new values)
+        if getattr(self, "c_inc_d", None) is None:
+            self.c_inc_d = torch.empty(self.S, dtype=torch.float64, device=self.device)
+            self.c_sca_d = torch.empty(self.S, dtype=torch.float64, device=self.device)
+        self.c_inc_d.copy_(torch.as_tensor(self.c_inc))
+        self.c_sca_d.copy_(torch.as_tensor(self.c_sca))
         ci = (ct.c_double * self.S)(*self.c_inc)
         cs = (ct.c_double * self.S)(*self.c_sca)
         N.check(self.lib.pdf_set_norms(self.ctx, ci, cs, _stream()))
@@ -272,8 +280,10 @@ class DeviceProblem:
     def _masked(self, rows):
         return rows if self.mask is None else rows * self.mask
 
-    def bp_initialize(self):
-        """Backprojection chi0 and R0 per scene (reconstruct.py:52-71)."""
+    def bp_initialize(self, check: bool = True):
+        """Backprojection chi0 and R0 per scene (reconstruct.py:52-71).  check=False
+        leaves the pole test as a device flag (`self.pole_flag`, raised later
+        by the caller) so the sequence has no host synchronisation."""
         d = self._masked(self.data)
         b = self.gs_adjoint(d)
         w = self._masked(self.gs_forward(b))
@@ -285,7 +295,8 @@ class DeviceProblem:
         e = self._einc_b() + self.apply_gd(j)
         chi0 = self._pixel_ls(j, e)
         q = self.beta * chi0 + 1.0
-        if bool((q.abs() < 1e-14).any()):
+        self.pole_flag = (q.abs() < 1e-14).any()
+        if check and bool(self.pole_flag):
             raise PoleError("beta*chi + 1 vanishes at some pixel")
         return chi0, self.beta * chi0 / q
 
@@ -297,12 +308,13 @@ class DeviceProblem:
         den = torch.sum((e.conj() * e).real, dim=1) + eps[:, None, None]
         return num / den
 
-    def init_alpha(self, r0: torch.Tensor) -> torch.Tensor:
-        """One exact line-search step of the frozen-R quadratic (reconstruct.py:74-153)."""
+    def init_alpha(self, r0: torch.Tensor, check: bool = True) -> torch.Tensor:
+        """One exact line-search step of the frozen-R quadratic (reconstruct.py:74-153).
+        check=False leaves the zero-gradient test as `self.zero_grad_flag`."""
         M2 = self.M * self.M
         beta = self.beta
-        c_inc = torch.as_tensor(self.c_inc, device=self.device)[:, None, None, None]
-        c_sca = torch.as_tensor(self.c_sca, device=self.device)[:, None, None]
+        c_inc = self.c_inc_d[:, None, None, None]
+        c_sca = self.c_sca_d[:, None, None]
         r0b = r0[:, None]
         einc = self._einc_b()
         gs_r = (2.0 / c_inc) * (r0b * einc)
@@ -318,7 +330,8 @@ class DeviceProblem:
              + torch.sum((rr.conj() * rr).real, dim=(1, 2)) / c_sca.view(-1))
         g2 = torch.sum((g.conj() * g).real, dim=(1, 2))
         ok = (q > 0) & (g2 > 0)
-        if not bool(ok.all()):
+        self.zero_grad_flag = ~ok.all()
+        if check and bool(self.zero_grad_flag):
             warnings.warn("zero initial gradient; starting from zero coefficients")
         t = torch.where(ok, g2 / (2.0 * torch.where(ok, q, torch.ones_like(q))), torch.zeros_like(q))
         return -t[:, None, None] * g
