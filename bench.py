@@ -348,10 +348,11 @@ def ncu_traffic(phase: str, split_bwd: bool = False):
             ids = ids[(0 if phase == "bwd_l3" else 1)::2]          # g_h launches: layer 3, layer 2
             vals = [per[i] for i in ids]
         elif split_bwd and phase == "bwd_l1":
-            # one Adam launch over all layers, or three (layer 1 + the side branch's 3 / 2) in the graph
-            n3 = len(ids) // 3 if len(ids) % 3 == 0 and "net_adam_x" in key else 0
-            vals = [per[ids[3 * q]] + per[ids[3 * q + 1]] + per[ids[3 * q + 2]] for q in range(n3)] if n3 else \
-                [per[i] for i in ids]
+            # one Adam launch over all layers (un-graphed) or three per iteration (layer 1 + the side
+            # branch's layers 3 / 2 in the graph): DRAM bytes per iteration = all Adam launches / iterations
+            gh = sum(1 for r in rows[hi + 1:] if "net_gh_" in r[ki] and r[mi] == "dram__bytes_read.sum")
+            iters = gh // 2
+            vals = [sum(per.values()) / iters] if iters else [per[i] for i in ids]
         else:
             if phase in LAYER_POS:
                 ids = ids[LAYER_POS[phase]::3]
