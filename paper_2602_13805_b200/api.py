@@ -20,6 +20,7 @@ reference.  Every numerical step runs in libpdfb200.so on the GPU.
 """
 from __future__ import annotations
 
+import os
 import time
 import warnings
 from concurrent.futures import ThreadPoolExecutor
@@ -395,14 +396,12 @@ def count_components(eps_map: np.ndarray, threshold: float) -> int:
     return int(n)
 
 
-def _theta0(seeds, m0_eff: int, workers: int = 8) -> np.ndarray:
-    """Reference-identical initial weights per scene (numpy PCG64 draws on the host)."""
-    def one(s):
-        return flatten_params(init_network(m0_eff, np.random.default_rng(int(s))))
-    if len(seeds) == 1:
-        return one(seeds[0])[None]
-    with ThreadPoolExecutor(max_workers=min(workers, len(seeds))) as ex:
-        return np.stack(list(ex.map(one, seeds)))
+def _theta0(seeds, m0_eff: int) -> np.ndarray:
+    """Reference-identical initial weights per scene (numpy PCG64 draws on the host cores)."""
+    out = np.empty((len(seeds), _flat_size(m0_eff)))
+    for f in _theta0_async(seeds, m0_eff, out):
+        f.result()
+    return out
 
 
 _THETA_POOL = None
@@ -414,15 +413,33 @@ def _flat_size(m0_eff: int) -> int:
     return h * d0 + h + h * h + h + d0 * h + d0
 
 
-def _theta0_async(seeds, m0_eff: int, out: np.ndarray, workers: int = 8):
-    """Start the per-scene draws of _theta0 into `out` rows; returns futures."""
+def init_flat_into(row: np.ndarray, m0_eff: int, seed: int) -> None:
+    """flatten_params(init_network(m0_eff, default_rng(seed))) written straight
+    into `row` (network.py:53-71): Generator.normal(0, s) is s * standard_normal
+    draw for draw, so the standard normals are drawn into the weight slices in
+    the reference's order (w1, then w2; w3 and the biases are zero)."""
+    rng = np.random.default_rng(int(seed))
+    d0 = 2 * m0_eff
+    h = 2 * d0
+    o = 0
+    for fi, fo, zero in ((d0, h, False), (h, h, False), (h, d0, True)):
+        w = row[o:o + fo * fi].reshape(fo, fi)
+        if zero:
+            w.fill(0.0)
+        else:
+            rng.standard_normal(out=w)
+            w *= np.sqrt(1.0 / fi)
+        o += fo * fi
+        row[o:o + fo] = 0.0
+        o += fo
+
+
+def _theta0_async(seeds, m0_eff: int, out: np.ndarray, workers: int | None = None):
+    """Start the per-scene draws of _theta0 into `out` rows (all host cores); returns futures."""
     global _THETA_POOL
     if _THETA_POOL is None:
-        _THETA_POOL = ThreadPoolExecutor(max_workers=workers)
-
-    def one(i, s):
-        out[i] = flatten_params(init_network(m0_eff, np.random.default_rng(int(s))))
-    return [_THETA_POOL.submit(one, i, s) for i, s in enumerate(seeds)]
+        _THETA_POOL = ThreadPoolExecutor(max_workers=workers or min(32, os.cpu_count() or 8))
+    return [_THETA_POOL.submit(init_flat_into, out[i], m0_eff, s) for i, s in enumerate(seeds)]
 
 
 class BatchReconstructor:

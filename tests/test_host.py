@@ -253,3 +253,15 @@ def test_incidence_shard_reducer_with_gloo(tmp_path):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "REDUCER OK" in out.stdout
+
+
+def test_initial_weights_drawn_in_place_match_reference_order():
+    """init_flat_into (draws straight into the flat parameter row) is bitwise
+    flatten_params(init_network(m0, default_rng(seed))) (network.py:53-71)."""
+    from paper_2602_13805_b200.api import _flat_size, _theta0, flatten_params, init_flat_into, init_network
+    for m0, seed in ((36, 0), (100, 7), (256, 3)):
+        row = np.empty(_flat_size(m0))
+        init_flat_into(row, m0, seed)
+        assert np.array_equal(row, flatten_params(init_network(m0, np.random.default_rng(seed))))
+    th = _theta0([4, 5], 36)
+    assert np.array_equal(th[1], flatten_params(init_network(36, np.random.default_rng(5))))
