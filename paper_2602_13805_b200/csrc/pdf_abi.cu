@@ -207,9 +207,12 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   c->xbwd = bx && d->dtype == PDF_F64 && c->rows <= 80 && (bx == 2 || (long long)d->S * (c->H / 8) <= 4 * 148);
   if (c->dgemm) {
     const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
+    // chunk granularity: 16 coefficients for the DMMA kernel (4 k-steps), the
+    // staged sub-tile for the float32 one
+    const int gk = d->dtype == PDF_F64 ? 16 : DG_KC;
     int want = std::max(1, (2 * 148 + d->S - 1) / d->S);
-    want = std::max(1, std::min(want, npix / DG_KC));
-    c->dg_chunk = ((npix + want - 1) / want + DG_KC - 1) / DG_KC * DG_KC;
+    want = std::max(1, std::min(want, npix / gk));
+    c->dg_chunk = ((npix + want - 1) / want + gk - 1) / gk * gk;
     c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
     const int ntp = ((d->n + 7) / 8) * ((d->R + 8 * DM_NTL - 1) / (8 * DM_NTL));
     c->dg_nq = std::max(1, std::min(4, 8 / ntp));
