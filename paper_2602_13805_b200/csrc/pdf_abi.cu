@@ -510,8 +510,18 @@ static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
     const dim3 grid((N + 7) / 8, 1, S);
     const size_t smem = fwd_x_smem_bytes(MT, K);
     void* args[] = {&a};
-    cudaError_t e = MT == 1 ? plain_launch(net_fwd_x_kernel<1>, grid, dim3(XW * 32), smem, st, args)
-                            : plain_launch(net_fwd_x_kernel<2>, grid, dim3(XW * 32), smem, st, args);
+    // x multicast over clusters of 4 CTAs (PDF_FWD_MC=1 stages it per CTA)
+    static const int mc = env_int("PDF_FWD_MC", 4);
+    cudaError_t e;
+    if (mc == 4 && grid.x % 4 == 0) {
+      e = MT == 1 ? prep(net_fwd_x_kernel<1, 4>, smem) : prep(net_fwd_x_kernel<2, 4>, smem);
+      if (e == cudaSuccess)
+        e = MT == 1 ? launch_cluster(net_fwd_x_kernel<1, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args)
+                    : launch_cluster(net_fwd_x_kernel<2, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args);
+    } else {
+      e = MT == 1 ? plain_launch(net_fwd_x_kernel<1, 1>, grid, dim3(XW * 32), smem, st, args)
+                  : plain_launch(net_fwd_x_kernel<2, 1>, grid, dim3(XW * 32), smem, st, args);
+    }
     if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net fwd (x): ") + cudaGetErrorString(e));
     return PDF_OK;
   }
@@ -813,8 +823,17 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
   const dim3 grid((K + 7) / 8, 1, c->d.S);
   const size_t smem = gh_x_smem_bytes(MT, N);
   void* args[] = {&a};
-  cudaError_t e = MT == 1 ? plain_launch(net_gh_x_kernel<1>, grid, dim3(XW * 32), smem, st, args)
-                          : plain_launch(net_gh_x_kernel<2>, grid, dim3(XW * 32), smem, st, args);
+  static const int mc = env_int("PDF_FWD_MC", 4);   // g_z multicast over clusters of 4 (as the forward)
+  cudaError_t e;
+  if (mc == 4 && grid.x % 4 == 0) {
+    e = MT == 1 ? prep(net_gh_x_kernel<1, 4>, smem) : prep(net_gh_x_kernel<2, 4>, smem);
+    if (e == cudaSuccess)
+      e = MT == 1 ? launch_cluster(net_gh_x_kernel<1, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args)
+                  : launch_cluster(net_gh_x_kernel<2, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args);
+  } else {
+    e = MT == 1 ? plain_launch(net_gh_x_kernel<1, 1>, grid, dim3(XW * 32), smem, st, args)
+                : plain_launch(net_gh_x_kernel<2, 1>, grid, dim3(XW * 32), smem, st, args);
+  }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net g_h (x): ") + cudaGetErrorString(e));
   return PDF_OK;
 }

@@ -185,10 +185,14 @@ __host__ __device__ constexpr size_t fwd_x_smem_bytes(int MT, int K) {
   return (xs + red) * sizeof(double);
 }
 
-template <int MT>
+// MC > 1: a cluster of MC CTAs along x shares the input block: each CTA
+// copies every MC-th row with one bulk copy multicast to all of them (TMA
+// engine), so the L2 serves x once per cluster instead of once per CTA.
+template <int MT, int MC>
 __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double> a) {
   constexpr int RPM = 8 * MT, THR = XW * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long xbar;
   const int K = a.K, N = a.N, rows = a.rows, XP = K + 2;
   double* Xs = reinterpret_cast<double*>(smem_raw);     // [RPM][K + 2]
   double* red = Xs + (size_t)RPM * XP;                  // [XW][RPM][8]
@@ -214,19 +218,40 @@ __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double
       }
   };
   tl_mark(a.tl, 0);
+  if constexpr (MC > 1) {
+    // padding rows (never copied) read as zero; barrier initialised before any peer's copy lands
+    for (int i = tid; i < (RPM - rows) * XP; i += THR) Xs[(size_t)rows * XP + i] = 0.0;
+    if (tid == 0) {
+      mbar_init(&xbar, 1);
+      mbar_fence_init_cluster();
+    }
+    cg::this_cluster().sync();
+  }
   if (a.w_early) loadW();
   pdl_wait();
   tl_mark(a.tl, 1);
   if (!a.w_early) loadW();
   if (a.step && tid == 0 && blockIdx.x == 0 && scene == 0) atomicAdd(a.step, 1);
-  const int seg = K / 2;
-  for (int i = tid; i < RPM * seg; i += THR) {
-    const int r = i / seg, s2 = i - r * seg;
-    const bool ok = r < rows;
-    cp_async16(Xs + (size_t)r * XP + 2 * s2, ok ? X + (size_t)r * K + 2 * s2 : X, ok);
+  if constexpr (MC > 1) {
+    const unsigned rank = cg::this_cluster().block_rank();
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&xbar, (unsigned)(rows * K * sizeof(double)));
+      for (int r = (int)rank; r < rows; r += MC)
+        bulk_copy_multicast(Xs + (size_t)r * XP, X + (size_t)r * K, (unsigned)(K * sizeof(double)), &xbar,
+                            (unsigned short)((1u << MC) - 1));
+    }
+    while (!mbar_try_wait(&xbar, 0)) {
+    }
+  } else {
+    const int seg = K / 2;
+    for (int i = tid; i < RPM * seg; i += THR) {
+      const int r = i / seg, s2 = i - r * seg;
+      const bool ok = r < rows;
+      cp_async16(Xs + (size_t)r * XP + 2 * s2, ok ? X + (size_t)r * K + 2 * s2 : X, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
   }
-  cp_async_commit();
-  cp_async_wait<0>();
   __syncthreads();
   pdl_trigger();
   double acc[MT][2];
@@ -536,10 +561,11 @@ __host__ __device__ constexpr size_t gh_x_smem_bytes(int MT, int N) {
 }
 
 // CTA = one k-tile of 8 outputs of g_h; its XW warps split the n reduction
-template <int MT>
+template <int MT, int MC>
 __global__ void __launch_bounds__(XW * 32, 1) net_gh_x_kernel(NetBwdArgs<double> a) {
   constexpr int RPM = 8 * MT, THR = XW * 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long gbar;
   const int K = a.K, N = a.N, rows = a.rows, GP = N + 2;
   double* Gz = reinterpret_cast<double*>(smem_raw);   // [RPM][N + 2]
   double* red = Gz + (size_t)RPM * GP;                 // [XW][RPM][8]
@@ -560,17 +586,37 @@ __global__ void __launch_bounds__(XW * 32, 1) net_gh_x_kernel(NetBwdArgs<double>
     const int n = nb + 4 * q + t;
     b[q] = (kok && n < ne) ? W[(size_t)n * K + k0 + g] : 0.0;
   }
+  if constexpr (MC > 1) {   // g_z multicast over the cluster (as net_fwd_x_kernel's input block)
+    for (int i = tid; i < (RPM - rows) * GP; i += THR) Gz[(size_t)rows * GP + i] = 0.0;
+    if (tid == 0) {
+      mbar_init(&gbar, 1);
+      mbar_fence_init_cluster();
+    }
+    cg::this_cluster().sync();
+  }
   pdl_wait();
   tl_mark(a.tl, 1);
   const double* __restrict__ gz = a.gz + scene * a.gz_ss;
-  const int seg = N / 2;
-  for (int i = tid; i < RPM * seg; i += THR) {
-    const int r = i / seg, s2 = i - r * seg;
-    const bool ok = r < rows;
-    cp_async16(Gz + (size_t)r * GP + 2 * s2, ok ? gz + (size_t)r * N + 2 * s2 : gz, ok);
+  if constexpr (MC > 1) {
+    const unsigned rank = cg::this_cluster().block_rank();
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&gbar, (unsigned)(rows * N * sizeof(double)));
+      for (int r = (int)rank; r < rows; r += MC)
+        bulk_copy_multicast(Gz + (size_t)r * GP, gz + (size_t)r * N, (unsigned)(N * sizeof(double)), &gbar,
+                            (unsigned short)((1u << MC) - 1));
+    }
+    while (!mbar_try_wait(&gbar, 0)) {
+    }
+  } else {
+    const int seg = N / 2;
+    for (int i = tid; i < RPM * seg; i += THR) {
+      const int r = i / seg, s2 = i - r * seg;
+      const bool ok = r < rows;
+      cp_async16(Gz + (size_t)r * GP + 2 * s2, ok ? gz + (size_t)r * N + 2 * s2 : gz, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
   }
-  cp_async_commit();
-  cp_async_wait<0>();
   __syncthreads();
   pdl_trigger();
   double acc[MT][2];
