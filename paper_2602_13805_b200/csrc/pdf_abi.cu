@@ -513,7 +513,12 @@ static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
     // x multicast over clusters of 4 CTAs (PDF_FWD_MC=1 stages it per CTA)
     static const int mc = env_int("PDF_FWD_MC", 4);
     cudaError_t e;
-    if (mc == 4 && grid.x % 4 == 0) {
+    if (mc == 8 && grid.x % 8 == 0) {
+      e = MT == 1 ? prep(net_fwd_x_kernel<1, 8>, smem) : prep(net_fwd_x_kernel<2, 8>, smem);
+      if (e == cudaSuccess)
+        e = MT == 1 ? launch_cluster(net_fwd_x_kernel<1, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args)
+                    : launch_cluster(net_fwd_x_kernel<2, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args);
+    } else if (mc >= 4 && grid.x % 4 == 0) {
       e = MT == 1 ? prep(net_fwd_x_kernel<1, 4>, smem) : prep(net_fwd_x_kernel<2, 4>, smem);
       if (e == cudaSuccess)
         e = MT == 1 ? launch_cluster(net_fwd_x_kernel<1, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args)
@@ -825,7 +830,12 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
   void* args[] = {&a};
   static const int mc = env_int("PDF_FWD_MC", 4);   // g_z multicast over clusters of 4 (as the forward)
   cudaError_t e;
-  if (mc == 4 && grid.x % 4 == 0) {
+  if (mc == 8 && grid.x % 8 == 0) {
+    e = MT == 1 ? prep(net_gh_x_kernel<1, 8>, smem) : prep(net_gh_x_kernel<2, 8>, smem);
+    if (e == cudaSuccess)
+      e = MT == 1 ? launch_cluster(net_gh_x_kernel<1, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args)
+                  : launch_cluster(net_gh_x_kernel<2, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args);
+  } else if (mc >= 4 && grid.x % 4 == 0) {
     e = MT == 1 ? prep(net_gh_x_kernel<1, 4>, smem) : prep(net_gh_x_kernel<2, 4>, smem);
     if (e == cudaSuccess)
       e = MT == 1 ? launch_cluster(net_gh_x_kernel<1, 4>, grid, dim3(XW * 32), smem, st, dim3(4, 1, 1), args)
