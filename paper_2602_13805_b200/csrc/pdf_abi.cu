@@ -438,7 +438,9 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   constexpr int epc = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
   if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
   void* args[] = {&p};
-  cudaError_t e = plain_launch(pixel_kernel<T, GRAD>, grid, dim3(PIX_NW * 32), smem, st, args);
+  const bool ilp2 = (long long)grid.x * grid.y * grid.z <= 4 * 148;   // latency regime
+  cudaError_t e = ilp2 ? plain_launch(pixel_kernel<T, GRAD, true>, grid, dim3(PIX_NW * 32), smem, st, args)
+                       : plain_launch(pixel_kernel<T, GRAD, false>, grid, dim3(PIX_NW * 32), smem, st, args);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("pixel kernel: ") + cudaGetErrorString(e));
   return PDF_OK;

@@ -50,7 +50,9 @@ constexpr int PIX_NW = 8;          // warps per CTA
 template <typename T>
 __device__ __forceinline__ T amag(C<T> z) { return sqrt_<T>(cabs2<T>(z)); }
 
-template <typename T, bool GRAD>
+// ILP2: the halo pass loads two views per pass (latency regime: few CTAs;
+// doubles the registers, so batches keep one view per pass)
+template <typename T, bool GRAD, bool ILP2 = false>
 __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
   constexpr int W = PIX_TX + 2;
   __shared__ C<T> pnum[PIX_NW][3 * W];
@@ -105,7 +107,27 @@ __global__ void __launch_bounds__(PIX_NW * 32) pixel_kernel(PixelArgs<T> a) {
       num[q] = czero<T>();
       den[q] = T(0);
     }
-    for (int i = warp; i < n; i += nw) {
+    // two views per pass: 16 loads in flight per thread, added in view order
+    int i = warp;
+    for (; ILP2 && i + nw < n; i += 2 * nw) {
+      C<T> j[2][QH], e[2][QH];
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < QH; ++q) {
+          const size_t o = (vbase + i + u * nw) * img + pix[q];
+          j[u][q] = ok[q] ? a.J[o] : czero<T>();
+          e[u][q] = ok[q] ? a.E[o] : czero<T>();
+        }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < QH; ++q) {
+          num[q] = cadd<T>(num[q], cmulc<T>(j[u][q], e[u][q]));
+          den[q] += cabs2<T>(e[u][q]);
+        }
+    }
+    for (; i < n; i += nw) {
       C<T> j[QH], e[QH];
 #pragma unroll
       for (int q = 0; q < QH; ++q) {
