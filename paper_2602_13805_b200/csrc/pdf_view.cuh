@@ -172,25 +172,6 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
     for (int i = tid; i < rp * M / EPC; i += blockDim.x) cp_async16(s.pre + i * EPC, src + i * EPC, true);
   }
   cp_async_commit();
-  if constexpr (MODE == VIEW_BWD) {
-    // G_S^H g_rows through H (pdf_aux.cuh) for my outputs i = rank + CS*o:
-    // g_rows was finalised two launches back (view_fwd / data term), so this
-    // runs before the dependency wait; warp w sums receivers w, w + nw, ...
-    const C<T>* grow = a.grows + (size_t)v * a.R;
-    const int nout = (M0 - rank + CS - 1) / CS;
-    C<T>* scr = s.dsum + M0 / CS + 1;   // [nw][32]
-    for (int ob = 0; ob < nout; ob += 32) {
-      const int o = ob + lane, i = rank + CS * o;
-      if (o < nout) scr[warp * 32 + lane] = data_adjoint_at<T>(grow, a.hs, a.R, M0, corner_slot(i / K, i % K, mf), warp, nw);
-      __syncthreads();
-      if (warp == 0 && o < nout) {
-        C<T> d = czero<T>();
-        for (int w = 0; w < nw; ++w) d = cadd<T>(d, scr[w * 32 + lane]);
-        s.dsum[o] = d;
-      }
-      __syncthreads();
-    }
-  }
   pdl_wait();   // everything below reads the previous kernel's outputs
   tl_mark(a.tl, 1);
 
@@ -290,6 +271,25 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   // other CTAs finish theirs, and the wait acquires everyone's scatter.
   tl_stage(a.tl, 1);
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  if constexpr (MODE == VIEW_BWD) {
+    // G_S^H g_rows through H (pdf_aux.cuh) for my outputs i = rank + CS*o,
+    // while the other CTAs finish their stage-A scatter; warp w sums
+    // receivers w, w + nw, ...
+    const C<T>* grow = a.grows + (size_t)v * a.R;
+    const int nout = (M0 - rank + CS - 1) / CS;
+    C<T>* scr = s.dsum + M0 / CS + 1;   // [nw][32]
+    for (int ob = 0; ob < nout; ob += 32) {
+      const int o = ob + lane, i = rank + CS * o;
+      if (o < nout) scr[warp * 32 + lane] = data_adjoint_at<T>(grow, a.hs, a.R, M0, corner_slot(i / K, i % K, mf), warp, nw);
+      __syncthreads();
+      if (warp == 0 && o < nout) {
+        C<T> d = czero<T>();
+        for (int w = 0; w < nw; ++w) d = cadd<T>(d, scr[w * 32 + lane]);
+        s.dsum[o] = d;
+      }
+      __syncthreads();
+    }
+  }
   if (MODE == VIEW_FWD && a.do_data) {
     // D[r] = sum_m alpha[m] H[r][m] - d[r] (masked), g_rows = 2 D mask / c_sca
     const C<T>* al = a.alpha + (size_t)v * M0;
