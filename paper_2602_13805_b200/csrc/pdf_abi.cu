@@ -134,7 +134,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   }
   c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
   c->ghp = c->xbwd ? w.take<double>((size_t)d.S * GH_NSL * c->rows * c->H) : nullptr;
-  c->ticket = c->xbwd ? w.take<int>((size_t)d.S * (c->H / GT_KB + 1)) : nullptr;
+  c->ticket = c->xbwd ? w.take<int>((size_t)d.S * (c->H / 64 + 1)) : nullptr;
   c->h1b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
   c->h2b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
   c->tsnap = c->xbwd ? w.take<int>(1) : nullptr;
@@ -778,10 +778,11 @@ static int split_finalize(pdf_ctx* c, double* bd, double* trace, cudaStream_t st
 // split network backward (latency regime, float64): g_h of layers 3 and 2,
 // then g_W + Adam of all layers in one launch
 template <int MT>
-static cudaError_t gh_t_launch(dim3 grid, GhArgs& a, cudaStream_t st) {
-  const size_t smem = gh_t_smem_bytes(MT);
+static cudaError_t gh_t_launch(dim3 grid, int ktw, GhArgs& a, cudaStream_t st) {
   void* args[] = {&a};
-  return plain_launch(net_gh_t_kernel<MT>, grid, dim3(XW * 32), smem, st, args);
+  if (ktw == 4) return plain_launch(net_gh_t_kernel<MT, 4>, grid, dim3(XW * 32), gh_t_smem_bytes(MT, 4), st, args);
+  if (ktw == 2) return plain_launch(net_gh_t_kernel<MT, 2>, grid, dim3(XW * 32), gh_t_smem_bytes(MT, 2), st, args);
+  return plain_launch(net_gh_t_kernel<MT, 1>, grid, dim3(XW * 32), gh_t_smem_bytes(MT, 1), st, args);
 }
 
 static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, int N, const double* theta,
@@ -792,7 +793,13 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
     GhArgs g = {};
     g.tl = g_tl_cur;
     g.rows = c->rows; g.K = K; g.N = N;
-    const int kbs = (K + GT_KB - 1) / GT_KB;
+    // 4 k-tiles per warp when the k-blocks x slices still cover the SMs
+    // (config 5: 4096 columns), else 1 (config 3)
+    static const int ktw_env = env_int("PDF_GH_KTW", 0);
+    // (2 / 4 k-tiles per warp reuse the A fragments from registers but were
+    // measured slower on configs 3 and 5: occupancy; PDF_GH_KTW for experiments)
+    const int ktw = ktw_env ? ktw_env : 1;
+    const int kbs = (K + gt_kb(ktw) - 1) / gt_kb(ktw);
     int nsl = 1;
     while (nsl < GH_NSL && (long long)kbs * nsl * c->d.S < 2 * 148 && N / (2 * nsl) >= 2 * GT_NC) nsl *= 2;
     g.nsl = nsl;
@@ -805,16 +812,16 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
     const dim3 grid(kbs, nsl, c->d.S);
     cudaError_t e;
     switch (MT) {
-      case 1: e = gh_t_launch<1>(grid, g, st); break;
-      case 2: e = gh_t_launch<2>(grid, g, st); break;
-      case 3: e = gh_t_launch<3>(grid, g, st); break;
-      case 4: e = gh_t_launch<4>(grid, g, st); break;
-      case 5: e = gh_t_launch<5>(grid, g, st); break;
-      case 6: e = gh_t_launch<6>(grid, g, st); break;
-      case 7: e = gh_t_launch<7>(grid, g, st); break;
-      case 8: e = gh_t_launch<8>(grid, g, st); break;
-      case 9: e = gh_t_launch<9>(grid, g, st); break;
-      default: e = gh_t_launch<10>(grid, g, st); break;
+      case 1: e = gh_t_launch<1>(grid, ktw, g, st); break;
+      case 2: e = gh_t_launch<2>(grid, ktw, g, st); break;
+      case 3: e = gh_t_launch<3>(grid, ktw, g, st); break;
+      case 4: e = gh_t_launch<4>(grid, ktw, g, st); break;
+      case 5: e = gh_t_launch<5>(grid, ktw, g, st); break;
+      case 6: e = gh_t_launch<6>(grid, ktw, g, st); break;
+      case 7: e = gh_t_launch<7>(grid, ktw, g, st); break;
+      case 8: e = gh_t_launch<8>(grid, ktw, g, st); break;
+      case 9: e = gh_t_launch<9>(grid, ktw, g, st); break;
+      default: e = gh_t_launch<10>(grid, ktw, g, st); break;
     }
     if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net g_h (tiled): ") + cudaGetErrorString(e));
     return PDF_OK;
@@ -1009,7 +1016,7 @@ static int create_impl(pdf_ctx* c, void* ws, size_t bytes, cudaStream_t st) {
   CK_CUDA(cudaMemcpyAsync(c->c_sca, c->c_sca_h.data(), c->d.S * sizeof(double), cudaMemcpyHostToDevice, st));
   CK_CUDA(cudaMemsetAsync(c->err, 0, c->d.S * sizeof(int), st));
   CK_CUDA(cudaMemsetAsync(c->step, 0, 2 * sizeof(int), st));
-  if (c->ticket) CK_CUDA(cudaMemsetAsync(c->ticket, 0, (size_t)c->d.S * (c->H / GT_KB + 1) * sizeof(int), st));
+  if (c->ticket) CK_CUDA(cudaMemsetAsync(c->ticket, 0, (size_t)c->d.S * (c->H / 64 + 1) * sizeof(int), st));
   const int PP = c->P * c->P;
   permute_khat_kernel<T><<<(PP + 255) / 256, 256, 0, st>>>((const C<T>*)c->d.gd_kernel_hat, (C<T>*)c->khat, c->P,
                                                             c->large && c->E >= 4 ? 1 : 0);

@@ -793,11 +793,16 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
 // of 32 staged with cp.async (double-buffered), split over grid.y slices;
 // the slice partials are added in slice order by the last CTA of each
 // k-block (atomic ticket, self-resetting), which applies (1 - h^2).
-constexpr int GT_NC = 32, GT_KB = XW * 8;
+constexpr int GT_NC = 32;
 constexpr int GH_NSL = 16;   // max n slices
-constexpr int GT_GP = GT_NC + 4, GT_WP = GT_KB + 4;   // pitches = 4 mod 16
-__host__ __device__ constexpr size_t gh_t_smem_bytes(int MT) {
-  return ((size_t)2 * 8 * MT * GT_GP + (size_t)2 * GT_NC * GT_WP) * sizeof(double);
+constexpr int GT_GP = GT_NC + 4;   // pitch = 4 mod 16
+// KTW k-tiles of 8 per warp (CTA = XW * 8 * KTW outputs): the A fragments of
+// all rows are reused from registers across them, so shared-memory traffic
+// per DMMA drops from ~1 fragment to (MT + KTW) / (MT KTW)
+__host__ __device__ constexpr int gt_kb(int KTW) { return XW * 8 * KTW; }
+__host__ __device__ constexpr int gt_wp(int KTW) { return gt_kb(KTW) + 4; }
+__host__ __device__ constexpr size_t gh_t_smem_bytes(int MT, int KTW) {
+  return ((size_t)2 * 8 * MT * GT_GP + (size_t)2 * GT_NC * gt_wp(KTW)) * sizeof(double);
 }
 
 struct GhArgs {
@@ -807,33 +812,33 @@ struct GhArgs {
   const double* theta; long long th_ss, w_off;
   double* gzprev; long long gzp_ss;
   double* part;                      // [S][nsl][rows][K]
-  int* ticket;                       // [S][K / GT_KB]
+  int* ticket;                       // [S][K / 64 + 1]
   int tl;
 };
 
-template <int MT>
+template <int MT, int KTW>
 __global__ void __launch_bounds__(XW * 32) net_gh_t_kernel(GhArgs a) {
-  constexpr int RPM = 8 * MT, THR = XW * 32;
+  constexpr int RPM = 8 * MT, THR = XW * 32, KB = gt_kb(KTW), WP = gt_wp(KTW);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Gs = reinterpret_cast<double*>(smem_raw);   // [2][RPM][GT_GP]
-  double* Ws = Gs + 2 * RPM * GT_GP;                   // [2][GT_NC][GT_WP]
+  double* Ws = Gs + 2 * RPM * GT_GP;                   // [2][GT_NC][WP]
   __shared__ int last_s;
   const int K = a.K, N = a.N, rows = a.rows;
   const int scene = blockIdx.z, sl = blockIdx.y, kb = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int k0 = kb * GT_KB;
+  const int k0 = kb * KB;
   const int n0 = sl * a.ns, n1 = min(N, n0 + a.ns);
   const double* __restrict__ W = a.theta + scene * a.th_ss + a.w_off;
   const double* __restrict__ gz = a.gz + scene * a.gz_ss;
   tl_mark(a.tl, 0);
   auto stage_w = [&](int c, int b) {
     const int nc = n0 + c * GT_NC;
-    double* dst = Ws + b * GT_NC * GT_WP;
-    for (int i = tid; i < GT_NC * GT_KB / 2; i += THR) {
-      const int r = i / (GT_KB / 2), sg = i % (GT_KB / 2), n = nc + r, k = k0 + 2 * sg;
+    double* dst = Ws + b * GT_NC * WP;
+    for (int i = tid; i < GT_NC * KB / 2; i += THR) {
+      const int r = i / (KB / 2), sg = i % (KB / 2), n = nc + r, k = k0 + 2 * sg;
       const bool ok = n < n1 && k < K;
-      cp_async16(dst + r * GT_WP + 2 * sg, ok ? W + (size_t)n * K + k : W, ok);
+      cp_async16(dst + r * WP + 2 * sg, ok ? W + (size_t)n * K + k : W, ok);
     }
   };
   auto stage_g = [&](int c, int b) {
@@ -852,21 +857,29 @@ __global__ void __launch_bounds__(XW * 32) net_gh_t_kernel(GhArgs a) {
   tl_mark(a.tl, 1);
   if (nch > 0) stage_g(0, 0);
   cp_async_commit();
-  double acc[MT][2];
+  double acc[MT][KTW][2];
 #pragma unroll
-  for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < KTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int c = 0; c < nch; ++c) {
     if (c + 1 < nch) { stage_w(c + 1, (c + 1) & 1); stage_g(c + 1, (c + 1) & 1); }
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* G = Gs + (c & 1) * RPM * GT_GP;
-    const double* Wc = Ws + (c & 1) * GT_NC * GT_WP;
+    const double* Wc = Ws + (c & 1) * GT_NC * WP;
 #pragma unroll
     for (int q = 0; q < GT_NC / 4; ++q) {
-      const double bv = Wc[(4 * q + t) * GT_WP + warp * 8 + g];      // B[t][g] = W[n + t][k + g]
+      double bv[KTW], av[MT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) dmma(acc[i][0], acc[i][1], G[(8 * i + g) * GT_GP + 4 * q + t], bv);
+      for (int j = 0; j < KTW; ++j) bv[j] = Wc[(4 * q + t) * WP + (warp * KTW + j) * 8 + g];   // B[t][g] = W[n + t][k + g]
+#pragma unroll
+      for (int i = 0; i < MT; ++i) av[i] = G[(8 * i + g) * GT_GP + 4 * q + t];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < KTW; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
     }
     __syncthreads();
   }
@@ -876,10 +889,12 @@ __global__ void __launch_bounds__(XW * 32) net_gh_t_kernel(GhArgs a) {
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int r = 8 * i + g, k = k0 + warp * 8 + 2 * t + cc;
-      if (r < rows && k < K) P[(size_t)r * K + k] = acc[i][cc];
-    }
+    for (int j = 0; j < KTW; ++j)
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int r = 8 * i + g, k = k0 + (warp * KTW + j) * 8 + 2 * t + cc;
+        if (r < rows && k < K) P[(size_t)r * K + k] = acc[i][j][cc];
+      }
   __threadfence();
   __syncthreads();
   if (tid == 0) {
@@ -892,8 +907,8 @@ __global__ void __launch_bounds__(XW * 32) net_gh_t_kernel(GhArgs a) {
   if (last_s) {
     __threadfence();
     const double* __restrict__ hin = a.hin + scene * a.hin_ss;
-    for (int e = tid; e < rows * GT_KB; e += THR) {
-      const int r = e / GT_KB, k = k0 + e % GT_KB;
+    for (int e = tid; e < rows * KB; e += THR) {
+      const int r = e / KB, k = k0 + e % KB;
       if (k >= K) continue;
       double s = 0.0;
       for (int q = 0; q < a.nsl; ++q)
