@@ -265,3 +265,14 @@ def test_initial_weights_drawn_in_place_match_reference_order():
         assert np.array_equal(row, flatten_params(init_network(m0, np.random.default_rng(seed))))
     th = _theta0([4, 5], 36)
     assert np.array_equal(th[1], flatten_params(init_network(36, np.random.default_rng(5))))
+
+
+def test_loss_trace_is_a_lazy_sequence_of_breakdowns():
+    from paper_2602_13805_b200.api import LossBreakdown, LossTrace
+    rows = np.arange(18, dtype=float).reshape(3, 6)      # state, data, bound, tv, bridge, total
+    tr = LossTrace(rows, (1e-3, 1e-5, 1e-5))
+    assert len(tr) == 3
+    assert tr[1] == LossBreakdown.from_row(rows[1], (1e-3, 1e-5, 1e-5))
+    assert [b.total for b in tr] == [5.0, 11.0, 17.0]
+    assert tr[-1].state == 12.0 and tr[1:][0].data == 7.0
+    assert np.array_equal(tr.as_array(), rows)
