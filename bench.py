@@ -467,7 +467,12 @@ def run_ours(args, d: Dist):
     proof = path_roofline(dev.M, dev.n, dev.R, int(dev.n_params), fp64_peak_tflops, peaks["hbm_gbs"], m0=4 * dev.mf ** 2)
     proof["frac"] = proof["t_roof_us_per_scene_iter"] / (1e3 * ms_step / k)
     roof.update({"kernel": dom, "algorithmic_per_launch": work, "launch_ms": phases[dom],
-                 "traffic": ncu_traffic(dom, getattr(dev, "split_bwd", False)), "share_of_step": share[dom]})
+                 "share_of_step": share[dom]})
+    # traffic: DRAM bytes (read + write) per launch of that kernel from the committed
+    # ncu launch list of this command (cold cache, serialised); null when absent
+    tr_info = ncu_traffic(dom, getattr(dev, "split_bwd", False))
+    roof["traffic"] = tr_info["bytes_per_launch"] if tr_info else None
+    roof["traffic_source"] = tr_info
 
     # ---- e2e through the public API with host buffers (per step: H2D data, D2H results)
     res = rec.run([data[0]], seeds=[cfg.rng_seed], chi_trues=[chi_true[0]])   # warm (theta0 cache)
