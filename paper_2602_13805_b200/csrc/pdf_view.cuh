@@ -89,7 +89,9 @@ __host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) 
   const int P = 2 * M, K = 2 * mf, M0 = K * K;
   const int rp = M / CS;
   size_t a = (size_t)M0 + (size_t)rp * K;
-  size_t xch = (size_t)CS * R > (size_t)M0 ? (size_t)CS * R : (size_t)M0;
+  // exchange: data-term partials (CS R) or the pushed truncation partials (CS ceil(M0 / CS))
+  const size_t xr = (size_t)CS * R, xt = (size_t)CS * ((M0 + CS - 1) / CS);
+  size_t xch = xr > xt ? xr : xt;
   // 8-CTA clusters (latency regime, one CTA per SM) also stage the constant
   // K^ columns and the E_inc / g_J-local rows; 4-CTA clusters (batches) keep
   // two CTAs per SM and read them from L2 in place
@@ -150,7 +152,8 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   s.khs = p; p += PRE ? (size_t)cp * P : 0;
   s.pre = p; p += PRE ? (size_t)rp * M : 0;
   s.dsum = p; p += (size_t)32 * (VIEW_MAX_THREADS / 32) + M0 / CS + 1;
-  C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)M0 ? (size_t)CS * a.R : (size_t)M0);
+  const int opr = (M0 + CS - 1) / CS;   // truncation outputs owned per rank
+  C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)CS * opr ? (size_t)CS * a.R : (size_t)CS * opr);
   double* red = reinterpret_cast<double*>(p);
 
   for (int i = tid; i < P; i += blockDim.x) s.tw[i] = a.twP[i];
@@ -409,9 +412,13 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
       __syncthreads();
     }
     // U[yl][w] = sum_x gJ[yl][x] exp(-2 pi i kc_w x / M)
-    // my partial G[u][w] = sum_yl exp(-2 pi i kr_u y / M) U[yl][w]
+    // my partial G[u][w] = sum_yl exp(-2 pi i kr_u y / M) U[yl][w], pushed
+    // straight into the owner's exchange slot [my rank][i / CS] (owner i % CS):
+    // one cluster barrier, and every CTA then reads only its own shared memory
     C<T>* U = s.small + M0;
-    C<T>* mine = xch;
+    auto push = [&](int i, C<T> val) {
+      cluster.map_shared_rank(xch, i % CS)[rank * opr + i / CS] = val;
+    };
     if constexpr (sizeof(T) == 8) {
       const C<T>* tw_ = s.twm;
       const C<T>* rw = s.rows;
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
       __syncthreads();
       cgemm_dmma(K, K, rp, [&](int u, int yl) { return tw_[(corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]; },
                  [&](int yl, int w) { return U[yl * K + w]; },
-                 [&](int u, int w, C<T> val) { mine[u * K + w] = val; });
+                 [&](int u, int w, C<T> val) { push(u * K + w, val); });
     } else {
       for (int i = tid; i < rp * K; i += blockDim.x) {
         const int yl = i / K, w = i % K;
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
         const int f = corner_freq<T>(u, mf, M);
         C<T> acc = czero<T>();
         for (int yl = 0; yl < rp; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], s.twm[(f * (y0 + yl)) & (M - 1)]));
-        mine[i] = acc;
+        push(i, acc);
       }
     }
     tl_stage(a.tl, 6);
@@ -452,10 +459,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
     const T inv = T(1) / (T(M) * T(M));
     for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {
       C<T> acc = czero<T>();
-      for (int c = 0; c < CS; ++c) {
-        const C<T>* other = cluster.map_shared_rank(xch, c);
-        acc = cadd<T>(acc, other[i]);
-      }
+      for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * opr + i / CS]);   // rank order
       acc = cscale<T>(acc, inv);
       acc = cadd<T>(acc, s.dsum[(i - rank) / CS]);
       const int u = i / K, w = i % K;
@@ -472,7 +476,6 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
         gyrow[re + D0 / 2] = acc.y * co[re + D0 / 2];
       }
     }
-    cluster.sync();
   }
   tl_mark(a.tl, 2);
 }
