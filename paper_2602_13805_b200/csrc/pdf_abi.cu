@@ -87,6 +87,10 @@ struct pdf_ctx {
   int capturing = 0, pend = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_g3 = nullptr, ev_g2 = nullptr, ev_a2 = nullptr;
+  // data part of g_alpha computed on the side branch while the pixel kernel runs
+  void* gad = nullptr;
+  int gad_ready = 0;
+  cudaEvent_t ev_vf = nullptr, ev_gad = nullptr;
   double *red1, *red2;   // split pixel stage scratch (local reductions)
   int *err, *step;
   std::vector<double> c_inc_h, c_sca_h;
@@ -139,6 +143,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->h2b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
   c->tsnap = c->xbwd ? w.take<int>(1) : nullptr;
   c->tsnap_b = c->xbwd ? w.take<int>(1) : nullptr;
+  c->gad = c->xbwd && !c->large ? w.take<C<T>>(SN * c->M0) : nullptr;
   c->red1 = c->split ? w.take<double>((size_t)d.S * (3 * img + 1)) : nullptr;
   c->red2 = c->split ? w.take<double>((size_t)d.S * (2 * img + 2)) : nullptr;
   c->dloss = w.take<double>(SN);
@@ -465,6 +470,7 @@ static int phys_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, do
   a.gE = (const C<T>*)c->gE; a.gJloc = (const C<T>*)c->gJ;
   a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
   a.grows = (C<T>*)c->grows;
+  a.gad = c->gad_ready ? (const C<T>*)c->gad : nullptr;
   return launch_view<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st);
 }
 
@@ -936,13 +942,31 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h2, c->H, c->D0, thc, o.w3, o.b3, nullptr, 1, nullptr, st));
   mark();
   if (run()) TRY(phys_forward<T>(c, c->alpha_hat, st));
+  // side branch: the data part of g_alpha (needs only g_rows) overlaps the pixel kernel
+  const bool gfork = fork && c->gad && run();
+  if (gfork) {
+    CK_CUDA(cudaEventRecord(c->ev_vf, st));
+    CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));
+    g_pdl_off = 1;
+    gad_kernel<T><<<dim3((c->M0 + 255) / 256, c->d.S * c->d.n), 256, 0, c->side>>>(
+        (const C<T>*)c->grows, (const C<T>*)c->hs, (C<T>*)c->gad, c->d.R, c->M0);
+    g_pdl_off = 0;
+    CK_CUDA(cudaGetLastError());
+    CK_CUDA(cudaEventRecord(c->ev_gad, c->side));
+  }
   mark();
   if (run()) {
     if (c->split) TRY(split_pixel<T>(c, st));
     else TRY((phys_pixel<T, true>(c, nullptr, st)));
   }
   mark();
-  if (run()) TRY(phys_backward<T>(c, nullptr, c->gy, st, bd, trace, !c->split));
+  if (gfork) {
+    CK_CUDA(cudaStreamWaitEvent(st, c->ev_gad, 0));
+    c->gad_ready = 1;
+  }
+  const int rb = run() ? phys_backward<T>(c, nullptr, c->gy, st, bd, trace, !c->split) : PDF_OK;
+  c->gad_ready = 0;
+  TRY(rb);
   mark();
   if (run() && c->split) TRY(split_finalize(c, bd, trace, st));
   mark();   // finalize is fused into view_bwd unless the pixel stage is split
@@ -1059,7 +1083,7 @@ extern "C" int pdf_ctx_destroy(pdf_ctx* c) {
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->g_stream) cudaStreamDestroy(c->g_stream);
   if (c->side) cudaStreamDestroy(c->side);
-  for (cudaEvent_t e : {c->ev_g3, c->ev_g2, c->ev_a2}) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_g3, c->ev_g2, c->ev_a2, c->ev_vf, c->ev_gad}) if (e) cudaEventDestroy(e);
   delete c;
   return PDF_OK;
 }
@@ -1206,6 +1230,8 @@ static int train_impl(pdf_ctx* c, void* theta, void* m, void* v, int t0, int k, 
       CK_CUDA(cudaEventCreateWithFlags(&c->ev_g3, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&c->ev_g2, cudaEventDisableTiming));
       CK_CUDA(cudaEventCreateWithFlags(&c->ev_a2, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&c->ev_vf, cudaEventDisableTiming));
+      CK_CUDA(cudaEventCreateWithFlags(&c->ev_gad, cudaEventDisableTiming));
     }
     cudaGraph_t g;
     CK_CUDA(cudaStreamBeginCapture(c->g_stream, cudaStreamCaptureModeThreadLocal));

@@ -87,6 +87,15 @@ __device__ __forceinline__ C<T> data_adjoint_at(const C<T>* grow, const C<T>* hs
   return cadd<T>(a0, a1);
 }
 
+// gad[v][slot] = sum_r g_rows[v][r] conj(H[r][slot]) for every view (the data
+// part of g_alpha, see above): CTA = 256 coefficients of one view
+template <typename T>
+__global__ void __launch_bounds__(256) gad_kernel(const C<T>* grows, const C<T>* hs, C<T>* gad, int R, int M0) {
+  const int v = blockIdx.y, m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M0) return;
+  gad[(size_t)v * M0 + m] = data_adjoint_at<T>(grows + (size_t)v * R, hs, R, M0, m, 0, 1);
+}
+
 template <typename T>
 __global__ void permute_khat_kernel(const C<T>* khat, C<T>* out, int P, int split) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;

@@ -55,6 +55,7 @@ struct ViewArgs {
   const C<T>* gE;     // [S*n][M][M]
   const C<T>* gJloc;  // [S*n][M][M]
   C<T>* galpha;       // [S*n][M0] or null
+  const C<T>* gad;    // [S*n][M0] data part of g_alpha (slot order, gad_kernel) or null: computed here
   T* gy;              // [S][rows][D0] or null
   const T* cout;      // [S][D0] output gain per feature
   int joint;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   // other CTAs finish theirs, and the wait acquires everyone's scatter.
   tl_stage(a.tl, 1);
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-  if constexpr (MODE == VIEW_BWD) {
+  if (MODE == VIEW_BWD && !a.gad) {
     // G_S^H g_rows through H (pdf_aux.cuh) for my outputs i = rank + CS*o,
     // while the other CTAs finish their stage-A scatter; warp w sums
     // receivers w, w + nw, ...
@@ -461,9 +462,9 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
       C<T> acc = czero<T>();
       for (int c = 0; c < CS; ++c) acc = cadd<T>(acc, xch[c * opr + i / CS]);   // rank order
       acc = cscale<T>(acc, inv);
-      acc = cadd<T>(acc, s.dsum[(i - rank) / CS]);
       const int u = i / K, w = i % K;
       const int slot = corner_slot(u, w, mf);
+      acc = cadd<T>(acc, a.gad ? a.gad[(size_t)v * M0 + slot] : s.dsum[(i - rank) / CS]);
       if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
       if (a.gy) {
         const int D0 = 2 * M0 * (a.joint ? a.n : 1);
