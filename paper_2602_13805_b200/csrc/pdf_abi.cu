@@ -90,6 +90,7 @@ struct pdf_ctx {
   // data part of g_alpha computed on the side branch while the pixel kernel runs
   void* gad = nullptr;
   int gad_ready = 0;
+  int dfork_ok = 0, skip_data = 0;   // data term (split-K GEMM) on the side branch as well
   cudaEvent_t ev_vf = nullptr, ev_gad = nullptr;
   double *red1, *red2;   // split pixel stage scratch (local reductions)
   int *err, *step;
@@ -136,7 +137,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   } else {
     c->spec = c->gpart = nullptr;
   }
-  c->dpart = c->dgemm ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
+  c->dpart = c->dgemm || c->dfork_ok ? w.take<C<T>>((size_t)d.S * c->dg_nchunks * d.n * d.R) : nullptr;
   c->ghp = c->xbwd ? w.take<double>((size_t)d.S * GH_NSL * c->rows * c->H) : nullptr;
   c->ticket = c->xbwd ? w.take<int>((size_t)d.S * (c->H / 64 + 1)) : nullptr;
   c->h1b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
@@ -210,7 +211,8 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // (measured: cfg2 -4 us, cfg3 167 -> 150 us per iteration, cfg5 unchanged)
   const int bx = env_int("PDF_BWD_X", 1);   // 2: force (experiments)
   c->xbwd = bx && d->dtype == PDF_F64 && c->rows <= 80 && (bx == 2 || (long long)d->S * (c->H / 8) <= 4 * 148);
-  if (c->dgemm) {
+  c->dfork_ok = c->xbwd && !c->large && d->n <= 80 && d->R <= 80 && env_int("PDF_DATA_FORK", 1);
+  if (c->dgemm || c->dfork_ok) {
     const int npix = c->M0;   // the data GEMM contracts spectral coefficients (H = G_S o expand)
     // chunk granularity: 16 coefficients for the DMMA kernel (4 k-steps), the
     // staged sub-tile for the float32 one
@@ -221,7 +223,8 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
     c->dg_nchunks = (npix + c->dg_chunk - 1) / c->dg_chunk;
     const int ntp = ((d->n + 7) / 8) * ((d->R + 8 * DM_NTL - 1) / (8 * DM_NTL));
     c->dg_nq = std::max(1, std::min(4, 8 / ntp));
-    if (d->n > 80 || d->R > 80) return fail(PDF_EINVAL, "at most 80 incidences / receivers for the data GEMM");
+    if (c->dgemm && (d->n > 80 || d->R > 80))
+      return fail(PDF_EINVAL, "at most 80 incidences / receivers for the data GEMM");
   }
   c->rsz = d->dtype == PDF_F64 ? 8 : 4;
   c->csz = 2 * c->rsz;
@@ -422,9 +425,9 @@ static int phys_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
   a.data = (const C<T>*)c->d.data; a.mask = (const T*)c->d.mask;
   a.c_sca = c->c_sca; a.J = (C<T>*)c->J; a.E = (C<T>*)c->E_; a.norms = c->norms;
-  a.grows = (C<T>*)c->grows; a.dloss = c->dloss; a.do_data = !c->dgemm;
+  a.grows = (C<T>*)c->grows; a.dloss = c->dloss; a.do_data = !c->dgemm && !c->skip_data;
   TRY((launch_view<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
-  return c->dgemm ? data_term<T>(c, alpha_hat, st) : PDF_OK;
+  return c->dgemm && !c->skip_data ? data_term<T>(c, alpha_hat, st) : PDF_OK;
 }
 
 template <typename T, bool GRAD>
@@ -941,9 +944,28 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   mark();
   if (run()) TRY(net_fwd_layer<T>(c, (const T*)c->h2, c->H, c->D0, thc, o.w3, o.b3, nullptr, 1, nullptr, st));
   mark();
-  if (run()) TRY(phys_forward<T>(c, c->alpha_hat, st));
+  // side branch: the data term D = alpha H^T - d and its g_alpha part need only
+  // alpha_hat; they overlap the view and pixel kernels of the main chain
+  const bool dfork = fork && c->dfork_ok && c->gad && run();
+  if (dfork) {
+    CK_CUDA(cudaEventRecord(c->ev_vf, st));
+    CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));
+    g_pdl_off = 1;
+    const int rd = data_term<T>(c, c->alpha_hat, c->side);
+    if (rd == PDF_OK)
+      gad_kernel<T><<<dim3((c->M0 + 255) / 256, c->d.S * c->d.n), 256, 0, c->side>>>(
+          (const C<T>*)c->grows, (const C<T>*)c->hs, (C<T>*)c->gad, c->d.R, c->M0);
+    g_pdl_off = 0;
+    TRY(rd);
+    CK_CUDA(cudaGetLastError());
+    CK_CUDA(cudaEventRecord(c->ev_gad, c->side));
+  }
+  c->skip_data = dfork;
+  const int rf = run() ? phys_forward<T>(c, c->alpha_hat, st) : PDF_OK;
+  c->skip_data = 0;
+  TRY(rf);
   // side branch: the data part of g_alpha (needs only g_rows) overlaps the pixel kernel
-  const bool gfork = fork && c->gad && run();
+  const bool gfork = fork && c->gad && run() && !dfork;
   if (gfork) {
     CK_CUDA(cudaEventRecord(c->ev_vf, st));
     CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));
@@ -960,7 +982,7 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
     else TRY((phys_pixel<T, true>(c, nullptr, st)));
   }
   mark();
-  if (gfork) {
+  if (gfork || dfork) {
     CK_CUDA(cudaStreamWaitEvent(st, c->ev_gad, 0));
     c->gad_ready = 1;
   }
