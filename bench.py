@@ -260,7 +260,7 @@ def large_leg(args, d: Dist):
         dev.set_data(data)
         _, r0 = dev.bp_initialize()
         dev.net_setup(dev.init_alpha(r0))
-        th, m, v = theta0.clone(), torch.zeros_like(theta0), torch.zeros_like(theta0)
+        th, m, v = dev.alloc_state(theta0)
         tr = torch.zeros(k, 1, 6, dtype=torch.float64, device=dev.device)
         dev.train(th, m, v, 0, 20, tr)
         th.copy_(theta0); m.zero_(); v.zero_()
@@ -406,7 +406,7 @@ def run_ours(args, d: Dist):
     alpha0 = dev.init_alpha(r0)
     dev.net_setup(alpha0)
     theta0 = torch.as_tensor(_theta0([cfg.rng_seed], rec.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
-    theta, m, v = theta0.clone(), torch.zeros_like(theta0), torch.zeros_like(theta0)
+    theta, m, v = dev.alloc_state(theta0)
     trace = torch.zeros(k, 1, 6, dtype=torch.float64, device=dev.device)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev.device)
 
@@ -512,7 +512,7 @@ def run_ours(args, d: Dist):
         # device-resident batched loop only
         devb = rb.dev
         th0 = torch.as_tensor(_theta0(idx, rb.m0_eff), dtype=devb.rdt, device=devb.device)
-        thb, mb, vb = th0.clone(), torch.zeros_like(th0), torch.zeros_like(th0)
+        thb, mb, vb = devb.alloc_state(th0)
         trb = torch.zeros(k, S, 6, dtype=torch.float64, device=devb.device)
         devb.train(thb, mb, vb, 0, k, trb)
         torch.cuda.synchronize()

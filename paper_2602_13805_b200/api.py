@@ -549,7 +549,9 @@ class BatchReconstructor:
         bufs = self.__dict__.get("_dev_bufs")
         if bufs is None or bufs[3].shape[0] < max(k, 1):
             n_par = _flat_size(self.m0_eff)
-            bufs = [torch.empty((self.S, n_par), dtype=dev.rdt, device=dev.device) for _ in range(3)]
+            # theta, m, v in one allocation: the library keeps that window L2-resident
+            flat = torch.empty((3, self.S, n_par), dtype=dev.rdt, device=dev.device)
+            bufs = [flat[0], flat[1], flat[2]]
             bufs.append(torch.empty((max(k, 1), self.S, 6), dtype=torch.float64, device=dev.device))
             self._dev_bufs = bufs
         theta, m, v, trace_buf = bufs

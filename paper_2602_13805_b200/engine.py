@@ -194,6 +194,13 @@ class DeviceProblem:
         cs = (ct.c_double * self.S)(*self.c_sca)
         N.check(self.lib.pdf_set_norms(self.ctx, ci, cs, _stream()))
 
+    def alloc_state(self, theta0: torch.Tensor):
+        """(theta, m, v) for train(): one allocation (the library keeps that
+        window L2-resident in the captured loop), theta = theta0, m = v = 0."""
+        flat = torch.zeros((3,) + tuple(theta0.shape), dtype=self.rdt, device=self.device)
+        flat[0].copy_(theta0)
+        return flat[0], flat[1], flat[2]
+
     def train(self, theta, m, v, t0: int, k: int, trace: torch.Tensor | None = None, use_graph: bool = True):
         N.check(self.lib.pdf_train(self.ctx, _ptr(theta), _ptr(m), _ptr(v), int(t0), int(k), _ptr(trace),
                                    int(use_graph), _stream()))

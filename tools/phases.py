@@ -41,7 +41,7 @@ def main():
     _, r0 = dev.bp_initialize()
     dev.net_setup(dev.init_alpha(r0))
     th0 = torch.as_tensor(_theta0(list(range(a.scenes)), rec.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
-    th, m, v = th0.clone(), torch.zeros_like(th0), torch.zeros_like(th0)
+    th, m, v = dev.alloc_state(th0)
     ph = dev.profile_phases(th, m, v, 0, a.iters)
     th.copy_(th0); m.zero_(); v.zero_()
     tr = torch.zeros(200, a.scenes, 6, dtype=torch.float64, device=dev.device)

@@ -39,7 +39,7 @@ def main():
     _, r0 = dev.bp_initialize()
     dev.net_setup(dev.init_alpha(r0))
     th = torch.as_tensor(_theta0(list(range(a.scenes)), rec.m0_eff), dtype=dev.rdt, device=dev.device).contiguous()
-    m, v = torch.zeros_like(th), torch.zeros_like(th)
+    th, m, v = dev.alloc_state(th)
     dev.train(th, m, v, 0, 20)
     rows = dev.timeline(th, m, v, 20)
     dev.check_errors()
