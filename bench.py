@@ -439,9 +439,13 @@ def run_ours(args, d: Dist):
     dev.check_errors()
     final_total = float(trace[-1, 0, 5].item())
 
-    # kernels per fused iteration: 3 forward layers, view_fwd, pixel, view_bwd
-    # (loss finalize fused), 3 backward layers with Adam
-    launches_per_iter = 9
+    # kernels per fused iteration of the captured graph: 3 forward layers,
+    # view_fwd, pixel, view_bwd (loss finalize fused), then either 3 fused
+    # backward layers with Adam, or (split backward, <= 16 rows, widths <= 1024)
+    # g_h3, g_h2, Adam layer 1 on the main chain plus the side branch's data
+    # GEMM, its reduce, gad and the Adam of layers 3 / 2
+    fork = dev.split_bwd and dev.rows <= 16 and dev.hidden <= 1024 and dev.d0 <= 1024
+    launches_per_iter = 14 if fork else 9 + (2 if dev.data_gemm else 0)
     # ---- per-kernel live timing (events between kernels of un-graphed iterations)
     theta.copy_(theta0); m.zero_(); v.zero_()
     phases = dev.profile_phases(theta, m, v, 0, 20)
