@@ -173,3 +173,37 @@ def test_train_step_split_backward_matches_oracle(tiny_setup, n):
         assert abs(trace[k, 0, 5].item() - parts["total"]) < 1e-9 * abs(parts["total"])
         want = O.adam_update(st, want, g)
     assert np.abs(th[0].cpu().numpy() - want).max() < 1e-9
+
+
+@pytest.mark.parametrize("n", [12, 16])
+def test_captured_graph_with_side_branches_matches_eager(tiny_setup, n):
+    """The captured training graph (side branches: data term + g_alpha data
+    part, Adam of layers 3 / 2; ping-pong activations) against the same
+    iterations launched eagerly, for 12 rows (padding rows in the multicast
+    staging) and 16 rows."""
+    from oracle import pdf_oracle as O
+    from paper_2602_13805_b200.engine import DeviceProblem
+    rng = np.random.default_rng(200 + n)
+    m, R = 16, tiny_setup.ops.gs_matrix.shape[0]
+    phi = 2 * np.pi * np.arange(n) / n
+    xy = np.linspace(-0.7, 0.7, m)
+    e_inc = np.exp(1j * 2 * np.pi * (np.cos(phi)[:, None, None] * xy[None, None, :]
+                                     + np.sin(phi)[:, None, None] * xy[None, :, None]))
+    data = 0.3 * (rng.standard_normal((n, R)) + 1j * rng.standard_normal((n, R)))
+    alpha0 = 0.05 * (rng.standard_normal((n, 36)) + 1j * rng.standard_normal((n, 36)))
+    params = O.init_net(36, np.random.default_rng(3))
+    flat = O.flat(params) + 0.02 * rng.standard_normal(O.flat(params).size)
+    dev = DeviceProblem(tiny_setup.ops, e_inc, data, mf=3, beta=6.0, lambdas=LAM, tau_b=0.5)
+    dev.net_setup(torch.as_tensor(alpha0[None], device="cuda"))
+    th0 = torch.as_tensor(flat[None], device="cuda").contiguous()
+    out = []
+    for graph in (True, False):
+        th, mm, vv = dev.alloc_state(th0)
+        tr = torch.zeros(30, 1, 6, dtype=torch.float64, device="cuda")
+        dev.train(th, mm, vv, 0, 30, tr, use_graph=graph)
+        torch.cuda.synchronize()
+        dev.check_errors()
+        out.append((th[0].cpu().numpy(), tr[:, 0, 5].cpu().numpy()))
+    (tg, lg), (te, le) = out
+    assert np.allclose(lg, le, rtol=1e-9, atol=0)
+    assert np.abs(tg - te).max() < 1e-9
