@@ -344,8 +344,7 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
       cgemm_dmma(K, K, VL_ROWS,
                  [&](int u, int yl) { return twm[(vl_corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]; },
                  [&](int yl, int w) { return U[yl * K + w]; }, [&](int u, int w, C<T> val) { gp[u * K + w] = val; });
-      return;
-    }
+    } else {
     for (int i = tid; i < VL_ROWS * K; i += blockDim.x) {
       const int yl = i / K, w = i % K;
       const int f = vl_corner_freq<T>(w, mf, M);
@@ -365,6 +364,7 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
       C<T> acc = czero<T>();
       for (int yl = 0; yl < VL_ROWS; ++yl) acc = cadd<T>(acc, cmul<T>(U[yl * K + w], twm[(f * (y0 + yl)) & (M - 1)]));
       gp[i] = acc;
+    }
     }
   } else {
 #pragma unroll
