@@ -531,6 +531,11 @@ static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
       if (e == cudaSuccess)
         e = MT == 1 ? launch_cluster(net_fwd_x_kernel<1, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args)
                     : launch_cluster(net_fwd_x_kernel<2, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args);
+    } else if (mc == 2 && grid.x % 2 == 0) {
+      e = MT == 1 ? prep(net_fwd_x_kernel<1, 2>, smem) : prep(net_fwd_x_kernel<2, 2>, smem);
+      if (e == cudaSuccess)
+        e = MT == 1 ? launch_cluster(net_fwd_x_kernel<1, 2>, grid, dim3(XW * 32), smem, st, dim3(2, 1, 1), args)
+                    : launch_cluster(net_fwd_x_kernel<2, 2>, grid, dim3(XW * 32), smem, st, dim3(2, 1, 1), args);
     } else if (mc >= 4 && grid.x % 4 == 0) {
       e = MT == 1 ? prep(net_fwd_x_kernel<1, 4>, smem) : prep(net_fwd_x_kernel<2, 4>, smem);
       if (e == cudaSuccess)
@@ -855,6 +860,11 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
     if (e == cudaSuccess)
       e = MT == 1 ? launch_cluster(net_gh_x_kernel<1, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args)
                   : launch_cluster(net_gh_x_kernel<2, 8>, grid, dim3(XW * 32), smem, st, dim3(8, 1, 1), args);
+  } else if (mc == 2 && grid.x % 2 == 0) {
+    e = MT == 1 ? prep(net_gh_x_kernel<1, 2>, smem) : prep(net_gh_x_kernel<2, 2>, smem);
+    if (e == cudaSuccess)
+      e = MT == 1 ? launch_cluster(net_gh_x_kernel<1, 2>, grid, dim3(XW * 32), smem, st, dim3(2, 1, 1), args)
+                  : launch_cluster(net_gh_x_kernel<2, 2>, grid, dim3(XW * 32), smem, st, dim3(2, 1, 1), args);
   } else if (mc >= 4 && grid.x % 4 == 0) {
     e = MT == 1 ? prep(net_gh_x_kernel<1, 4>, smem) : prep(net_gh_x_kernel<2, 4>, smem);
     if (e == cudaSuccess)
