@@ -449,8 +449,10 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
   void* args[] = {&p};
   const bool ilp2 = (long long)grid.x * grid.y * grid.z <= 4 * 148;   // latency regime
-  cudaError_t e = ilp2 ? plain_launch(pixel_kernel<T, GRAD, true>, grid, dim3(PIX_NW * 32), smem, st, args)
-                       : plain_launch(pixel_kernel<T, GRAD, false>, grid, dim3(PIX_NW * 32), smem, st, args);
+  static const int pw = env_int("PDF_PIX_WARPS", PIX_NW);   // experiments: warps per CTA (<= PIX_NW)
+  const dim3 blk(32 * std::min(std::max(pw, 1), PIX_NW));
+  cudaError_t e = ilp2 ? plain_launch(pixel_kernel<T, GRAD, true>, grid, blk, smem, st, args)
+                       : plain_launch(pixel_kernel<T, GRAD, false>, grid, blk, smem, st, args);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("pixel kernel: ") + cudaGetErrorString(e));
   return PDF_OK;
