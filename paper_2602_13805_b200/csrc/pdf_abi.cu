@@ -194,7 +194,7 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   c->chunk = c->dg_chunk = c->dg_nchunks = 0;
   if (c->large) {
     const size_t csz = d->dtype == PDF_F64 ? 16 : 8;
-    const long long budget = (long long)env_int("PDF_SPEC_MIB", 48) << 20;   // L2-resident spectrum chunk
+    const long long budget = (long long)env_int("PDF_SPEC_MIB", 72) << 20;   // L2-resident spectrum chunk
     const long long per = (long long)2 * M * M * csz;
     long long ch = std::max(1LL, budget / per);
     c->chunk = (int)std::min<long long>(ch, (long long)d->S * d->n);
@@ -449,7 +449,10 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
   void* args[] = {&p};
   const bool ilp2 = (long long)grid.x * grid.y * grid.z <= 4 * 148;   // latency regime
-  static const int pw = env_int("PDF_PIX_WARPS", PIX_NW);   // experiments: warps per CTA (<= PIX_NW)
+  // batches with few views: 4-warp CTAs (more CTAs per SM, smaller barrier
+  // domains; measured cfg4 4557 -> 4513 us/iter, but cfg5's 72 views slow down)
+  static const int pw_env = env_int("PDF_PIX_WARPS", 0);
+  const int pw = pw_env ? pw_env : (!ilp2 && c->d.n <= 16 ? 4 : PIX_NW);
   const dim3 blk(32 * std::min(std::max(pw, 1), PIX_NW));
   cudaError_t e = ilp2 ? plain_launch(pixel_kernel<T, GRAD, true>, grid, blk, smem, st, args)
                        : plain_launch(pixel_kernel<T, GRAD, false>, grid, blk, smem, st, args);
@@ -932,7 +935,8 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   auto mark = [&]() {
     if (ev) cudaEventRecord(ev[ph], st);
     ++ph;
-    g_tl_cur = c->tl_on && ph <= PDF_NPHASES ? g_tl_iter * PDF_NPHASES + ph : 0;
+    const int slot = g_tl_iter * PDF_NPHASES + ph;
+    g_tl_cur = c->tl_on && ph <= PDF_NPHASES && slot <= PDF_TL_SLOTS ? slot : 0;
   };
   auto run = [&]() { return !(skip >> ph & 1); };
   const Offs o = offsets(c);
@@ -1255,7 +1259,8 @@ static int train_impl(pdf_ctx* c, void* theta, void* m, void* v, int t0, int k, 
     for (int i = 0; i < k; ++i) TRY(iteration<T>(c, theta, m, v, nullptr, nullptr, tr, 1, st));
     return PDF_OK;
   }
-  const int G = 10;  // iterations per captured graph
+  // iterations per captured graph (graph boundaries cost a full drain + launch)
+  static const int G = std::max(1, env_int("PDF_GRAPH_ITERS", 10));
   if (!(c->gexec && c->g_theta == theta && c->g_m == m && c->g_v == v && c->g_trace == (void*)tr)) {
     if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
     // capture on a private stream (the caller's may be the legacy default
