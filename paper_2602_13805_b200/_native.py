@@ -11,6 +11,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PDF_LIB_PATH") or os.path.join(_HERE, "libpdfb200.so")   # override: A/B measurements only
+# (an override library must still export every symbol: a missing one raises below)
 
 ABI_VERSION = 1
 PDF_F64, PDF_F32 = 0, 1
@@ -101,9 +102,7 @@ def lib():
         "pdf_shard_step_c": (ct.c_int, [vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
-        if os.environ.get("PDF_LIB_PATH") and not hasattr(L, name):
-            continue   # A/B against an older build
-        f = getattr(L, name)
+        f = getattr(L, name)      # AttributeError names the missing symbol
         f.restype = res
         f.argtypes = args
     if L.pdf_abi_version() != ABI_VERSION:

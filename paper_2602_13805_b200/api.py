@@ -32,7 +32,7 @@ import torch
 from scipy import ndimage
 
 from .config import CcoParams, ImagingConfig
-from .engine import DeviceProblem
+from .engine import DeviceProblem, check_config_supported
 from .errors import PoleError, ZeroDataError  # noqa: F401  (re-exported)
 from .geometry import AntennaArray, ComplexGrid, build_array, build_grid
 from .operators import GreensOperators, ScatteredData, build_greens, incident_fields
@@ -158,31 +158,89 @@ class LossContext:
 
 
 @dataclass
-class PipelineState:
-    """Intermediates of one composite-loss evaluation (losses.py:202-212).
+class ContrastRecovery:
+    """recover_contrast with its reusable intermediates (cie.py:53-63)."""
+    chi: np.ndarray           # (m1, m2)
+    j_views: np.ndarray       # (n, m1, m2) currents expand(alpha)
+    e_views: np.ndarray       # (n, m1, m2) total fields E_inc + G_D J
+    numerator: np.ndarray     # (m1, m2) sum_i J_i conj(E_i)
+    denominator: np.ndarray   # (m1, m2) real, sum_i |E_i|^2 + eps_reg
+    eps_reg: float
+    degenerate: np.ndarray    # (m1, m2) bool, denominator <= 10 eps_reg
 
-    The GPU keeps J, E, chi ... in device workspace; the host record carries
-    the coefficients, the breakdown and the recovered contrast."""
-    alpha_hat: np.ndarray
-    chi: np.ndarray
+
+@dataclass
+class PipelineState:
+    """Intermediates of one composite-loss evaluation (losses.py:200-212), same fields.
+
+    The loss itself comes from the fused library kernels (pdf_loss_value); the
+    intermediates are assembled on the device from the library's operator
+    primitives (expand, G_D, G_S) and copied to the host once."""
+    alpha_hat: np.ndarray      # (n, m0)
+    rec: ContrastRecovery
+    r_hat: np.ndarray          # (m1, m2)
+    p_views: np.ndarray        # (n, m1, m2) E + beta J
+    state_res: np.ndarray      # (n, m1, m2)
+    data_res: np.ndarray       # (n, n_rx), masked
     breakdown: LossBreakdown
+
+    @property
+    def chi(self) -> np.ndarray:
+        return self.rec.chi
 
 
 def _cdev(x, dev: DeviceProblem):
     return torch.as_tensor(np.ascontiguousarray(x), dtype=dev.cdt, device=dev.device)
 
 
+def _recovery_dev(dev: DeviceProblem, alpha_d: torch.Tensor, eps_reg: float | None = None):
+    """(J, E, num, den, eps, chi) of cie.py:66-99 on the device for one scene's views
+    (alpha_d: (n, m0)), from the library's expand and G_D primitives."""
+    j = dev.expand(alpha_d)
+    einc = dev.e_inc if dev.e_inc.dim() == 3 else dev.e_inc[0]
+    e = einc + dev.apply_gd(j)
+    pw = torch.sum((e.conj() * e).real, dim=(-1, -2))
+    eps = (1e-10 * pw.max() / (dev.M * dev.M)) if eps_reg is None else torch.tensor(float(eps_reg),
+                                                                                     dtype=dev.rdt, device=dev.device)
+    num = torch.sum(j * e.conj(), dim=0)
+    den = torch.sum((e.conj() * e).real, dim=0) + eps
+    return j, e, num, den, eps, num / den
+
+
+def _recovery_host(j, e, num, den, eps, chi) -> ContrastRecovery:
+    epsf = float(eps)
+    den_h = den.cpu().numpy()
+    return ContrastRecovery(chi=chi.cpu().numpy(), j_views=j.cpu().numpy(), e_views=e.cpu().numpy(),
+                            numerator=num.cpu().numpy(), denominator=den_h, eps_reg=epsf,
+                            degenerate=den_h <= 10.0 * epsf)
+
+
 def pipeline_forward(alpha_hat: np.ndarray, ctx: LossContext) -> PipelineState:
     alpha_hat = np.atleast_2d(np.asarray(alpha_hat, dtype=np.complex128))
+    if alpha_hat.shape != (ctx.n_views, ctx.basis.m0):
+        raise ValueError("need one coefficient vector per incidence view")
     dev = ctx.device()
-    bd, chi = dev.loss_value(_cdev(alpha_hat[None], dev), want_chi=True)
-    dev.check_errors()
-    return PipelineState(alpha_hat=alpha_hat, chi=chi[0].cpu().numpy(),
+    a = _cdev(alpha_hat[None], dev)
+    bd, _ = dev.loss_value(a)
+    dev.check_errors()           # PoleError / FloatingPointError (named terms) as the reference raises them
+    j, e, num, den, eps, chi = _recovery_dev(dev, a[0])
+    beta = ctx.beta
+    r_hat = dev.r_fixed[0] if dev.r_fixed is not None else beta * chi / (beta * chi + 1.0)
+    p = e + beta * j
+    sres = r_hat * p - beta * j
+    dres = dev.gs_forward(j) - dev.data[0]
+    if dev.mask is not None:
+        dres = dres * dev.mask[0]
+    return PipelineState(alpha_hat=alpha_hat, rec=_recovery_host(j, e, num, den, eps, chi),
+                         r_hat=r_hat.cpu().numpy(), p_views=p.cpu().numpy(), state_res=sres.cpu().numpy(),
+                         data_res=dres.cpu().numpy(),
                          breakdown=LossBreakdown.from_row(bd[0].cpu().numpy(), ctx.lambdas))
 
 
 def pipeline_backward(state: PipelineState, ctx: LossContext) -> np.ndarray:
-    """g_alpha at state.alpha_hat (the fused kernels recompute the forward)."""
+    """g_alpha at state.alpha_hat (losses.py:267-306).  The library's fused
+    kernels run the forward and the hand adjoint in one pass (the forward
+    intermediates never leave the SM), so the state only supplies alpha_hat."""
     g, _ = grad_alpha(state.alpha_hat, ctx)
     return g
 
@@ -343,9 +401,7 @@ def adam_step(state: AdamState, params: NetworkParams, grad: np.ndarray) -> tupl
     flat = flatten_params(params)
     if grad.shape != flat.shape:
         raise ValueError("gradient length does not match parameter count")
-    if (state.b1, state.b2, state.eps) != (0.9, 0.999, 1e-8):
-        raise ValueError("only the reference's Adam constants are supported on the device")
-    dev = _adam_device(state.lr)
+    dev = _adam_device(state.lr, state.b1, state.b2, state.eps)
     t = state.step + 1
     to = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=dev.device).clone()  # noqa
     p, m, v, g = to(flat), to(state.m), to(state.v), to(grad)
@@ -359,13 +415,15 @@ def adam_step(state: AdamState, params: NetworkParams, grad: np.ndarray) -> tupl
 _ADAM_DEVS: dict = {}
 
 
-def _adam_device(lr: float) -> DeviceProblem:
-    if lr not in _ADAM_DEVS:
+def _adam_device(lr: float, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8) -> DeviceProblem:
+    key = (float(lr), float(b1), float(b2), float(eps))
+    if key not in _ADAM_DEVS:
         cfg = ImagingConfig(m1=16, m2=16, m_f=1, n_tx=1, n_rx=1, learn_rate=lr).validate()
         ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
-        _ADAM_DEVS[lr] = DeviceProblem(ops, np.ones((1, 16, 16), complex), np.ones((1, 1), complex), mf=1,
-                                       beta=6.0, lambdas=(0, 0, 0), tau_b=0.5, lr=lr)
-    return _ADAM_DEVS[lr]
+        _ADAM_DEVS[key] = DeviceProblem(ops, np.ones((1, 16, 16), complex), np.ones((1, 1), complex), mf=1,
+                                        beta=6.0, lambdas=(0, 0, 0), tau_b=0.5, lr=lr, adam_b1=b1, adam_b2=b2,
+                                        adam_eps=eps)
+    return _ADAM_DEVS[key]
 
 
 # ---------------------------------------------------------------------------- pipeline
@@ -455,6 +513,7 @@ class BatchReconstructor:
                  array: AntennaArray | None = None, mask=None, dtype: str = "f64", use_graph: bool = True,
                  theta_cache: bool = True):
         config.validate()
+        check_config_supported(config)
         self.config = config
         self.array = build_array(config) if array is None else array
         self.grid = build_grid(config)
@@ -510,12 +569,16 @@ class BatchReconstructor:
             bufs[slot] = torch.empty((self.S, _flat_size(self.m0_eff)), dtype=torch.float64, pin_memory=True)
         return bufs[slot]
 
-    def run(self, datas, seeds=None, chi_trues=None, k_iters: int | None = None, prefetch_seeds=None) -> list:
+    def run(self, datas, seeds=None, chi_trues=None, k_iters: int | None = None, prefetch_seeds=None,
+            check_init: bool = False) -> list:
         """Reconstruct the S scenes of `datas` (see the class docstring).
 
         prefetch_seeds: seeds of the NEXT batch; its reference-identical
         initial weights are drawn on the host cores while this batch trains on
-        the GPU (a batch pipeline pays the draws only once, up front)."""
+        the GPU (a batch pipeline pays the draws only once, up front).
+        check_init: raise the initialisation's PoleError before the training
+        loop starts, as the reference does (one host synchronisation);
+        otherwise it is raised after the loop (no synchronisation before it)."""
         cfg = self.config
         t0 = time.perf_counter()
         mats = np.stack([np.asarray(d.matrix if isinstance(d, ScatteredData) else d) for d in datas])
@@ -545,6 +608,10 @@ class BatchReconstructor:
                 pending = _theta0_async(seeds, self.m0_eff, self._pinned(slot).numpy())
         dev.set_data(mats)
         chi0, alpha0 = self._initialise()
+        if check_init and bool(dev.pole_flag):
+            for f in pending or ():
+                f.result()       # the pinned buffer must be idle before a later run reuses it
+            raise PoleError("beta*chi + 1 vanishes at some pixel")
         # persistent device state (theta, Adam moments, trace) for this batch shape
         bufs = self.__dict__.get("_dev_bufs")
         if bufs is None or bufs[3].shape[0] < max(k, 1):
@@ -608,11 +675,12 @@ def reconstruct(config: ImagingConfig, data: ScatteredData, array: AntennaArray 
     ``e_inc`` overrides the reference's line-source illumination (e.g. plane
     waves for the BASELINE configs); everything else follows the reference."""
     config.validate()
+    check_config_supported(config)
     t0 = time.perf_counter()
     if config.freeze_r:
         return _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0)
     rec = BatchReconstructor(config, 1, e_inc=e_inc, array=array, mask=data.mask, dtype=dtype)
-    res = rec.run([data], chi_trues=[chi_true])[0]
+    res = rec.run([data], chi_trues=[chi_true], check_init=True)[0]
     res.wall_time = time.perf_counter() - t0
     return res
 
@@ -658,39 +726,88 @@ def _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0):
                                 wall_time=time.perf_counter() - t0, rel_error=rel)
 
 
+class _DevCache:
+    """Small LRU of DeviceProblems for the one-shot API functions (bp_initialize,
+    init_alpha, recover_contrast, apply_cco): operators and workspace are
+    uploaded once per (operators, incident fields, data) identity.  The cache
+    holds references to the keyed host arrays, so an id is never reused while
+    its entry lives; like the reference's functions it treats inputs as
+    immutable."""
+
+    def __init__(self, size: int = 4):
+        self.size = size
+        self.items: list = []
+
+    def get(self, key, objs, make):
+        for i, (k, o, dev) in enumerate(self.items):
+            if k == key and all(a is b for a, b in zip(o, objs)):
+                self.items.append(self.items.pop(i))
+                return dev
+        dev = make()
+        self.items.append((key, objs, dev))
+        if len(self.items) > self.size:
+            self.items.pop(0)
+        return dev
+
+
+_ONE_SHOT = _DevCache()
+
+
+def _one_shot_device(ops: GreensOperators, views, data: ScatteredData | None, m_f: int, beta: float,
+                     n_rx: int | None = None) -> DeviceProblem:
+    views = np.asarray(views)
+    mat = data.matrix if data is not None else None
+    mask = data.mask if data is not None else None
+    key = (id(ops), id(views), id(mat), id(mask), m_f, float(beta))
+
+    def make():
+        d = mat if mat is not None else np.ones((views.shape[0], ops.n_rx if n_rx is None else n_rx), complex)
+        return DeviceProblem(ops, views, d, mf=m_f, beta=beta, lambdas=(0, 0, 0), tau_b=0.5, mask=mask)
+    return _ONE_SHOT.get(key, (ops, views, mat, mask), make)
+
+
 def bp_initialize(data: ScatteredData, e_inc, ops: GreensOperators, beta: float):
     """Backprojection (reconstruct.py:52-71) on the GPU; returns host (chi0, r0)."""
     views = e_inc.views if hasattr(e_inc, "views") else np.asarray(e_inc)
-    m_f = 1
-    dev = DeviceProblem(ops, views, data.matrix, mf=m_f, beta=beta, lambdas=(0, 0, 0), tau_b=0.5,
-                        mask=data.mask)
+    dev = _one_shot_device(ops, views, data, 1, beta)
     chi0, r0 = dev.bp_initialize()
     return chi0[0].cpu().numpy(), r0[0].cpu().numpy()
 
 
 def init_alpha(r0, data: ScatteredData, e_inc, ops: GreensOperators, basis: SpectralBasis, beta: float):
+    """Exact line-search initial coefficients (reconstruct.py:139-153) on the GPU."""
     views = e_inc.views if hasattr(e_inc, "views") else np.asarray(e_inc)
-    dev = DeviceProblem(ops, views, data.matrix, mf=basis.m_f, beta=beta, lambdas=(0, 0, 0), tau_b=0.5,
-                        mask=data.mask)
+    dev = _one_shot_device(ops, views, data, basis.m_f, beta)
     a0 = dev.init_alpha(torch.as_tensor(np.asarray(r0)[None], dtype=dev.cdt, device=dev.device))
     return a0[0].cpu().numpy()
 
 
-def recover_contrast(alpha, e_inc, ops: GreensOperators, basis: SpectralBasis):
+def recover_contrast(alpha, e_inc, ops: GreensOperators, basis: SpectralBasis, eps_reg: float | None = None,
+                     full: bool = False):
+    """Contrast implied by spectral coefficients (cie.py:83-99) on the GPU.
+
+    full=True returns the ContrastRecovery record; eps_reg overrides the
+    default floor 1e-10 max_i ||E_i||^2 / M^2 (cie.py:42-50)."""
     alpha = np.atleast_2d(np.asarray(alpha, dtype=np.complex128))
-    if alpha.shape[0] != e_inc.shape[0]:
+    views = e_inc.views if hasattr(e_inc, "views") else np.asarray(e_inc)
+    if alpha.shape[0] != views.shape[0]:
         raise ValueError("need one coefficient vector per incidence view")
-    dev = DeviceProblem(ops, e_inc, np.ones((e_inc.shape[0], ops.n_rx), complex), mf=basis.m_f, beta=6.0,
-                        lambdas=(0, 0, 0), tau_b=0.5)
-    _, chi = dev.loss_value(_cdev(alpha[None], dev), want_chi=True)
-    return chi[0].cpu().numpy()
+    dev = _one_shot_device(ops, views, None, basis.m_f, 6.0)
+    a = _cdev(alpha[None], dev)
+    if eps_reg is None and not full:
+        _, chi = dev.loss_value(a, want_chi=True)     # the fused library path
+        return chi[0].cpu().numpy()
+    parts = _recovery_dev(dev, a[0], eps_reg)
+    return _recovery_host(*parts) if full else parts[-1].cpu().numpy()
 
 
 def apply_cco(chi: np.ndarray, params: CcoParams) -> np.ndarray:
+    """Contrast-compensated operator (filters.py:56-67) on the GPU."""
+    from .engine import GRID_SIZES
     chi = np.asarray(chi, dtype=np.complex128)
     M = chi.shape[0]
-    if chi.shape != (M, M) or M not in (16, 32, 64, 128):
-        raise ValueError("apply_cco on the GPU needs a square power-of-two image (16..128)")
+    if chi.ndim != 2 or chi.shape != (M, M) or M not in GRID_SIZES:
+        raise ValueError(f"apply_cco on the GPU needs a square image with edge in {GRID_SIZES}, got {chi.shape}")
     dev = _cco_device(M)
     out = dev.apply_cco(_cdev(chi[None], dev), params)
     return out[0].cpu().numpy()

@@ -929,8 +929,13 @@ template <typename T>
 static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, double* bd, double* trace, int fused,
                      cudaStream_t st, cudaEvent_t* ev = nullptr) {
   // phase order (PDF_NPHASES = 10): fwd_l1 fwd_l2 fwd_l3 view_fwd pixel view_bwd finalize bwd_l3 bwd_l2 bwd_l1
-  // PDF_SKIP_PHASES (bitmask, measurement experiments only) drops kernels.
+  // PDF_SKIP_PHASES (bitmask) drops kernels: measurement experiments only,
+  // compiled in only with -DPDF_EXPERIMENTS (never in the product library)
+#ifdef PDF_EXPERIMENTS
   static const int skip = env_int("PDF_SKIP_PHASES", 0);
+#else
+  constexpr int skip = 0;
+#endif
   int ph = 0;
   auto mark = [&]() {
     if (ev) cudaEventRecord(ev[ph], st);

@@ -25,6 +25,57 @@ def _stream():
     return ct.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+GRID_SIZES = (16, 32, 64, 128, 256)
+MAX_VIEWS = 80
+MAX_RECEIVERS = 80
+
+
+def check_supported(ops, e_inc: np.ndarray, data: np.ndarray, mf: int, joint: bool = False) -> None:
+    """Reject, before any pointer reaches the C ABI, the problems the sm_100a
+    kernels do not cover ('Supported shapes'): the grid
+    must be square with a power-of-two edge in [16, 256], at most 80
+    incidences and 80 receivers, and every operator must have the shape the
+    grid implies.  The reference accepts any m1 x m2; there is no host path
+    here, so an unsupported shape is a ValueError naming the limit."""
+    if e_inc.ndim not in (3, 4):
+        raise ValueError(f"e_inc must be (n, m1, m2) or (S, n, m1, m2), got shape {e_inc.shape}")
+    m1, m2 = e_inc.shape[-2], e_inc.shape[-1]
+    if m1 != m2:
+        raise ValueError(f"unsupported grid {m1}x{m2}: the GPU path needs a square grid (m1 == m2)")
+    M = m1
+    if M not in GRID_SIZES:
+        raise ValueError(f"unsupported grid {M}x{M}: the edge must be one of {GRID_SIZES}")
+    if (ops.m1, ops.m2) != (M, M):
+        raise ValueError(f"operators were built for a {ops.m1}x{ops.m2} grid, e_inc is {M}x{M}")
+    if tuple(np.shape(ops.gd_kernel_hat)) != (2 * M, 2 * M):
+        raise ValueError(f"gd_kernel_hat must be ({2 * M}, {2 * M}), got {np.shape(ops.gd_kernel_hat)}")
+    S, n, R = data.shape
+    if tuple(np.shape(ops.gs_matrix)) != (R, M * M):
+        raise ValueError(f"gs_matrix must be ({R}, {M * M}) for {R} receivers, got {np.shape(ops.gs_matrix)}")
+    if e_inc.shape[-3] != n:
+        raise ValueError(f"e_inc has {e_inc.shape[-3]} views, the data {n}")
+    if e_inc.ndim == 4 and e_inc.shape[0] != S:
+        raise ValueError(f"per-scene e_inc has {e_inc.shape[0]} scenes, the data {S}")
+    if n > MAX_VIEWS:
+        raise ValueError(f"{n} incidences: the GPU path supports at most {MAX_VIEWS}")
+    if R > MAX_RECEIVERS:
+        raise ValueError(f"{R} receivers: the GPU path supports at most {MAX_RECEIVERS}")
+    if mf < 1 or 2 * mf > M:
+        raise ValueError(f"m_f = {mf}: need 1 <= m_f and 2 m_f <= {M}")
+
+
+def check_config_supported(config) -> None:
+    """check_supported() on an ImagingConfig, before any operator is built."""
+    if config.m1 != config.m2:
+        raise ValueError(f"unsupported grid {config.m1}x{config.m2}: the GPU path needs a square grid (m1 == m2)")
+    if config.m1 not in GRID_SIZES:
+        raise ValueError(f"unsupported grid {config.m1}x{config.m2}: the edge must be one of {GRID_SIZES}")
+    if config.n_tx > MAX_VIEWS:
+        raise ValueError(f"{config.n_tx} incidences: the GPU path supports at most {MAX_VIEWS}")
+    if config.n_rx > MAX_RECEIVERS:
+        raise ValueError(f"{config.n_rx} receivers: the GPU path supports at most {MAX_RECEIVERS}")
+
+
 class DeviceProblem:
     """S scenes sharing one geometry, resident in HBM.
 
@@ -34,13 +85,8 @@ class DeviceProblem:
 
     def __init__(self, ops, e_inc, data, *, mf: int, beta: float, lambdas, tau_b: float, mask=None,
                  r_fixed=None, joint: bool = False, lr: float = 1e-2, dtype: str = "f64",
-                 device: str | torch.device = "cuda"):
-        if not torch.cuda.is_available():
-            raise RuntimeError("the PDF hot path needs a CUDA device (no CPU fallback)")
-        self.lib = N.lib()
-        self.device = torch.device(device)
-        self.rdt = torch.float64 if dtype == "f64" else torch.float32
-        self.cdt = torch.complex128 if dtype == "f64" else torch.complex64
+                 device: str | torch.device = "cuda", adam_b1: float = 0.9, adam_b2: float = 0.999,
+                 adam_eps: float = 1e-8):
         data = np.asarray(data)
         if data.ndim == 2:
             data = data[None]
@@ -48,6 +94,13 @@ class DeviceProblem:
         e_inc = np.asarray(e_inc)
         shared = e_inc.ndim == 3
         M = e_inc.shape[-1]
+        check_supported(ops, e_inc, data, mf, joint)    # before any device work
+        if not torch.cuda.is_available():
+            raise RuntimeError("the PDF hot path needs a CUDA device (no CPU fallback)")
+        self.lib = N.lib()
+        self.device = torch.device(device)
+        self.rdt = torch.float64 if dtype == "f64" else torch.float32
+        self.cdt = torch.complex128 if dtype == "f64" else torch.complex64
         self.S, self.n, self.R, self.M, self.mf = S, n, R, M, mf
         self.m0 = 4 * mf * mf
         self.beta, self.lambdas, self.tau_b = float(beta), tuple(float(x) for x in lambdas), float(tau_b)
@@ -90,7 +143,7 @@ class DeviceProblem:
         d.beta = self.beta
         d.lambda1, d.lambda2, d.lambda3 = self.lambdas
         d.tau_b = self.tau_b
-        d.lr, d.adam_b1, d.adam_b2, d.adam_eps = float(lr), 0.9, 0.999, 1e-8
+        d.lr, d.adam_b1, d.adam_b2, d.adam_eps = float(lr), float(adam_b1), float(adam_b2), float(adam_eps)
         d.e_inc = self.e_inc.data_ptr()
         d.e_inc_scene_stride = 0 if shared else n * M * M
         d.gd_kernel_hat = self.khat.data_ptr()

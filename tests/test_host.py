@@ -276,3 +276,50 @@ def test_loss_trace_is_a_lazy_sequence_of_breakdowns():
     assert [b.total for b in tr] == [5.0, 11.0, 17.0]
     assert tr[-1].state == 12.0 and tr[1:][0].data == 7.0
     assert np.array_equal(tr.as_array(), rows)
+
+
+# ------------------------------------------------------------------ supported shapes (checked before the ABI)
+def test_non_square_grid_rejected_before_the_abi():
+    from paper_2602_13805_b200 import build_array, build_grid, build_greens, incident_fields
+    from paper_2602_13805_b200.config import ImagingConfig
+    from paper_2602_13805_b200.engine import DeviceProblem, check_config_supported, check_supported
+    cfg = ImagingConfig(m1=32, m2=64, m_f=3, n_tx=8, n_rx=8).validate()   # the reference accepts it
+    grid, arr = build_grid(cfg), build_array(cfg)
+    ops = build_greens(cfg, arr, grid)
+    e_inc = incident_fields(cfg, arr, grid).views
+    data = np.ones((1, 8, 8), complex)
+    with pytest.raises(ValueError, match="square grid"):
+        check_config_supported(cfg)
+    with pytest.raises(ValueError, match="square grid"):
+        check_supported(ops, e_inc, data, 3)
+    with pytest.raises(ValueError, match="square grid"):
+        DeviceProblem(ops, e_inc, data, mf=3, beta=6.0, lambdas=(0, 0, 0), tau_b=0.5)
+    # transposed e_inc against 32x64 operators: square but mismatched operators
+    sq = np.ones((8, 32, 32), complex)
+    with pytest.raises(ValueError, match="operators were built"):
+        check_supported(ops, sq, data, 3)
+
+
+def test_reconstruct_rejects_unsupported_shapes_up_front():
+    from paper_2602_13805_b200 import ScatteredData, reconstruct
+    from paper_2602_13805_b200.config import ImagingConfig
+    for kw, msg in ((dict(m1=40, m2=40), "edge must be one of"), (dict(n_tx=81), "incidences"),
+                    (dict(n_rx=96), "receivers")):
+        cfg = ImagingConfig(**{**dict(m1=32, m2=32, m_f=3, n_tx=8, n_rx=8), **kw}).validate()
+        with pytest.raises(ValueError, match=msg):
+            reconstruct(cfg, ScatteredData(matrix=np.ones((cfg.n_tx, cfg.n_rx), complex)))
+
+
+def test_operator_shape_mismatch_rejected():
+    from dataclasses import replace
+    from paper_2602_13805_b200.engine import check_supported
+    s = Setup(cfg_tiny(), plane=False)
+    data = np.ones((1, 8, 8), complex)
+    check_supported(s.ops, s.e_inc, data, 3)
+    bad = replace(s.ops, gs_matrix=s.ops.gs_matrix[:, :100])
+    with pytest.raises(ValueError, match="gs_matrix"):
+        check_supported(bad, s.e_inc, data, 3)
+    with pytest.raises(ValueError, match="views"):
+        check_supported(s.ops, s.e_inc[:4], data, 3)
+    with pytest.raises(ValueError, match="m_f"):
+        check_supported(s.ops, s.e_inc, data, 9)
