@@ -24,6 +24,8 @@
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
  *   pdf_shard_step_a/b/c  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
  *                       (views split over ranks, caller all-reduces between the steps)
+ *   pdf_relative_error  relative_error                  reconstruct.py:243-247
+ *   pdf_count_components count_components               reconstruct.py:250-254
  *   pdf_get_error       PoleError / FloatingPointError  cie.py:27-29, losses.py:239-243,
  *                                                       network.py:221-222, 260-261
  *
@@ -170,6 +172,18 @@ int pdf_shard_step_a(pdf_ctx* ctx, const void* theta, double* red1, void* stream
 int pdf_shard_step_b(pdf_ctx* ctx, const double* red1, double* red2, void* chi_out, void* stream);
 int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* grad, double* breakdown,
                      void* stream);
+
+/* reconstruction metrics (reconstruct.py:243-254), context-free, float64 images.
+ * Real parts are read with an element stride (1 = float64 image, 2 = interleaved complex128) and
+ * `offset` is added to each (eps = chi + offset).  Results are DEVICE arrays of `count` entries.
+ *   pdf_relative_error    out[k] = ||Re a_k - Re b_k||_F / ||Re b_k||_F   (relative_error)
+ *   pdf_count_components  out[k] = 4-connected components of {Re a_k > threshold} (count_components,
+ *                         scipy.ndimage.label with the 4-neighbour structure); labels = device
+ *                         workspace of count * m1 * m2 int32 */
+int pdf_relative_error(const double* eps_hat, const double* eps_true, int32_t stride, int64_t n_pix, int32_t count,
+                       double offset, double* out, void* stream);
+int pdf_count_components(const double* eps, int32_t stride, int32_t m1, int32_t m2, int32_t count, double offset,
+                         double threshold, int32_t* labels, int32_t* out, void* stream);
 
 /* copies the per-scene sticky error words to host (synchronises stream), then clears them */
 int pdf_get_error(pdf_ctx* ctx, int32_t* err_host, void* stream);

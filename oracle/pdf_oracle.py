@@ -524,6 +524,28 @@ def relative_error(eps_hat, eps_true):
                  / np.linalg.norm(np.real(eps_true)))
 
 
+def count_components(eps_map, threshold) -> int:
+    """4-connected components of {Re eps > threshold} (reconstruct.py:250-254),
+    restated as an explicit-stack flood fill (the reference calls scipy.ndimage.label)."""
+    fgm = np.real(np.asarray(eps_map)) > threshold
+    m1, m2 = fgm.shape
+    seen = np.zeros_like(fgm)
+    n = 0
+    for r0, c0 in zip(*np.nonzero(fgm)):
+        if seen[r0, c0]:
+            continue
+        n += 1
+        seen[r0, c0] = True
+        stack = [(r0, c0)]
+        while stack:
+            r, c = stack.pop()
+            for rr, cc in ((r - 1, c), (r + 1, c), (r, c - 1), (r, c + 1)):
+                if 0 <= rr < m1 and 0 <= cc < m2 and fgm[rr, cc] and not seen[rr, cc]:
+                    seen[rr, cc] = True
+                    stack.append((rr, cc))
+    return n
+
+
 def reconstruct_loop(ctx: Context, alpha0, k_iters, lr=1e-2, seed=0, joint=False,
                      rdtype=np.float64, use_cco=True, cco_kw=None):
     """The reference's k-loop plus epilogue (reconstruct.py:208-226)."""

@@ -33,6 +33,7 @@ EXPORTS = (
     "pdf_expand", "pdf_truncate", "pdf_apply_cco", "pdf_get_error", "pdf_profile_train", "pdf_fp64_probe",
     "pdf_timeline_reset", "pdf_timeline_read", "pdf_ctx_paths",
     "pdf_net_setup_sharded", "pdf_shard_buffer_sizes", "pdf_shard_step_a", "pdf_shard_step_b", "pdf_shard_step_c",
+    "pdf_relative_error", "pdf_count_components",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
 
@@ -100,6 +101,8 @@ def lib():
         "pdf_shard_step_a": (ct.c_int, [vp, vp, vp, vp]),
         "pdf_shard_step_b": (ct.c_int, [vp, vp, vp, vp, vp]),
         "pdf_shard_step_c": (ct.c_int, [vp, vp, vp, vp, vp, vp]),
+        "pdf_relative_error": (ct.c_int, [vp, vp, i32, i64, i32, ct.c_double, vp, vp]),
+        "pdf_count_components": (ct.c_int, [vp, i32, i32, i32, i32, ct.c_double, ct.c_double, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)      # AttributeError names the missing symbol

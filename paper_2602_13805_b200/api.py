@@ -29,12 +29,12 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import torch
-from scipy import ndimage
 
 from .config import CcoParams, ImagingConfig
 from .engine import DeviceProblem, check_config_supported
 from .errors import PoleError, ZeroDataError  # noqa: F401  (re-exported)
 from .geometry import AntennaArray, ComplexGrid, build_array, build_grid
+from .metrics import count_components, relative_error, relative_error_dev  # noqa: F401  (GPU, reconstruct.py:243-254)
 from .operators import GreensOperators, ScatteredData, build_greens, incident_fields
 
 EPS_TV = 1e-12
@@ -442,18 +442,6 @@ class ReconstructionResult:
         return self.chi_cco.values + 1.0
 
 
-def relative_error(eps_hat: np.ndarray, eps_true: np.ndarray) -> float:
-    return float(np.linalg.norm(np.real(eps_hat) - np.real(eps_true)) / np.linalg.norm(np.real(eps_true)))
-
-
-FOUR_CONN = np.array([[0, 1, 0], [1, 1, 1], [0, 1, 0]], dtype=bool)
-
-
-def count_components(eps_map: np.ndarray, threshold: float) -> int:
-    _, n = ndimage.label(np.real(eps_map) > threshold, structure=FOUR_CONN)
-    return int(n)
-
-
 def _theta0(seeds, m0_eff: int) -> np.ndarray:
     """Reference-identical initial weights per scene (numpy PCG64 draws on the host cores)."""
     out = np.empty((len(seeds), _flat_size(m0_eff)))
@@ -644,6 +632,14 @@ class BatchReconstructor:
         ahat = dev.net_forward(theta)
         bd, chi = dev.loss_value(ahat, want_chi=True)
         chi_cco = dev.apply_cco(chi, cfg.cco) if cfg.use_cco else chi.clone()
+        rels = None
+        if chi_trues is not None and any(c is not None for c in chi_trues):
+            # relative_error(chi_cco.real + 1, chi_true.real + 1) of every scene in one device reduction
+            tr_h = np.zeros((self.S, self.config.m1, self.config.m2), complex)
+            for s_, c in enumerate(chi_trues):
+                if c is not None:
+                    tr_h[s_] = c.values if isinstance(c, ComplexGrid) else c
+            rels = relative_error_dev(chi_cco, torch.as_tensor(tr_h, device=dev.device), offset=1.0)
         if bool(dev.pole_flag):     # deferred checks of the initialisation (no host sync before the loop)
             raise PoleError("beta*chi + 1 vanishes at some pixel")
         if bool(dev.zero_grad_flag):
@@ -651,14 +647,14 @@ class BatchReconstructor:
         dev.check_errors()
         chi0_h, chi_h, cco_h = chi0.cpu().numpy(), chi.cpu().numpy(), chi_cco.cpu().numpy()
         tr_h, bd_h = trace.cpu().numpy(), bd.cpu().numpy()
+        rel_h = rels.cpu().numpy() if rels is not None else None
         wall = time.perf_counter() - t0
         out = []
         cs = self.grid.cell_size
         for s in range(self.S):
             rel = None
-            if chi_trues is not None and chi_trues[s] is not None:
-                ct_ = chi_trues[s].values if isinstance(chi_trues[s], ComplexGrid) else chi_trues[s]
-                rel = relative_error(cco_h[s].real + 1.0, np.real(ct_) + 1.0)
+            if rel_h is not None and chi_trues[s] is not None:
+                rel = float(rel_h[s])
             out.append(ReconstructionResult(
                 chi_hat=ComplexGrid(chi_h[s], cs), chi_cco=ComplexGrid(cco_h[s], cs),
                 chi0=ComplexGrid(chi0_h[s], cs),
@@ -717,7 +713,8 @@ def _reconstruct_frozen(config, data, array, chi_true, e_inc, dtype, t0):
     rel = None
     cco_h = chi_cco[0].cpu().numpy()
     if chi_true is not None:
-        rel = relative_error(cco_h.real + 1.0, chi_true.values.real + 1.0)
+        rel = float(relative_error_dev(chi_cco[0], torch.as_tensor(chi_true.values, device=dev.device),
+                                       offset=1.0)[0].item())
     tr = trace.cpu().numpy()
     return ReconstructionResult(chi_hat=ComplexGrid(chi[0].cpu().numpy(), cs), chi_cco=ComplexGrid(cco_h, cs),
                                 chi0=ComplexGrid(chi0[0].cpu().numpy(), cs),

@@ -1,6 +1,9 @@
 """Build libpdfb200.so in-tree for sm_100a (nvcc; no torch types in the ABI).
 
     python -m paper_2602_13805_b200.build [--force]
+
+Every csrc/*.cu is one translation unit, compiled in parallel to build/*.o
+and linked into one shared library.
 """
 from __future__ import annotations
 
@@ -11,16 +14,36 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build")
 OUT = os.path.join(HERE, "libpdfb200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+CFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+
+
+def units() -> list[str]:
+    return sorted(os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith(".cu"))
+
+
+def headers() -> list[str]:
+    hs = [os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith((".cuh", ".h"))]
+    return hs + [os.path.join(ROOT, "include", "pdf_abi.h")]
 
 
 def sources() -> list[str]:
-    out = [os.path.join(SRC, f) for f in sorted(os.listdir(SRC)) if f.endswith((".cu", ".cuh"))]
-    out.append(os.path.join(ROOT, "include", "pdf_abi.h"))
-    return out
+    return units() + headers()
+
+
+def _obj(cu: str) -> str:
+    return os.path.join(OBJ, os.path.basename(cu)[:-3] + ".o")
+
+
+def _stale(cu: str) -> bool:
+    o = _obj(cu)
+    if not os.path.exists(o):
+        return True
+    t = os.path.getmtime(o)
+    return any(os.path.getmtime(s) > t for s in [cu] + headers())
 
 
 def up_to_date() -> bool:
@@ -33,7 +56,21 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", os.path.join(SRC, "pdf_abi.cu")]
+    os.makedirs(OBJ, exist_ok=True)
+    todo = [cu for cu in units() if force or _stale(cu)]
+    procs = []
+    for cu in todo:
+        cmd = [NVCC, *CFLAGS, "-c", "-o", _obj(cu) + ".tmp", cu]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        procs.append((cu, subprocess.Popen(cmd)))
+    failed = [cu for cu, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(os.path.basename(f) for f in failed)}")
+    for cu in todo:
+        os.replace(_obj(cu) + ".tmp", _obj(cu))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", OUT + ".tmp", *[_obj(cu) for cu in units()]]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

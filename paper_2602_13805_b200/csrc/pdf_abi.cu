@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/pdf_abi.h"
+#include "pdf_internal.h"
 #include "pdf_aux.cuh"
 #include "pdf_common.cuh"
 #include "pdf_net.cuh"
@@ -41,6 +42,8 @@ static int fail(int code, const std::string& msg) {
   if (code == PDF_ECUDA) (void)cudaGetLastError();   // do not leak a stale error into the next call
   return code;
 }
+
+int pdf_fail(int code, const std::string& msg) { return fail(code, msg); }
 
 #define CK_CUDA(expr)                                                               \
   do {                                                                              \

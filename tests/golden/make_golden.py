@@ -235,8 +235,8 @@ def make_cfg3():
     plane_case("cfg3", cfg, scene, 20.0, 2, 500)
 
 
-def make_cfg4(n_scenes=2, k=500):
-    for idx in range(n_scenes):
+def make_cfg4(n_scenes=2, k=500, first=0):
+    for idx in range(first, first + n_scenes):
         cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
                             k_iters=k, rng_seed=idx).validate()
         scene, rng = cfg4_scene(idx)
@@ -278,6 +278,110 @@ def make_cfg5(k=300):
     out = composed_reconstruct(cfg, data, views, ops, chi, k)
     save("cfg5", trace=out["trace"], final=out["final"], rel_error=np.array(out["rel_error"]), **common)
     print(f"cfg5: rel_error {out['rel_error']:.6f}  ({time.time() - t0:.1f}s)", flush=True)
+
+
+def make_edges():
+    """Edge cases the reference's own tests pin, on its tiny setup (tests/conftest.py:43-57):
+    pole (cie.py:24-30, tests/test_cie.py:29), state = 0 at R = 0 (tests/test_losses.py:128-133),
+    masked data = 1 at alpha = 0 (tests/test_losses.py:105-119), dead-mode whitening floor and
+    the global-rms = 0 branch (network.py:88-104, tests/test_network.py:63-70)."""
+    from dataclasses import replace
+    from pdfisp.cie import PoleError
+    from pdfisp.losses import pipeline_forward
+    cfg = ImagingConfig(m1=16, m2=16, m_f=3, n_tx=8, n_rx=8, k_iters=30).validate()
+    grid, arr = build_grid(cfg), build_array(cfg)
+    ops = build_greens(cfg, arr, grid)
+    einc = incident_fields(cfg, arr, grid)
+    basis = SpectralBasis(16, 16, 3)
+    sim = simulate(cfg, builtin_scene("austria", 2.0, scale=0.9))
+    lam = (1e-3, 1e-5, 1e-5)
+    ctx = LossContext(data=sim.data, e_inc=einc.views, ops=ops, basis=basis, beta=6.0, lambdas=lam, tau_b=0.5)
+    n, m0 = 8, basis.m0
+    # pole: G_D switched off (K^ = 0), one unit incident view, a constant current J = c with
+    # c = -(1 + eps_reg) / beta, so chi = J conj(E) / (|E|^2 + eps_reg) = -1 / beta to rounding
+    ops0 = replace(ops, gd_kernel_hat=np.zeros_like(ops.gd_kernel_hat))
+    e1 = np.ones((1, 16, 16), complex)
+    d1 = ScatteredData(matrix=sim.data.matrix[:1])
+    ctx_pole = LossContext(data=d1, e_inc=e1, ops=ops0, basis=basis, beta=6.0, lambdas=lam, tau_b=0.5)
+    c = -(1.0 + 1e-10) / 6.0
+    alpha_pole = np.zeros((1, m0), complex)
+    alpha_pole[0, 0] = c * 256.0          # slot 0 = DC: expand gives c at every pixel
+    try:
+        pipeline_forward(alpha_pole, ctx_pole)
+        raise SystemExit("the reference did not raise PoleError")
+    except PoleError:
+        pass
+    # a nearby non-pole point evaluates (the device must not flag it)
+    alpha_near = alpha_pole * 1.001
+    g_near, bd_near = grad_alpha(alpha_near, ctx_pole)
+    # state term 0 at R = 0 (frozen R = 0, alpha = 0)
+    ctx_r0 = LossContext(data=sim.data, e_inc=einc.views, ops=ops, basis=basis, beta=6.0, lambdas=lam, tau_b=0.5,
+                         r_fixed=np.zeros((16, 16), complex))
+    g_r0, bd_r0 = grad_alpha(np.zeros((n, m0), complex), ctx_r0)
+    assert bd_r0.state == 0.0
+    # masked data term = 1 at alpha = 0
+    mask = np.zeros((n, 8))
+    mask[:, :4] = 1.0
+    ctx_mk = LossContext(data=ScatteredData(matrix=sim.data.matrix, mask=mask), e_inc=einc.views, ops=ops,
+                         basis=basis, beta=6.0, lambdas=lam, tau_b=0.5)
+    g_mk0, bd_mk0 = grad_alpha(np.zeros((n, m0), complex), ctx_mk)
+    # whitening floor (a dead mode) and the global-rms = 0 branch
+    chi0, r0 = bp_initialize(sim.data, einc, ops, 6.0)
+    alpha0 = init_alpha(r0, sim.data, einc, ops, basis, 6.0)
+    alpha_dead = alpha0.copy()
+    alpha_dead[:, 0] = 0.0
+    params = network.init_network(m0, np.random.default_rng(5))
+    flat = network.flatten_params(params)
+    flat = flat + 0.05 * np.random.default_rng(5).standard_normal(flat.size)
+    params = network.unflatten_params(flat, params)
+    dalpha_dead = network.forward_net(params, alpha_dead)
+    grad_dead, bd_dead = network.grad_loss(params, alpha_dead, ctx)
+    alpha_zero = np.zeros((n, m0), complex)
+    dalpha_zero = network.forward_net(params, alpha_zero)
+    grad_zero, bd_zero = network.grad_loss(params, alpha_zero, ctx)
+    save("edges", alpha_pole=alpha_pole, data1=d1.matrix, alpha_near=alpha_near, g_near=g_near,
+         bd_near=np.array(bd_near.as_row()), g_r0=g_r0, bd_r0=np.array(bd_r0.as_row()), mask=mask,
+         g_mk0=g_mk0, bd_mk0=np.array(bd_mk0.as_row()), alpha0=alpha0, alpha_dead=alpha_dead, net_flat=flat,
+         dalpha_dead=dalpha_dead, grad_dead=grad_dead, bd_dead=np.array(bd_dead.as_row()),
+         dalpha_zero=dalpha_zero, grad_zero=grad_zero, bd_zero=np.array(bd_zero.as_row()))
+
+
+def make_metrics():
+    """relative_error / count_components (reconstruct.py:243-254) on images of many shapes."""
+    from pdfisp.reconstruct import count_components as cc_ref, relative_error as re_ref
+    from pdfisp.scenes import austria_preset
+    rng = np.random.default_rng(21)
+    shapes = [(6, 6), (12, 10), (9, 31), (32, 48), (64, 64), (256, 256), (1, 17), (17, 1)]
+    imgs, counts, thr = [], [], 1.5
+    for sh in shapes:
+        for dens in (0.2, 0.45, 0.59, 0.8):
+            img = np.where(rng.random(sh) < dens, 2.0, 1.0)
+            imgs.append(img)
+            counts.append(cc_ref(img, thr))
+    # a one-pixel-wide serpentine (one component of 64 x 64 / 2 pixels, long union chains)
+    snake = np.ones((64, 64))
+    snake[::2, :] = 2.0
+    for r in range(1, 64, 2):
+        snake[r, 63 if (r // 2) % 2 == 0 else 0] = 2.0
+    chk = np.indices((32, 32)).sum(0) % 2 + 1.0     # checkerboard: 4-connectivity isolates every cell
+    grid = build_grid(ImagingConfig())
+    aus = rasterize(austria_preset(2.0), grid).values.real + 1.0
+    extra = [snake, chk * 1.6 / 1.5, aus, np.zeros((8, 8)), np.full((8, 8), 2.0)]
+    ex_counts = [cc_ref(x, thr) for x in extra]
+    a = rng.standard_normal((3, 32, 32)) + 1j * rng.standard_normal((3, 32, 32))
+    b = rng.standard_normal((3, 32, 32)) + 1j * rng.standard_normal((3, 32, 32))
+    rels = [re_ref(a[k].real + 1.0, b[k].real + 1.0) for k in range(3)]
+    # images are stored as uint8 masks of {Re eps > 1.5} scaled back to eps in {1, 2} by the tests
+    arrs = {f"img{k}": (x > thr).astype(np.uint8) for k, x in enumerate(imgs)}
+    arrs.update({f"extra{k}": (x > thr).astype(np.uint8) for k, x in enumerate(extra)})
+    save("metrics", counts=np.array(counts), extra_counts=np.array(ex_counts), rel_a=a, rel_b=b,
+         rels=np.array(rels), thr=np.array(thr), **arrs)
+    print("counts", counts, ex_counts)
+
+
+def make_cfg4more():
+    """Eight more config-4 scenes (indices 2-9), 500 iterations each."""
+    make_cfg4(n_scenes=8, first=2)
 
 
 if __name__ == "__main__":

@@ -96,3 +96,64 @@ def test_cfg1_step_and_trajectory(cfg1_setup, g_cfg1):
     np.testing.assert_allclose(tot, g["trace"][:, 5], rtol=1e-7)
     r = O.relative_error(out["chi_cco"].real + 1, g["chi_true"].real + 1)
     assert abs(r - float(g["rel_error"])) < 1e-8
+
+
+# ------------------------------------------------------------------ edge cases the reference's tests pin
+@pytest.fixture(scope="module")
+def g_edges():
+    from conftest import golden
+    return golden("edges")
+
+
+def _pole_ctx(setup, g):
+    from dataclasses import replace
+    ops0 = replace(oracle_ops(setup), k_hat=np.zeros((32, 32), complex))
+    return O.Context(g["data1"], np.ones((1, 16, 16), complex), ops0, 3, 6.0, LAM, 0.5)
+
+
+def test_edges_pole(tiny_setup, g_edges):
+    """cie.py:24-30 (tests/test_cie.py:29): beta chi + 1 = 0 at a pixel raises."""
+    ctx = _pole_ctx(tiny_setup, g_edges)
+    with pytest.raises(O.OraclePoleError):
+        O.grad_alpha(g_edges["alpha_pole"], ctx)
+    got, parts = O.grad_alpha(g_edges["alpha_near"], ctx)
+    assert rel(got, g_edges["g_near"]) < 1e-12
+
+
+def test_edges_state_zero_and_masked_data(tiny_setup, g_tiny, g_edges):
+    """tests/test_losses.py:128-133 (state = 0 at R = 0) and :105-119 (masked data = 1 at alpha = 0)."""
+    g = g_edges
+    zero = np.zeros((8, 36), complex)
+    got, parts = O.grad_alpha(zero, _ctx(tiny_setup, g_tiny, r_fixed=np.zeros((16, 16), complex)))
+    assert parts["state"] == 0.0 and g["bd_r0"][0] == 0.0
+    assert rel(got, g["g_r0"]) < 1e-12
+    got, parts = O.grad_alpha(zero, _ctx(tiny_setup, g_tiny, mask=g["mask"]))
+    assert parts["data"] == pytest.approx(1.0, rel=1e-14) and g["bd_mk0"][1] == pytest.approx(1.0, rel=1e-14)
+    assert rel(got, g["g_mk0"]) < 1e-12
+
+
+def test_edges_whitening_floor_and_zero_rms(tiny_setup, g_tiny, g_edges):
+    """network.py:88-104 (tests/test_network.py:63-70): a dead mode hits the floor; rms 0 gives unit scales."""
+    g = g_edges
+    like = O.init_net(36, np.random.default_rng(5))
+    params = O.unflat(g["net_flat"], like)
+    ctx = _ctx(tiny_setup, g_tiny)
+    for a, da, gr in (("alpha_dead", "dalpha_dead", "grad_dead"), ("alpha_zero", None, "grad_zero")):
+        alpha = g[a] if a in g else np.zeros((8, 36), complex)
+        want_da = g[da] if da else g["dalpha_zero"]
+        assert rel(O.delta_alpha(params, alpha), want_da) < 1e-12
+        grad, _ = O.grad_loss(params, alpha, ctx)
+        assert rel(grad, g[gr]) < 1e-12
+
+
+def test_metrics_match_reference():
+    """relative_error / count_components (reconstruct.py:243-254) against the reference's outputs."""
+    from conftest import golden
+    g = golden("metrics")
+    thr = float(g["thr"])
+    for k, want in enumerate(g["counts"]):
+        assert O.count_components(g[f"img{k}"] + 1.0, thr) == want, k
+    for k, want in enumerate(g["extra_counts"]):
+        assert O.count_components(g[f"extra{k}"] + 1.0, thr) == want, k
+    for k, want in enumerate(g["rels"]):
+        assert abs(O.relative_error(g["rel_a"][k].real + 1.0, g["rel_b"][k].real + 1.0) - want) < 1e-15
