@@ -24,6 +24,8 @@
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
  *   pdf_shard_step_a/b/c  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
  *                       (views split over ranks, caller all-reduces between the steps)
+ *   pdf_solve_total_field _solve_bicgstab /            forward.py:193-248,
+ *                       solve_total_field               forward.py:251-275
  *   pdf_relative_error  relative_error                  reconstruct.py:243-247
  *   pdf_count_components count_components               reconstruct.py:250-254
  *   pdf_get_error       PoleError / FloatingPointError  cie.py:27-29, losses.py:239-243,
@@ -69,7 +71,8 @@ enum pdf_status {
   PDF_OK = 0,
   PDF_EINVAL = -1,      /* bad argument / unsupported shape */
   PDF_ECUDA = -2,       /* CUDA runtime error */
-  PDF_ENOMEM = -3       /* workspace too small */
+  PDF_ENOMEM = -3,      /* workspace too small */
+  PDF_ENOCONV = -4      /* NoConvergenceError: an iterative solve stopped at maxiter */
 };
 
 typedef struct pdf_ctx pdf_ctx;
@@ -172,6 +175,19 @@ int pdf_shard_step_a(pdf_ctx* ctx, const void* theta, double* red1, void* stream
 int pdf_shard_step_b(pdf_ctx* ctx, const double* red1, double* red2, void* chi_out, void* stream);
 int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* grad, double* breakdown,
                      void* stream);
+
+/* forward solve (method of moments): (I - G_D chi) x = b for the n views of
+ * S scenes by batched BiCGStab with the reference's restart clause, on the context's G_D (the context
+ * must be float64; its S / n / R are not used).  chi [S][m1][m2], b [S or 1][n][m1][m2] (b_scene_stride
+ * elements between scenes, 0 = shared), x [S][n][m1][m2] output; workspace (device) of
+ * pdf_solver_workspace_bytes(ctx, S * n) bytes.  residuals (device [S * n], may be NULL) receives
+ * ||x - b - G_D(chi x)|| / ||b|| per view; *iters_out (host) the iterations run.  Synchronises
+ * `stream` every few iterations.  Returns PDF_ENOCONV (message names the views above tol) when some
+ * view has not converged at the check before iteration maxiter - 1, as the reference raises. */
+size_t pdf_solver_workspace_bytes(const pdf_ctx* ctx, int32_t count_views);
+int pdf_solve_total_field(pdf_ctx* ctx, const void* chi, const void* b, int64_t b_scene_stride, void* x, int32_t S,
+                          int32_t n, double tol, int32_t maxiter, void* workspace, size_t workspace_bytes,
+                          double* residuals, int32_t* iters_out, void* stream);
 
 /* reconstruction metrics (reconstruct.py:243-254), context-free, float64 images.
  * Real parts are read with an element stride (1 = float64 image, 2 = interleaved complex128) and

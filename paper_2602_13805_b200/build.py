@@ -65,10 +65,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         procs.append((cu, subprocess.Popen(cmd)))
     failed = [cu for cu, p in procs if p.wait() != 0]
+    for cu in todo:
+        if cu not in failed:
+            os.replace(_obj(cu) + ".tmp", _obj(cu))
     if failed:
         raise subprocess.CalledProcessError(1, f"nvcc {' '.join(os.path.basename(f) for f in failed)}")
-    for cu in todo:
-        os.replace(_obj(cu) + ".tmp", _obj(cu))
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            "-o", OUT + ".tmp", *[_obj(cu) for cu in units()]]
     if verbose:

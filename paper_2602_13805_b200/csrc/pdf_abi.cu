@@ -1152,6 +1152,13 @@ extern "C" int pdf_net_dims(const pdf_ctx* c, int32_t* rows, int32_t* d0, int32_
   return PDF_OK;
 }
 
+int pdf_ctx_info(const pdf_ctx* c, int* M, int* dtype) {
+  if (!c) return fail(PDF_EINVAL, "null ctx");
+  if (M) *M = c->M;
+  if (dtype) *dtype = c->d.dtype;
+  return PDF_OK;
+}
+
 #define DISPATCH(c, fn, ...) ((c)->d.dtype == PDF_F64 ? fn<double>(__VA_ARGS__) : fn<float>(__VA_ARGS__))
 
 template <typename T>

@@ -11,3 +11,7 @@ int pdf_fail(int code, const std::string& msg);
     cudaError_t e_ = (expr);                                                                \
     if (e_ != cudaSuccess) return pdf_fail(PDF_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+struct pdf_ctx;
+// grid edge M and element type (enum pdf_dtype) of a context
+int pdf_ctx_info(const pdf_ctx* c, int* M, int* dtype);

@@ -1,16 +1,20 @@
 """Operator construction and the fixture forward model (host, one-time setup).
 
 Out of the per-iteration hot path (SURVEY 2.1 marks these one-time): the
-Green's operators are assembled once per geometry in float64 on the host and
-uploaded; synthetic measurements come from a method-of-moments solve.
+Green's operators are assembled once per geometry in float64 (host scipy here,
+or on the GPU by greens.build_greens_gpu) and uploaded; synthetic
+measurements come from a method-of-moments solve (dense LU on the host up to
+1024 cells, the library's batched BiCGStab on the GPU above, as the
+reference's 'auto' choice).
 
 Physics follows the reference exactly (forward.py:1-374): time convention
 exp(-i w t), first-kind Hankel H0^(1), equal-area-disk cell quadrature
 (radius a = h / sqrt(pi)), off-diagonal (i pi k0 a/2) J1(k0 a) H0(k0 rho),
 self term (i pi k0 a/2) H1(k0 a) - 1, wrap-indexed (2 m1, 2 m2) kernel with
-row m1 / column m2 zeroed.  Bessel functions come from scipy.special (the
-reference's own Chebyshev fits agree with it to ~1e-15, pinned in
-tests/test_setup_parity.py).
+row m1 / column m2 zeroed.  Bessel functions come from scipy.special here (the
+reference's own Chebyshev fits agree with it to ~1e-15; the operators are
+pinned against the reference's golden K^ / G_S in tests/test_oracle.py and
+tests/test_host.py).
 """
 from __future__ import annotations
 
@@ -130,53 +134,13 @@ def apply_gd_host(ops: GreensOperators, x: np.ndarray) -> np.ndarray:
     return y[..., :m1, :m2]
 
 
-def _bicgstab(chi: np.ndarray, b: np.ndarray, ops: GreensOperators, tol: float, maxiter: int):
-    """BiCGStab on (I - G_D chi) x = b, all views at once, per-view restarts."""
-    A = lambda v: v - apply_gd_host(ops, chi * v)   # noqa: E731
-    dot = lambda u, v: np.einsum("nij,nij->n", np.conj(u), v)   # noqa: E731
-    nb = np.sqrt(dot(b, b).real)
-    nb[nb == 0] = 1.0
-    x = b.copy()
-    r = b - A(x)
-    r0 = r.copy()
-    rho = alpha = om = np.ones(b.shape[0], dtype=np.complex128)
-    v = np.zeros_like(b)
-    p = np.zeros_like(b)
-    res = np.sqrt(dot(r, r).real) / nb
-    for _ in range(maxiter):
-        if np.all(res <= tol):
-            return x
-        act = (res > tol)[:, None, None]
-        rho1 = dot(r0, r)
-        lost = np.abs(rho1) < 1e-300 * np.abs(dot(r, r))
-        if lost.any():
-            sel = lost[:, None, None]
-            r0 = np.where(sel, r, r0)
-            p = np.where(sel, 0.0, p)
-            v = np.where(sel, 0.0, v)
-            rho1 = np.where(lost, dot(r0, r), rho1)
-            om = np.where(lost, 1.0, om)
-            alpha = np.where(lost, 1.0, alpha)
-            rho = np.where(lost, 1.0, rho)
-        beta = (rho1 / np.where(rho == 0, 1, rho)) * (alpha / np.where(om == 0, 1, om))
-        rho = rho1
-        p = np.where(act, r + beta[:, None, None] * (p - om[:, None, None] * v), p)
-        v = np.where(act, A(p), v)
-        den = dot(r0, v)
-        alpha = rho / np.where(den == 0, 1, den)
-        s = r - alpha[:, None, None] * v
-        t = A(s)
-        tt = dot(t, t).real
-        om = dot(t, s) / np.where(tt == 0, 1, tt)
-        x = np.where(act, x + alpha[:, None, None] * p + om[:, None, None] * s, x)
-        r = np.where(act, s - om[:, None, None] * t, r)
-        res = np.where(act[:, 0, 0], np.sqrt(dot(r, r).real) / nb, res)
-    raise NoConvergenceError(f"forward solve: {int((res > tol).sum())} view(s) above tol after {maxiter}")
-
-
 def solve_total_field(chi: ComplexGrid, e_inc: FieldSet, ops: GreensOperators, tol: float = 1e-8,
                       maxiter: int = 2000, method: str = "auto") -> FieldSet:
-    """E = E_inc + G_D (chi E) for every view (reference forward.py:251-275)."""
+    """E = E_inc + G_D (chi E) for every view (reference forward.py:251-275).
+
+    method 'dense' LU-solves the explicit operator on the host (small grids),
+    'fft' runs the batched BiCGStab on the GPU (raises NoConvergenceError),
+    'auto' picks dense up to 1024 cells, as the reference does."""
     c = chi.values
     b = e_inc.views
     if c.shape != b.shape[-2:]:
@@ -191,13 +155,16 @@ def solve_total_field(chi: ComplexGrid, e_inc: FieldSet, ops: GreensOperators, t
         dj = (jj[:, None] - jj[None, :]) % (2 * ops.m2)
         G = ops.gd_kernel[di, dj]
         x = np.linalg.solve(np.eye(m) - G * c.ravel()[None, :], b.reshape(-1, m).T).T.reshape(b.shape)
+        num = x - b - apply_gd_host(ops, c * x)
+        nb = np.sqrt(np.sum(np.abs(b) ** 2, axis=(1, 2)))
+        res = np.sqrt(np.sum(np.abs(num) ** 2, axis=(1, 2))) / np.where(nb > 0, nb, 1.0)
     elif method == "fft":
-        x = _bicgstab(c, b, ops, tol, maxiter)
+        # batched BiCGStab on the GPU (solver.py, csrc/pdf_solver.cu; forward.py:193-248)
+        from .solver import solve_fields_gpu
+        xd, rd, _ = solve_fields_gpu(c, b, ops, tol=tol, maxiter=maxiter)
+        x, res = xd[0].cpu().numpy(), rd[0].cpu().numpy()
     else:
         raise ValueError(f"unknown method {method!r}")
-    num = x - b - apply_gd_host(ops, c * x)
-    res = (np.sqrt(np.sum(np.abs(num) ** 2, axis=(1, 2)))
-           / np.maximum(np.sqrt(np.sum(np.abs(b) ** 2, axis=(1, 2))), 1e-300))
     return FieldSet(views=x, role="total", residuals=res)
 
 

@@ -3,9 +3,8 @@
 Synthetic inputs stand in for the paper's scenes (BASELINE.json configs):
 plane-wave incidences, lambda = 1 m (frequency = C0), m_f mapped from the
 "N x N modes" wording as m_f = (N+1)/2.  Measurements are
-synthesised by a method-of-moments solve of E = E_inc + G_D(chi E) -- on the
-GPU (batched BiCGStab over the library's G_D primitive) for bench-sized
-batches, or on the host (operators.simulate) -- then G_S(chi E) plus circular
+synthesised by a method-of-moments solve of E = E_inc + G_D(chi E) -- the
+library's batched BiCGStab on the GPU (pdf_solve_total_field) -- then G_S(chi E) plus circular
 AWGN drawn with numpy's generator exactly as the reference's add_awgn.
 Fixture synthesis is out of the timed hot path.
 """
@@ -122,44 +121,11 @@ def synthesize_gpu(config: ImagingConfig, scenes, rngs, snr_db: float, tol: floa
     e_inc = plane_wave_fields(config, grid).views
     S, n = len(scenes), e_inc.shape[0]
     chis = np.stack([rasterize(s, grid).values for s in scenes])
+    from .solver import solve_fields_gpu
+    x, _, _ = solve_fields_gpu(chis, e_inc, ops, tol=tol, maxiter=maxiter)    # batched BiCGStab (pdf_solver.cu)
     dev = DeviceProblem(ops, e_inc, np.ones((S, n, arr.n_rx), complex), mf=1, beta=config.beta,
                         lambdas=(0, 0, 0), tau_b=0.5)
     chi = torch.as_tensor(chis, device=dev.device)[:, None]
-    b = torch.as_tensor(e_inc, device=dev.device).unsqueeze(0).expand(S, -1, -1, -1).contiguous()
-
-    def A(v):
-        return v - dev.apply_gd(chi * v)
-
-    def dot(u, v):
-        return torch.sum(u.conj() * v, dim=(-1, -2))
-
-    nb = torch.sqrt(dot(b, b).real).clamp_min(1e-300)
-    x = b.clone()
-    r = b - A(x)
-    r0 = r.clone()
-    one = torch.ones_like(nb, dtype=b.dtype)
-    rho, alpha, om = one.clone(), one.clone(), one.clone()
-    v = torch.zeros_like(b)
-    p = torch.zeros_like(b)
-    res = torch.sqrt(dot(r, r).real) / nb
-    for _ in range(maxiter):
-        if bool((res <= tol).all()):
-            break
-        act = (res > tol)[..., None, None]
-        rho1 = dot(r0, r)
-        beta_ = (rho1 / torch.where(rho == 0, one, rho)) * (alpha / torch.where(om == 0, one, om))
-        rho = rho1
-        p = torch.where(act, r + beta_[..., None, None] * (p - om[..., None, None] * v), p)
-        v = torch.where(act, A(p), v)
-        den = dot(r0, v)
-        alpha = rho / torch.where(den == 0, one, den)
-        s = r - alpha[..., None, None] * v
-        t = A(s)
-        tt = dot(t, t).real
-        om = dot(t, s) / torch.where(tt == 0, torch.ones_like(tt), tt).to(b.dtype)
-        x = torch.where(act, x + alpha[..., None, None] * p + om[..., None, None] * s, x)
-        r = torch.where(act, s - om[..., None, None] * t, r)
-        res = torch.where(act[..., 0, 0], torch.sqrt(dot(r, r).real) / nb, res)
     rows = dev.gs_forward((chi * x).contiguous()).cpu().numpy()
     data = np.stack([awgn(rows[s], snr_db, rngs[s]) for s in range(S)])
     return data, chis

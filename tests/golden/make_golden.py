@@ -379,6 +379,34 @@ def make_metrics():
     print("counts", counts, ex_counts)
 
 
+def make_solver():
+    """Forward solves of the reference (forward.py:193-275, 335-374): BiCGStab on a 32 x 32
+    and a 64 x 64 grid, its dense-LU answer, NoConvergenceError at a small maxiter, and
+    simulate() on a 64 x 64 grid (line sources, noise-free)."""
+    from pdfisp.forward import NoConvergenceError
+    out = {}
+    for m in (32, 64):
+        cfg = ImagingConfig(m1=m, m2=m, m_f=3, n_tx=8, n_rx=8).validate()
+        grid, arr = build_grid(cfg), build_array(cfg)
+        ops = build_greens(cfg, arr, grid)
+        einc = incident_fields(cfg, arr, grid)
+        chi = rasterize(builtin_scene("austria", 3.0, scale=0.9), grid)
+        fs = solve_total_field(chi, einc, ops, method="fft")
+        out[f"x{m}"], out[f"res{m}"] = fs.views, fs.residuals
+        if m == 32:
+            out["x32_dense"] = solve_total_field(chi, einc, ops, method="dense").views
+        try:
+            solve_total_field(chi, einc, ops, maxiter=3, method="fft")
+            raise SystemExit("expected NoConvergenceError")
+        except NoConvergenceError as ex:
+            out[f"noconv_msg{m}"] = np.array(str(ex))
+    cfg = ImagingConfig(m1=64, m2=64, m_f=3, n_tx=8, n_rx=8).validate()
+    sim = simulate(cfg, builtin_scene("austria", 3.0, scale=0.9))
+    out["sim64_data"] = sim.data.matrix
+    save("solver", **out)
+    print({k: v for k, v in out.items() if "msg" in k})
+
+
 def make_cfg4more():
     """Eight more config-4 scenes (indices 2-9), 500 iterations each."""
     make_cfg4(n_scenes=8, first=2)

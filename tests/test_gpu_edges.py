@@ -54,7 +54,8 @@ def test_pole_raises_through_the_loss(tiny_setup, g_edges):
     # the error word is cleared by the read: a nearby regular point evaluates normally
     g, bd = grad_alpha(g_edges["alpha_near"], ctx)
     assert rel(g, g_edges["g_near"]) < 1e-10
-    np.testing.assert_allclose(bd.as_row(), g_edges["bd_near"], rtol=1e-10)
+    # the state residual cancels to ~1e-14 near the pole: absolute tolerance on that term
+    np.testing.assert_allclose(bd.as_row(), g_edges["bd_near"], rtol=1e-10, atol=1e-20)
 
 
 def test_pole_raises_after_training_graph(tiny_setup, g_edges):
