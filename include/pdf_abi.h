@@ -24,6 +24,10 @@
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
  *   pdf_shard_step_a/b/c  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
  *                       (views split over ranks, caller all-reduces between the steps)
+ *   pdf_bessel          bessel_j0/j1/y0/y1, hankel1_*   special.py:64-106
+ *   pdf_build_greens    build_greens                    forward.py:101-137
+ *   pdf_incident_fields incident_fields (line sources)  forward.py:174-181
+ *                       (+ plane waves)
  *   pdf_solve_total_field _solve_bicgstab /            forward.py:193-248,
  *                       solve_total_field               forward.py:251-275
  *   pdf_relative_error  relative_error                  reconstruct.py:243-247
@@ -72,7 +76,8 @@ enum pdf_status {
   PDF_EINVAL = -1,      /* bad argument / unsupported shape */
   PDF_ECUDA = -2,       /* CUDA runtime error */
   PDF_ENOMEM = -3,      /* workspace too small */
-  PDF_ENOCONV = -4      /* NoConvergenceError: an iterative solve stopped at maxiter */
+  PDF_ENOCONV = -4,     /* NoConvergenceError: an iterative solve stopped at maxiter */
+  PDF_EGEOMETRY = -5    /* GeometryError: an antenna inside the grid / on a cell centre */
 };
 
 typedef struct pdf_ctx pdf_ctx;
@@ -175,6 +180,25 @@ int pdf_shard_step_a(pdf_ctx* ctx, const void* theta, double* red1, void* stream
 int pdf_shard_step_b(pdf_ctx* ctx, const double* red1, double* red2, void* chi_out, void* stream);
 int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* grad, double* breakdown,
                      void* stream);
+
+/* one-time operator construction on the device (context-free, float64 / complex128, device arrays).
+ *   pdf_bessel           j[k] = J_order(x[k]), y[k] = Y_order(x[k]) (order 0 or 1; either output may be
+ *                        NULL); J even / odd in x, Y = NaN for x < 0, -inf at 0
+ *   pdf_build_greens     gd_kernel [2 m1][2 m2] (wrap-indexed displacement kernel), gd_kernel_hat = its
+ *                        unnormalised fft2, gs_matrix [R][m1 m2] (NULL = skip), *gd_diag_host (2 doubles,
+ *                        may be NULL) = the self term; xs [m2] / ys [m1] cell-centre coordinates, rx [R][2]
+ *                        receiver positions; m1, m2 powers of two <= 512; synchronises `stream`;
+ *                        PDF_EGEOMETRY if a receiver lies inside the pixel grid
+ *   pdf_incident_fields  out [n][m1][m2]: kind 0 = unit line sources (i/4) H0(k0 |r - src_v|) with
+ *                        src [n][2] positions (PDF_EGEOMETRY if one coincides with a cell centre),
+ *                        kind 1 = plane waves exp(i k0 (x cos src_v + y sin src_v)) with src [n] angles;
+ *                        synchronises `stream` */
+int pdf_bessel(int32_t order, const double* x, double* j, double* y, int64_t count, void* stream);
+int pdf_build_greens(double k0, double cell_size, int32_t m1, int32_t m2, const double* xs, const double* ys,
+                     const double* rx, int32_t R, void* gd_kernel, void* gd_kernel_hat, void* gs_matrix,
+                     double* gd_diag_host, void* stream);
+int pdf_incident_fields(int32_t kind, double k0, int32_t m1, int32_t m2, const double* xs, const double* ys,
+                        const double* src, int32_t n, void* out, void* stream);
 
 /* forward solve (method of moments): (I - G_D chi) x = b for the n views of
  * S scenes by batched BiCGStab with the reference's restart clause, on the context's G_D (the context

@@ -499,14 +499,21 @@ class BatchReconstructor:
 
     def __init__(self, config: ImagingConfig, S: int, e_inc: np.ndarray | None = None,
                  array: AntennaArray | None = None, mask=None, dtype: str = "f64", use_graph: bool = True,
-                 theta_cache: bool = True):
+                 theta_cache: bool = True, device_ops: bool = True):
         config.validate()
         check_config_supported(config)
         self.config = config
         self.array = build_array(config) if array is None else array
         self.grid = build_grid(config)
-        self.ops = build_greens(config, self.array, self.grid)
-        self.e_inc = incident_fields(config, self.array, self.grid).views if e_inc is None else np.asarray(e_inc)
+        if device_ops:
+            # operators and incident fields built in HBM by the library (greens.py)
+            from .greens import build_greens_device, incident_fields_device
+            self.ops = build_greens_device(config, self.array, self.grid)
+            self.e_inc = (incident_fields_device(config, self.array, self.grid, "line") if e_inc is None
+                          else np.asarray(e_inc))
+        else:
+            self.ops = build_greens(config, self.array, self.grid)
+            self.e_inc = incident_fields(config, self.array, self.grid).views if e_inc is None else np.asarray(e_inc)
         self.basis = SpectralBasis(config.m1, config.m2, config.m_f)
         self.S = S
         self.use_graph = use_graph

@@ -30,7 +30,11 @@ MAX_VIEWS = 80
 MAX_RECEIVERS = 80
 
 
-def check_supported(ops, e_inc: np.ndarray, data: np.ndarray, mf: int, joint: bool = False) -> None:
+def _shape(x) -> tuple:
+    return tuple(x.shape) if hasattr(x, "shape") else tuple(np.shape(x))
+
+
+def check_supported(ops, e_inc, data: np.ndarray, mf: int, joint: bool = False) -> None:
     """Reject, before any pointer reaches the C ABI, the problems the sm_100a
     kernels do not cover ('Supported shapes'): the grid
     must be square with a power-of-two edge in [16, 256], at most 80
@@ -47,11 +51,11 @@ def check_supported(ops, e_inc: np.ndarray, data: np.ndarray, mf: int, joint: bo
         raise ValueError(f"unsupported grid {M}x{M}: the edge must be one of {GRID_SIZES}")
     if (ops.m1, ops.m2) != (M, M):
         raise ValueError(f"operators were built for a {ops.m1}x{ops.m2} grid, e_inc is {M}x{M}")
-    if tuple(np.shape(ops.gd_kernel_hat)) != (2 * M, 2 * M):
-        raise ValueError(f"gd_kernel_hat must be ({2 * M}, {2 * M}), got {np.shape(ops.gd_kernel_hat)}")
+    if _shape(ops.gd_kernel_hat) != (2 * M, 2 * M):
+        raise ValueError(f"gd_kernel_hat must be ({2 * M}, {2 * M}), got {_shape(ops.gd_kernel_hat)}")
     S, n, R = data.shape
-    if tuple(np.shape(ops.gs_matrix)) != (R, M * M):
-        raise ValueError(f"gs_matrix must be ({R}, {M * M}) for {R} receivers, got {np.shape(ops.gs_matrix)}")
+    if _shape(ops.gs_matrix) != (R, M * M):
+        raise ValueError(f"gs_matrix must be ({R}, {M * M}) for {R} receivers, got {_shape(ops.gs_matrix)}")
     if e_inc.shape[-3] != n:
         raise ValueError(f"e_inc has {e_inc.shape[-3]} views, the data {n}")
     if e_inc.ndim == 4 and e_inc.shape[0] != S:
@@ -91,7 +95,8 @@ class DeviceProblem:
         if data.ndim == 2:
             data = data[None]
         S, n, R = data.shape
-        e_inc = np.asarray(e_inc)
+        if not isinstance(e_inc, torch.Tensor):      # host array, or a device tensor (greens.py)
+            e_inc = np.asarray(e_inc)
         shared = e_inc.ndim == 3
         M = e_inc.shape[-1]
         check_supported(ops, e_inc, data, mf, joint)    # before any device work
@@ -123,7 +128,10 @@ class DeviceProblem:
         # normalisers in float64 on the host, exactly as losses.py:67-76
         dm = data if mask is None else data * np.broadcast_to(np.asarray(mask, dtype=float), data.shape)
         self.c_sca = np.array([float(np.vdot(dm[s], dm[s]).real) for s in range(S)])
-        if shared:
+        if isinstance(e_inc, torch.Tensor):
+            p2 = (self.e_inc.conj() * self.e_inc).real
+            self.c_inc = np.full(S, float(p2.sum())) if shared else p2.reshape(S, -1).sum(-1).cpu().numpy()
+        elif shared:
             ci = float(np.vdot(e_inc, e_inc).real)
             self.c_inc = np.full(S, ci)
         else:

@@ -407,6 +407,41 @@ def make_solver():
     print({k: v for k, v in out.items() if "msg" in k})
 
 
+def make_special():
+    """The reference's cylinder functions (special.py:64-106) on a grid spanning both regions."""
+    from pdfisp import special as sp
+    rng = np.random.default_rng(17)
+    x = np.concatenate([np.linspace(1e-4, 60.0, 2401), rng.uniform(0.0, 300.0, 600), [8.0, 17.0, 0.5, 1e-6]])
+    save("special", x=x, j0=sp.bessel_j0(x), j1=sp.bessel_j1(x), y0=sp.bessel_y0(x), y1=sp.bessel_y1(x),
+         xneg=-x[:50], j0neg=sp.bessel_j0(-x[:50]), j1neg=sp.bessel_j1(-x[:50]))
+
+
+def cfg4_sensitivity(idx: int, k: int = 500, eps=(1e-15, -1e-15)):
+    """The reference's own rounding sensitivity on config-4 scene idx: its final relative
+    error after k iterations when the measured data are scaled by (1 + eps), eps ~ 1 ulp.
+    The loss passes a chaotic transient in its first iterations, so scenes whose reference
+    output moves by ~1e-3 under 1e-15 input changes cannot be reproduced closer than that
+    by any other summation order."""
+    cfg = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
+                        k_iters=k, rng_seed=idx).validate()
+    scene, rng = cfg4_scene(idx)
+    grid, arr, ops, views, chi, data = plane_problem(cfg, scene, 20 * np.log10(100 / 5), rng)
+    out = []
+    for e in eps:
+        d2 = ScatteredData(matrix=data.matrix * (1.0 + e))
+        out.append(composed_reconstruct(cfg, d2, views, ops, chi, k)["rel_error"])
+    return np.array(out)
+
+
+def make_cfg4sens():
+    """Per-scene sensitivity records for config-4 scenes given in $SCENES (default 0-9)."""
+    scenes = [int(x) for x in os.environ.get("SCENES", "0,1,2,3,4,5,6,7,8,9").split(",")]
+    for idx in scenes:
+        rel = cfg4_sensitivity(idx)
+        save(f"cfg4_sens_s{idx}", rel_perturbed=rel, eps=np.array([1e-15, -1e-15]))
+        print(f"cfg4 scene {idx}: perturbed rel_error {rel}", flush=True)
+
+
 def make_cfg4more():
     """Eight more config-4 scenes (indices 2-9), 500 iterations each."""
     make_cfg4(n_scenes=8, first=2)
