@@ -442,6 +442,21 @@ def make_cfg4sens():
         print(f"cfg4 scene {idx}: perturbed rel_error {rel}", flush=True)
 
 
+def make_files():
+    """.emsca / .grid files written by the reference (fileio.py:98-145)."""
+    from pdfisp.fileio import save_dataset, save_grid
+    from pdfisp.geometry import ComplexGrid
+    rng = np.random.default_rng(31)
+    mat = rng.standard_normal((8, 12)) + 1j * rng.standard_normal((8, 12))
+    mask = rng.random((8, 12)) > 0.25
+    save_dataset(os.path.join(HERE, "ref_masked.emsca"), ScatteredData(matrix=mat * mask, snr_db=26.02, mask=mask),
+                 meta={"scene": "random", "seed": 31})
+    save_dataset(os.path.join(HERE, "ref_plain.emsca"), ScatteredData(matrix=mat))
+    img = rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))
+    save_grid(os.path.join(HERE, "ref.grid"), ComplexGrid(values=img, cell_size=0.09375), config_hash="abc123")
+    save("files", mat=mat, mask=mask, img=img)
+
+
 def make_cfg4more():
     """Eight more config-4 scenes (indices 2-9), 500 iterations each."""
     make_cfg4(n_scenes=8, first=2)
