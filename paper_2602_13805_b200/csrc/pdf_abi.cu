@@ -977,10 +977,13 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
     CK_CUDA(cudaEventRecord(c->ev_vf, st));
     CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));
     g_pdl_off = 1;
+    const int tl_keep = g_tl_cur;
+    g_tl_cur = 0;          // side-branch kernels carry no timeline slot (the slots time the main chain)
     const int rd = data_term<T>(c, c->alpha_hat, c->side);
     if (rd == PDF_OK)
       gad_kernel<T><<<dim3((c->M0 + 255) / 256, c->d.S * c->d.n), 256, 0, c->side>>>(
           (const C<T>*)c->grows, (const C<T>*)c->hs, (C<T>*)c->gad, c->d.R, c->M0);
+    g_tl_cur = tl_keep;
     g_pdl_off = 0;
     TRY(rd);
     CK_CUDA(cudaGetLastError());
@@ -996,6 +999,7 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
     CK_CUDA(cudaEventRecord(c->ev_vf, st));
     CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));
     g_pdl_off = 1;
+    // (gad_kernel carries no timeline slot argument)
     gad_kernel<T><<<dim3((c->M0 + 255) / 256, c->d.S * c->d.n), 256, 0, c->side>>>(
         (const C<T>*)c->grows, (const C<T>*)c->hs, (C<T>*)c->gad, c->d.R, c->M0);
     g_pdl_off = 0;
@@ -1035,10 +1039,13 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
         if (run()) TRY(adam_x_all(c, (double*)theta, (double*)m, (double*)v, st, 1, c->tsnap));
         CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_g3, 0));
         g_pdl_off = 1;
+        const int tl_keep = g_tl_cur;
+        g_tl_cur = 0;
         int r1 = run() ? adam_x_all(c, (double*)theta, (double*)m, (double*)v, c->side, 4, c->tsnap) : PDF_OK;
         cudaError_t e1 = cudaStreamWaitEvent(c->side, c->ev_g2, 0);
         int r2 = run() && r1 == PDF_OK ? adam_x_all(c, (double*)theta, (double*)m, (double*)v, c->side, 2, c->tsnap)
                                        : PDF_OK;
+        g_tl_cur = tl_keep;
         g_pdl_off = 0;
         TRY(r1);
         TRY(r2);
