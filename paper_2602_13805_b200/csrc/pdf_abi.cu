@@ -340,6 +340,7 @@ static VLArgs<T> vl_common(pdf_ctx* c) {
   a.M = c->M; a.mf = c->d.mf; a.R = c->d.R; a.n = c->d.n; a.NPV = c->NPV;
   a.khat = (const C<T>*)c->khat; a.twP = (const C<T>*)c->twP; a.twM = (const C<T>*)c->twM;
   a.spec = (C<T>*)c->spec;
+  a.tl = g_tl_cur;
   return a;
 }
 
@@ -385,6 +386,7 @@ static int data_term(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   g.data = (const C<T>*)c->d.data; g.mask = (const T*)c->d.mask; g.c_sca = c->c_sca;
   g.grows = (C<T>*)c->grows; g.dloss = c->dloss;
   g.nq = c->dg_nq;
+  g.tl = g_tl_cur;
   void* args[] = {&g};
   cudaError_t e;
   if constexpr (sizeof(T) == 8)

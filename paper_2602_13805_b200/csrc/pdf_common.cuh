@@ -110,6 +110,11 @@ __device__ __forceinline__ void tl_mark(int slot1, int k) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   if (k < 2) atomicMin(&g_tl[slot1 - 1][k], t); else atomicMax(&g_tl[slot1 - 1][2], t);
 }
+// exit stamp on every return path of a kernel (measurement timeline)
+struct TlExit {
+  int slot1;
+  __device__ __forceinline__ ~TlExit() { tl_mark(slot1, 2); }
+};
 // stage stamps inside a kernel: the last CTA to reach stage k (measurement)
 constexpr int TL_STAGES = 8;
 __device__ unsigned long long g_tls[TL_SLOTS][TL_STAGES];

@@ -733,7 +733,8 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
       const bool ok = r < rows && kk < K;
       cp_async16(hS + r * HP + 2 * sg, ok ? hin + (size_t)r * K + kk : hin, ok);
     }
-    if (L.wait) { pdl_wait(); tl_mark(a.tl, 1); }
+    if (L.wait) pdl_wait();
+    tl_mark(a.tl, 1);   // first dependent work (CTAs of layers whose g_z is old do not wait)
     for (int i = tid; i < RPM * AX_NB / 2; i += blockDim.x) {
       const int r = i / (AX_NB / 2), sg = i % (AX_NB / 2), nn = nb * AX_NB + 2 * sg;
       const bool ok = r < rows && nn < N;
@@ -773,7 +774,8 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
     const int bn = (item - wc) * 256 + tid;
     const size_t o = L.b_off + (bn < N ? bn : 0);
     double p = th[o], m1 = mm[o], v1 = vv[o];
-    if (L.wait) { pdl_wait(); tl_mark(a.tl, 1); }
+    if (L.wait) pdl_wait();
+    tl_mark(a.tl, 1);   // first dependent work (CTAs of layers whose g_z is old do not wait)
     __syncthreads();
     if (bn < N) {
       double gb = 0.0;

@@ -63,6 +63,7 @@ struct VLArgs {
   const C<T>* hs;              // [R][M0] spectral receiver operator (pdf_aux.cuh)
   FinalizeArgs fin;
   int do_fin;
+  int tl;                      // timeline slot + 1 (0: off)
 };
 
 template <typename T>
@@ -87,6 +88,8 @@ __host__ __device__ inline size_t vl_out_smem(int E, int mf) {
 // ---------------------------------------------------------------------------
 template <typename T, int E, int MODE>
 __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   constexpr int P = 32 * E, M = P / 2, KH = E / 2, TP = VL_ROWS + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mf = a.mf, K = 2 * mf, M0 = K * K;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   LaneTw<T, (SPLIT ? E / 2 : 1)> ltwh;
   if constexpr (SPLIT) ltwh.load(twh, lane); else ltw.load(tw, lane);
   pdl_wait();
+  tl_mark(a.tl, 1);
 
   C<T> x[E];
 #pragma unroll
@@ -206,6 +210,8 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
 // ---------------------------------------------------------------------------
 template <typename T, int E>
 __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   constexpr int P = 32 * E, M = P / 2, KH = E / 2;
   constexpr bool SPLIT = E >= 4;
   constexpr int EH = E / 2;
@@ -222,6 +228,7 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
     LaneTw<T, E / 2> lt;
     lt.load(twh, lane);
     pdl_wait();
+  tl_mark(a.tl, 1);
     C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
     C<T> xin[EH], r[EH], t[EH];
 #pragma unroll
@@ -248,6 +255,7 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
   LaneTw<T, E> ltw;
   ltw.load(tw, lane);
   pdl_wait();
+  tl_mark(a.tl, 1);
   C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
   C<T> x[E];
 #pragma unroll
@@ -264,6 +272,8 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
 // ---------------------------------------------------------------------------
 template <typename T, int E, int MODE>
 __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   constexpr int P = 32 * E, M = P / 2, KH = E / 2, SP = P + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mf = a.mf, K = 2 * mf, M0 = K * K;
@@ -283,6 +293,7 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   for (int i = tid; i < P / 2; i += blockDim.x) twh[i] = a.twP[2 * i];
   for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
   pdl_wait();
+  tl_mark(a.tl, 1);
   const C<T>* in = a.spec + (size_t)vr * P * M + y0;
   for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
     const int pos = i / VL_ROWS, yl = i % VL_ROWS;
@@ -381,10 +392,13 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
 // the loss breakdown (losses.py:36-49)
 template <typename T>
 __global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   __shared__ double red[4][4];
   const int M = a.M, mf = a.mf, K = 2 * mf, M0 = K * K;
   const int v = blockIdx.y, scene = v / a.n, view = v % a.n;
   pdl_wait();
+  tl_mark(a.tl, 1);
   if (a.do_fin && view == 0 && blockIdx.x == 0) finalize_block(a.fin, scene, red);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= M0) return;
@@ -422,6 +436,7 @@ struct DataArgs {
   const double* c_sca;
   C<T>* grows;
   double* dloss;
+  int tl;               // timeline slot + 1 (0: off)
 };
 
 constexpr int DG_KC = 32;          // pixels per staged sub-tile
@@ -442,6 +457,8 @@ __host__ __device__ inline size_t dg_smem(int n, int R) {
 // with cp.async.
 template <typename T>
 __global__ void __launch_bounds__(512) data_gemm_kernel(DataArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   constexpr int EPC = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;   // complex per 16 B
   constexpr int PT = DG_KC + EPC;                                         // padded pitch
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -477,6 +494,7 @@ __global__ void __launch_bounds__(512) data_gemm_kernel(DataArgs<T> a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = czero<T>();
   pdl_wait();
+  tl_mark(a.tl, 1);
   stage(p0, 0);
   int s = 0;
   for (int k0 = p0; k0 < p1; k0 += DG_KC, s ^= 1) {
@@ -538,6 +556,8 @@ __host__ __device__ inline size_t dm_smem(int n, int R, int nq) {
 
 
 __global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = a.n, R = a.R, npix = a.npix, NQ = a.nq;
   const int MTs = (n + 7) / 8, RGs = (R + 8 * DM_NTL - 1) / (8 * DM_NTL), NTP = MTs * RGs;
@@ -550,6 +570,7 @@ __global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
   const double2* J = reinterpret_cast<const double2*>(a.J) + (size_t)scene * n * npix;
   const double2* G = reinterpret_cast<const double2*>(a.gs);
   pdl_wait();
+  tl_mark(a.tl, 1);
   for (int item = warp; item < NTP * NQ; item += 8) {
     const int tp = item % NTP, q = item / NTP, mt = tp / RGs, rg = tp % RGs;
     const int v = 8 * mt + g;
@@ -610,9 +631,12 @@ __global__ void __launch_bounds__(256) data_mma_kernel(DataArgs<double> a) {
 // D = sum of chunk partials - d (masked), g_rows = 2 D mask / c_sca, ||D||^2 per view
 template <typename T>
 __global__ void __launch_bounds__(128) data_reduce_kernel(DataArgs<T> a) {
+  tl_mark(a.tl, 0);
+  TlExit tl_exit_{a.tl};
   __shared__ double red[4];
   const int v = blockIdx.x, scene = v / a.n, i = v % a.n, R = a.R;
   pdl_wait();
+  tl_mark(a.tl, 1);
   double part = 0.0;
   const double csca = a.c_sca[scene];
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
