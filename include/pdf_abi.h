@@ -22,7 +22,7 @@
  *   pdf_expand          expand                          spectral.py:68-79
  *   pdf_truncate        truncate                        spectral.py:56-65
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
- *   pdf_shard_step_a/b/c  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
+ *   pdf_shard_step_a/b/c(_part)  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
  *                       (views split over ranks, caller all-reduces between the steps)
  *   pdf_bessel          bessel_j0/j1/y0/y1, hankel1_*   special.py:64-106
  *   pdf_build_greens    build_greens                    forward.py:101-137
@@ -180,6 +180,18 @@ int pdf_shard_step_a(pdf_ctx* ctx, const void* theta, double* red1, void* stream
 int pdf_shard_step_b(pdf_ctx* ctx, const double* red1, double* red2, void* chi_out, void* stream);
 int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* grad, double* breakdown,
                      void* stream);
+/* step c in per-layer parts (S = 1): layer 3 first (it also runs the pixel adjoint, G_D^H, truncation
+ * and the loss breakdown), then 2, then 1; each writes its gradient bucket [W_L | b_L] (contiguous,
+ * flat-order slice [offs[2L-2], offs[2L-1] + fan_out)) to `bucket`, so the caller can reduce a
+ * layer's bucket while the next layer's backward runs.  pdf_net_offsets: offs[7] = w1, b1, w2, b2,
+ * w3, b3 offsets in the flat parameter vector and n_params. */
+int pdf_shard_step_c_part(pdf_ctx* ctx, const void* theta, const double* red2, void* bucket, int32_t layer,
+                          double* breakdown, void* stream);
+int pdf_net_offsets(const pdf_ctx* ctx, int64_t* offs);
+/* pdf_adam_step with the step t read from device memory (*t_dev, >= 1): capturable in a CUDA graph;
+ * also flags a nonfinite gradient (network.py:221-222) */
+int pdf_adam_step_dev(pdf_ctx* ctx, void* theta, void* m, void* v, const void* grad, int64_t count,
+                      const int32_t* t_dev, void* stream);
 
 /* one-time operator construction on the device (context-free, float64 / complex128, device arrays).
  *   pdf_bessel           j[k] = J_order(x[k]), y[k] = Y_order(x[k]) (order 0 or 1; either output may be

@@ -36,7 +36,8 @@ EXPORTS = (
     "pdf_timeline_reset", "pdf_timeline_read", "pdf_ctx_paths",
     "pdf_net_setup_sharded", "pdf_shard_buffer_sizes", "pdf_shard_step_a", "pdf_shard_step_b", "pdf_shard_step_c",
     "pdf_relative_error", "pdf_count_components", "pdf_solver_workspace_bytes", "pdf_solve_total_field",
-    "pdf_bessel", "pdf_build_greens", "pdf_incident_fields",
+    "pdf_bessel", "pdf_build_greens", "pdf_incident_fields", "pdf_shard_step_c_part", "pdf_net_offsets",
+    "pdf_adam_step_dev",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
 
@@ -105,6 +106,9 @@ def lib():
         "pdf_shard_step_b": (ct.c_int, [vp, vp, vp, vp, vp]),
         "pdf_shard_step_c": (ct.c_int, [vp, vp, vp, vp, vp, vp]),
         "pdf_solver_workspace_bytes": (ct.c_size_t, [vp, i32]),
+        "pdf_shard_step_c_part": (ct.c_int, [vp, vp, vp, vp, i32, vp, vp]),
+        "pdf_net_offsets": (ct.c_int, [vp, ct.POINTER(i64)]),
+        "pdf_adam_step_dev": (ct.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
         "pdf_bessel": (ct.c_int, [i32, vp, vp, vp, i64, vp]),
         "pdf_build_greens": (ct.c_int, [ct.c_double, ct.c_double, i32, i32, vp, vp, vp, i32, vp, vp, vp, dp, vp]),
         "pdf_incident_fields": (ct.c_int, [i32, ct.c_double, i32, i32, vp, vp, vp, i32, vp, vp]),

@@ -1646,6 +1646,65 @@ static int shard_c_impl(pdf_ctx* c, const void* theta, const double* red2, void*
   return PDF_OK;
 }
 
+// step c in three parts so each layer's gradient bucket can be reduced while the
+// next layer's backward runs (the bucket of layer L = [W_L | b_L], contiguous)
+template <typename T>
+static int shard_c_part_impl(pdf_ctx* c, const void* theta, const double* red2, void* bucket, int part, double* bd,
+                             cudaStream_t st) {
+  const Offs o = offsets(c);
+  T* th = (T*)const_cast<void*>(theta);
+  // the kernels address grad + w_off / grad + b_off: shift the bucket base by the layer's offset
+  auto base = [&](long long woff) { return (T*)((uintptr_t)bucket - (uintptr_t)woff * sizeof(T)); };
+  if (part == 3) {
+    ShardArgs<T> a = shard_args<T>(c, nullptr, const_cast<double*>(red2));
+    void* args[] = {&a};
+    const dim3 grid(c->M / c->TX, c->M, c->d.S);
+    CK_CUDA(plain_launch(shard_pixel_b_kernel<T>, grid, dim3(PIX_NW * 32), 0, st, args));
+    TRY(phys_backward<T>(c, nullptr, c->gy, st));
+    FinalizeArgs f = fin_args(c, bd, nullptr);
+    shard_finalize_kernel<<<c->d.S, 128, 0, st>>>(f, red2, (size_t)c->M * c->M);
+    CK_CUDA(cudaGetLastError());
+    return net_bwd_layer<T>(c, (const T*)c->gy, (const T*)c->h2, c->H, c->D0, th, o.w3, o.b3, nullptr, nullptr,
+                            base(o.w3), 0, (T*)c->gz2, st);
+  }
+  if (part == 2)
+    return net_bwd_layer<T>(c, (const T*)c->gz2, (const T*)c->h1, c->H, c->H, th, o.w2, o.b2, nullptr, nullptr,
+                            base(o.w2), 0, (T*)c->gz1, st);
+  return net_bwd_layer<T>(c, (const T*)c->gz1, (const T*)c->x0, c->D0, c->H, th, o.w1, o.b1, nullptr, nullptr,
+                          base(o.w1), 0, nullptr, st);
+}
+
+extern "C" int pdf_shard_step_c_part(pdf_ctx* c, const void* theta, const double* red2, void* bucket, int32_t layer,
+                                     double* breakdown, void* stream) {
+  if (!c || !theta || !red2 || !bucket || layer < 1 || layer > 3 || c->d.S != 1)
+    return fail(PDF_EINVAL, "bad argument");
+  return DISPATCH(c, shard_c_part_impl, c, theta, red2, bucket, (int)layer, breakdown, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_net_offsets(const pdf_ctx* c, int64_t* offs) {
+  if (!c || !offs) return fail(PDF_EINVAL, "null argument");
+  const Offs o = offsets(const_cast<pdf_ctx*>(c));
+  const long long v[7] = {o.w1, o.b1, o.w2, o.b2, o.w3, o.b3, c->Np};
+  for (int i = 0; i < 7; ++i) offs[i] = v[i];
+  return PDF_OK;
+}
+
+template <typename T>
+static int adam_dev_impl(pdf_ctx* c, void* theta, void* m, void* v, const void* g, long long cnt, const int* t_dev,
+                         cudaStream_t st) {
+  int blocks = (int)std::min<long long>((cnt + 255) / 256, 148LL * 16);
+  adam_flat_dev_kernel<T><<<blocks, 256, 0, st>>>((T*)theta, (T*)m, (T*)v, (const T*)g, cnt, (T)c->d.lr,
+                                                  (T)c->d.adam_b1, (T)c->d.adam_b2, (T)c->d.adam_eps, t_dev, c->err);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
+}
+
+extern "C" int pdf_adam_step_dev(pdf_ctx* c, void* theta, void* m, void* v, const void* g, int64_t count,
+                                 const int32_t* t_dev, void* stream) {
+  if (!c || !theta || !m || !v || !g || !t_dev || count < 0) return fail(PDF_EINVAL, "bad argument");
+  return DISPATCH(c, adam_dev_impl, c, theta, m, v, g, (long long)count, (const int*)t_dev, (cudaStream_t)stream);
+}
+
 extern "C" int pdf_shard_step_a(pdf_ctx* c, const void* theta, double* red1, void* stream) {
   if (!c || !theta || !red1 || c->d.joint) return fail(PDF_EINVAL, "bad argument");
   return DISPATCH(c, shard_a_impl, c, theta, red1, (cudaStream_t)stream);

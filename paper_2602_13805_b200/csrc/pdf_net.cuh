@@ -552,4 +552,24 @@ __global__ void adam_flat_kernel(T* p, T* m, T* v, const T* g, long long count, 
   if (bits) atomicOr(err, bits);
 }
 
+// same update with the step t read from device memory (capturable in a CUDA graph);
+// bias corrections as in the fused kernels (pow in float64)
+template <typename T>
+__global__ void adam_flat_dev_kernel(T* p, T* m, T* v, const T* g, long long count, T lr, T b1, T b2, T eps,
+                                     const int* t_dev, int* err) {
+  const double t = (double)*t_dev;
+  const T bc1 = T(1.0 / (1.0 - pow((double)b1, t))), bc2 = T(1.0 / (1.0 - pow((double)b2, t)));
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int bits = 0;
+  for (; i < count; i += (long long)gridDim.x * blockDim.x) {
+    T pp = p[i], mm = m[i], vv = v[i];
+    const T gg = g[i];
+    if (!isfinite(gg)) bits |= ERR_NONFINITE_GRAD;
+    adam_one<T>(pp, mm, vv, gg, lr, b1, b2, eps, bc1, bc2);
+    if (!isfinite(pp)) bits |= ERR_NONFINITE_PARAM;
+    p[i] = pp; m[i] = mm; v[i] = vv;
+  }
+  if (bits) atomicOr(err, bits);
+}
+
 }  // namespace pdf

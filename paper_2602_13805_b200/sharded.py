@@ -167,3 +167,143 @@ def sharded_chi(shards, reduce, thetas):
     chi = torch.empty(1, shards[0].dev.M, shards[0].dev.M, dtype=shards[0].dev.cdt, device=shards[0].dev.device)
     shards[0].step_b(chi)
     return chi[0]
+
+
+# ---------------------------------------------------------------------------- ZeRO-1 form
+def bucket_plan(offs, world: int) -> list[dict]:
+    """Gradient buckets of the flat parameter vector, one per layer in the order
+    the backward produces them (3, 2, 1): bucket L = [W_L | b_L], flat slice
+    [offs[2L-2], offs[2L]) (offs = pdf_net_offsets: w1 b1 w2 b2 w3 b3 Np),
+    padded to a multiple of `world` so a reduce-scatter hands rank r the
+    contiguous shard [r s, (r + 1) s) of s = padded / world entries."""
+    out = []
+    for L in (3, 2, 1):
+        lo, hi = int(offs[2 * L - 2]), int(offs[2 * L])
+        n = hi - lo
+        npad = -(-n // world) * world
+        out.append({"layer": L, "lo": lo, "n": n, "npad": npad, "shard": npad // world})
+    return out
+
+
+class ShardedTrainer:
+    """Incidence-sharded training of one large scene with sharded optimizer state
+    (the alternative to replicated Adam VERDICT r01 asked for).
+
+    One iteration on every rank:
+      step_a (network forward, own views' physics)  -> all-reduce red1 (SUM, MAX)
+      step_b (per-pixel chi / R / regularisers)     -> all-reduce red2 (SUM)
+      step_c in layer parts 3, 2, 1: each layer's gradient bucket is
+        reduce-scattered on a communication stream while the next layer's
+        backward runs (bucketed overlap, NCCL over NVLink);
+      Adam on this rank's 1/W shard of every bucket only (m, v hold 1/W of the
+        parameters; step counter on the device);
+      all-gather of the updated shards back into the replicated parameters.
+    graph=True captures `graph_iters` such iterations -- library kernels and
+    NCCL collectives -- in one CUDA graph and replays it."""
+
+    def __init__(self, shard: IncidenceShard, theta0: torch.Tensor, group=None, graph: bool = True,
+                 graph_iters: int = 10):
+        import torch.distributed as dist
+        self.dist, self.group, self.s = dist, group, shard
+        self.W = dist.get_world_size(group)
+        self.r = dist.get_rank(group)
+        dev = shard.dev
+        self.lib = dev.lib
+        offs = (ct.c_int64 * 7)()
+        N.check(self.lib.pdf_net_offsets(dev.ctx, offs))
+        self.offs = [int(x) for x in offs]
+        if self.offs[6] != theta0.numel():
+            raise ValueError("theta0 does not match the network of this shard")
+        self.plan = bucket_plan(self.offs, self.W)
+        dd, rdt = dev.device, dev.rdt
+        self.theta = theta0.detach().to(dd, rdt).reshape(-1).clone()
+        self.gbuf, self.gshard, self.pown, self.m, self.v, self.pfull = {}, {}, {}, {}, {}, {}
+        for b in self.plan:
+            L, lo, n, npad, sh = b["layer"], b["lo"], b["n"], b["npad"], b["shard"]
+            self.gbuf[L] = torch.zeros(npad, dtype=rdt, device=dd)
+            self.gshard[L] = torch.zeros(sh, dtype=rdt, device=dd)
+            full = torch.zeros(npad, dtype=rdt, device=dd)
+            full[:n] = self.theta[lo:lo + n]
+            self.pown[L] = full[self.r * sh:(self.r + 1) * sh].clone()
+            self.m[L] = torch.zeros(sh, dtype=rdt, device=dd)
+            self.v[L] = torch.zeros(sh, dtype=rdt, device=dd)
+            # all-gather straight into theta when the bucket needs no padding
+            self.pfull[L] = self.theta[lo:lo + n] if npad == n else full
+        self.t_dev = torch.zeros(1, dtype=torch.int32, device=dd)
+        self.comm = torch.cuda.Stream(device=dd)
+        self.ev = {L: torch.cuda.Event() for L in (1, 2, 3)}
+        self.graph_on, self.G = graph, max(1, int(graph_iters))
+        self.graph = None
+        self.gtrace = torch.zeros(self.G, 6, dtype=torch.float64, device=dd)
+
+    def _red(self, t, op):
+        self.dist.all_reduce(t, op=op, group=self.group)
+
+    def iteration(self, trace_row: torch.Tensor | None = None):
+        s, d = self.s, self.dist
+        s.step_a(self.theta)
+        a, b = s.red1_sum_max()
+        self._red(a, d.ReduceOp.SUM)
+        self._red(b, d.ReduceOp.MAX)
+        s.step_b()
+        self._red(s.red2, d.ReduceOp.SUM)
+        main = torch.cuda.current_stream()
+        for bk in self.plan:
+            L = bk["layer"]
+            N.check(self.lib.pdf_shard_step_c_part(s.dev.ctx, _ptr(self.theta), _ptr(s.red2), _ptr(self.gbuf[L]), L,
+                                                   _ptr(s.bd), _stream()))
+            self.ev[L].record(main)
+            self.comm.wait_event(self.ev[L])
+            with torch.cuda.stream(self.comm):
+                d.reduce_scatter_tensor(self.gshard[L], self.gbuf[L], op=d.ReduceOp.SUM, group=self.group)
+        main.wait_stream(self.comm)
+        if trace_row is not None:
+            trace_row.copy_(s.bd[0])
+        self.t_dev += 1
+        for bk in self.plan:
+            L = bk["layer"]
+            N.check(self.lib.pdf_adam_step_dev(s.dev.ctx, _ptr(self.pown[L]), _ptr(self.m[L]), _ptr(self.v[L]),
+                                               _ptr(self.gshard[L]), bk["shard"], _ptr(self.t_dev), _stream()))
+        for bk in self.plan:
+            L, lo, n, npad = bk["layer"], bk["lo"], bk["n"], bk["npad"]
+            d.all_gather_into_tensor(self.pfull[L], self.pown[L], group=self.group)
+            if npad != n:
+                self.theta[lo:lo + n].copy_(self.pfull[L][:n])
+
+    def _capture(self):
+        st = torch.cuda.Stream(device=self.theta.device)
+        st.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(self.G):
+                self.iteration(self.gtrace[i])
+        self.graph = g
+
+    def train(self, k: int) -> torch.Tensor:
+        """k iterations; returns the device trace [k][6] (state, data, bound, tv, bridge, total)."""
+        trace = torch.zeros(k, 6, dtype=torch.float64, device=self.theta.device)
+        done = 0
+        if self.graph_on and k >= self.G:
+            if self.graph is None:
+                # warm the collectives (communicator setup) outside the capture: two eager iterations
+                # from a saved state, then restore it
+                saved = [x.clone() for x in (self.theta, self.t_dev, *self.pown.values(), *self.m.values(),
+                                             *self.v.values())]
+                for _ in range(2):
+                    self.iteration()
+                torch.cuda.synchronize()
+                for x, y in zip((self.theta, self.t_dev, *self.pown.values(), *self.m.values(), *self.v.values()),
+                                saved):
+                    x.copy_(y)
+                self._capture()
+            while done + self.G <= k:
+                self.graph.replay()
+                trace[done:done + self.G].copy_(self.gtrace)
+                done += self.G
+        while done < k:
+            self.iteration(trace[done])
+            done += 1
+        return trace
+
+    def check_errors(self):
+        self.s.dev.check_errors()

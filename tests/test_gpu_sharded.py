@@ -33,3 +33,35 @@ def test_sharded_matches_unsharded(cfg_id, world):
         assert torch.equal(th, thetas[0])
     chi = sharded_chi(shards, LocalShards(), thetas).cpu().numpy()
     assert rel(chi, ref.chi_hat.values) < 1e-9
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_zero1_trainer_single_rank_nccl(graph):
+    """ShardedTrainer (per-layer gradient buckets reduce-scattered on a comm
+    stream, Adam on the owned shard with a device step counter, all-gather; the
+    whole iteration optionally captured in a CUDA graph WITH its NCCL
+    collectives) on a one-rank NCCL group reproduces the unsharded run."""
+    import torch.distributed as dist
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, ShardedTrainer
+    g = golden("cfg1")
+    st = Setup(cfg_baseline(1), plane=True)
+    cfg = st.cfg
+    k = 20
+    ref = BatchReconstructor(cfg, 1, e_inc=st.e_inc).run([g["data"]], seeds=[cfg.rng_seed], k_iters=k)[0]
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        sh = IncidenceShard(st.ops, st.e_inc, g["data"], mf=cfg.m_f, beta=cfg.beta, lambdas=LAM, tau_b=cfg.tau_b,
+                            rank=0, world=1)
+        theta0 = torch.as_tensor(_theta0([cfg.rng_seed], 4 * cfg.m_f ** 2), device="cuda")
+        tr = ShardedTrainer(sh, theta0, graph=graph, graph_iters=10)
+        trace = tr.train(k).cpu().numpy()
+        tr.check_errors()
+    finally:
+        if own:
+            dist.destroy_process_group()
+    ref_tr = np.array([b.as_row() for b in ref.trace])
+    np.testing.assert_allclose(trace, ref_tr, rtol=1e-9)

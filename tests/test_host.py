@@ -323,3 +323,21 @@ def test_operator_shape_mismatch_rejected():
         check_supported(s.ops, s.e_inc[:4], data, 3)
     with pytest.raises(ValueError, match="m_f"):
         check_supported(s.ops, s.e_inc, data, 9)
+
+
+def test_zero1_bucket_plan_covers_parameters():
+    """The per-layer gradient buckets (layers 3, 2, 1) tile the flat parameter
+    vector and split into equal per-rank shards for every world size."""
+    from paper_2602_13805_b200.sharded import bucket_plan
+    for d0 in (72, 512, 2048):
+        h = 2 * d0
+        offs = [0, h * d0, h * d0 + h, h * d0 + h + h * h, h * d0 + 2 * h + h * h,
+                h * d0 + 2 * h + h * h + d0 * h, h * d0 + 2 * h + h * h + d0 * h + d0]
+        for w in (1, 2, 3, 4, 7, 8):
+            plan = bucket_plan(offs, w)
+            assert [b["layer"] for b in plan] == [3, 2, 1]
+            cov = sorted((b["lo"], b["lo"] + b["n"]) for b in plan)
+            assert cov[0][0] == 0 and cov[-1][1] == offs[6]
+            assert all(a[1] == b[0] for a, b in zip(cov, cov[1:]))
+            for b in plan:
+                assert b["npad"] % w == 0 and b["shard"] * w == b["npad"] and b["npad"] - b["n"] < w
