@@ -291,10 +291,14 @@ def run_reference(args, d: Dist):
 
 
 # ----------------------------------------------------------------------------- roofline
-def algorithmic_work(dev, phase: str, in_graph: bool = False):
-    """Algorithmic bytes (HBM-bound kernels) or FP64 flops per launch.
-    in_graph: the split-backward layout of the captured single-scene graph, where
-    bwd_l1 is layer 1's g_W + Adam only (layers 3 / 2 run on a side branch)."""
+def algorithmic_work(dev, phase: str, in_graph: bool = False, fp64_tflops: float = 36.2, hbm_gbs: float = 6453.4):
+    """(bound, work) per launch: algorithmic bytes of an HBM-bound kernel or FP64
+    flops of a compute-bound one.  The network layers
+    carry both (W / m / v bytes and 2 rows N K DMMA flops per product); the
+    binding one -- the larger of bytes / HBM peak and flops / FP64 peak -- is
+    reported (HBM at 16 rows, FP64 from ~40 rows on: config 5's 72 rows).
+    in_graph: the split-backward layout of the captured single-scene graph,
+    where bwd_l1 is layer 1's g_W + Adam only (layers 3 / 2 on a side branch)."""
     M, P, n, R, S = dev.M, 2 * dev.M, dev.n, dev.R, dev.S
     K = 2 * dev.mf
     rows, D0, H = dev.rows, dev.d0, dev.hidden
@@ -314,17 +318,22 @@ def algorithmic_work(dev, phase: str, in_graph: bool = False):
         return None, 0
     N_, K_ = layer
     if phase.startswith("fwd"):
-        return "hbm", S * es * (N_ * K_ + rows * K_ + rows * N_)
-    if getattr(dev, "split_bwd", False):
+        b, f = S * es * (N_ * K_ + rows * K_ + rows * N_), S * 2.0 * rows * N_ * K_
+    elif getattr(dev, "split_bwd", False):
         # split backward: bwd_l3 / bwd_l2 = g_h kernels (W_old read, g_z and h read,
         # g_z' written); bwd_l1 = g_W + Adam (W, m, v read + written)
         if phase in ("bwd_l3", "bwd_l2"):
-            return "hbm", S * es * (N_ * K_ + rows * (N_ + 2 * K_))
-        if in_graph and graph_fork(dev):
-            return "hbm", S * es * (6 * (H * D0 + H) + rows * (H + D0))
-        weights = H * D0 + H * H + D0 * H
-        return "hbm", S * es * (6 * (weights + 2 * H + D0) + rows * (2 * H + D0) * 2)
-    return "hbm", S * es * (6 * N_ * K_ + rows * (K_ + 2 * N_))
+            b, f = S * es * (N_ * K_ + rows * (N_ + 2 * K_)), S * 2.0 * rows * N_ * K_
+        elif in_graph and graph_fork(dev):
+            b, f = S * es * (6 * (H * D0 + H) + rows * (H + D0)), S * 2.0 * rows * H * D0
+        else:
+            weights = H * D0 + H * H + D0 * H
+            b, f = S * es * (6 * (weights + 2 * H + D0) + rows * (2 * H + D0) * 2), S * 2.0 * rows * weights
+    else:
+        b, f = S * es * (6 * N_ * K_ + rows * (K_ + 2 * N_)), S * 4.0 * rows * N_ * K_
+    if f / (fp64_tflops * 1e12) > b / (hbm_gbs * 1e9):
+        return "fp64", f
+    return "hbm", b
 
 
 def graph_fork(dev) -> bool:
@@ -352,7 +361,7 @@ def roofline_table(dev, phases_us: dict, period_us: float, fp64_tflops: float, h
                    in_graph: bool = True) -> dict:
     out = {}
     for p, us in phases_us.items():
-        bound, work = algorithmic_work(dev, p, in_graph)
+        bound, work = algorithmic_work(dev, p, in_graph, fp64_tflops, hbm_gbs)
         if bound is None or us <= 0:
             continue
         if bound == "hbm":

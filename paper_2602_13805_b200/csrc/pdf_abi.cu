@@ -448,19 +448,28 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   p.rfixed = c->d.freeze_r ? (const C<T>*)c->d.r_fixed : nullptr;
   p.c_inc = c->c_inc; p.gJ = (C<T>*)c->gJ; p.gE = (C<T>*)c->gE; p.part = c->part;
   p.chi_out = (C<T>*)chi_out; p.err = c->err;
-  dim3 grid(c->M / c->TX, c->M, c->d.S);
   const size_t smem = 0;
   constexpr int epc = 16 / sizeof(C<T>) > 0 ? 16 / sizeof(C<T>) : 1;
   if ((c->d.n * c->d.R) % epc) return fail(PDF_EINVAL, "n * R must be even in complex64 mode");
   void* args[] = {&p};
-  const bool ilp2 = (long long)grid.x * grid.y * grid.z <= 4 * 148;   // latency regime
-  // batches with few views: 4-warp CTAs (more CTAs per SM, smaller barrier
-  // domains; measured cfg4 4557 -> 4513 us/iter, but cfg5's 72 views slow down)
+  // latency regime (one row per CTA still leaves SMs idle): TY = 1, 8 warps;
+  // batches of <= 16 views: TY = 2 rows per CTA share the halo rows, 8 warps
+  // (cfg4 638 -> 591 us); many views (cfg5's 72): TY = 1, 4-warp CTAs
+  // (measured TY / warps: cfg4 1/4 629, 1/8 986, 2/4 681, 2/8 591 us; cfg5
+  // 1/4 142, 1/8 151, 2/4 150, 2/8 160 us; cfg2 8.2-8.9 us for all)
+  const long long rows1 = (long long)(c->M / c->TX) * c->M * c->d.S;
+  const bool batch = rows1 > 4 * 148;
+  static const int ty_env = env_int("PDF_PIX_TY", 0);
+  const int ty = ty_env == 1 || ty_env == 2 ? ty_env : (batch && c->d.n <= 16 ? 2 : 1);
   static const int pw_env = env_int("PDF_PIX_WARPS", 0);
-  const int pw = pw_env ? pw_env : (!ilp2 && c->d.n <= 16 ? 4 : PIX_NW);
-  const dim3 blk(32 * std::min(std::max(pw, 1), PIX_NW));
-  cudaError_t e = ilp2 ? plain_launch(pixel_kernel<T, GRAD, true>, grid, blk, smem, st, args)
-                       : plain_launch(pixel_kernel<T, GRAD, false>, grid, blk, smem, st, args);
+  const int pw = std::min(std::max(pw_env ? pw_env : (batch && ty == 1 ? 4 : PIX_NW), 1), PIX_NW);
+  const int vpw = (c->d.n + pw - 1) / pw;       // views per warp; the first VC stay in registers
+  const dim3 grid(c->M / c->TX, c->M / ty, c->d.S), blk(32 * pw);
+  cudaError_t e;
+  if (ty == 1) e = vpw <= 2 ? plain_launch(pixel_kernel<T, GRAD, 1, 2>, grid, blk, smem, st, args)
+                            : plain_launch(pixel_kernel<T, GRAD, 1, 4>, grid, blk, smem, st, args);
+  else e = vpw <= 2 ? plain_launch(pixel_kernel<T, GRAD, 2, 2>, grid, blk, smem, st, args)
+                    : plain_launch(pixel_kernel<T, GRAD, 2, 4>, grid, blk, smem, st, args);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("pixel kernel: ") + cudaGetErrorString(e));
   return PDF_OK;
