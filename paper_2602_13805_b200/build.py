@@ -54,6 +54,20 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    import time
+    while True:
+        t0 = time.time()
+        out = _build_once(force, verbose)
+        # a source edited while nvcc ran: its object may predate the edit -- build again
+        if all(os.path.getmtime(s) <= t0 for s in sources()):
+            return out
+        force = False
+        for cu in units():
+            if any(os.path.getmtime(s) > t0 for s in [cu] + headers()) and os.path.exists(_obj(cu)):
+                os.utime(_obj(cu), (t0 - 1, t0 - 1))
+
+
+def _build_once(force: bool, verbose: bool) -> str:
     if not force and up_to_date():
         return OUT
     os.makedirs(OBJ, exist_ok=True)
