@@ -341,3 +341,19 @@ def test_zero1_bucket_plan_covers_parameters():
             assert all(a[1] == b[0] for a, b in zip(cov, cov[1:]))
             for b in plan:
                 assert b["npad"] % w == 0 and b["shard"] * w == b["npad"] and b["npad"] - b["n"] < w
+
+
+def test_bench_spawns_its_own_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks; rank 0
+    prints the single JSON line (reference arm, gloo on this CPU-only host)."""
+    import json
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+           "--warmup", "1", "--cpu-sample-iters", "1"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["host"]["nproc"] >= 1
