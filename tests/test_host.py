@@ -357,3 +357,13 @@ def test_bench_spawns_its_own_ranks():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["host"]["nproc"] >= 1
+
+
+def test_config_hash_matches_reference():
+    """config_hash keys the reference's file headers and study cells (config.py:195-199);
+    values computed by the unmodified reference for its default config and BASELINE cfg2."""
+    from paper_2602_13805_b200.config import C0, ImagingConfig, config_hash
+    assert config_hash(ImagingConfig()) == "eefe7666ca70d135"
+    cfg2 = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
+                         k_iters=500, rng_seed=1)
+    assert config_hash(cfg2) == "f74b4a5e2a8a3f31"
