@@ -516,8 +516,13 @@ def large_leg(args, d: Dist, fp64, hbm, notes):
         try:
             trn = ShardedTrainer(sh, theta0, graph=True)
             trn.train(10)
+            torch.cuda.synchronize()
+            bad = None
         except Exception as ex:      # noqa: BLE001 -- reported in the line
-            mode = f"replicated-eager (zero1 graph failed: {type(ex).__name__}: {ex})"
+            bad = f"{type(ex).__name__}: {ex}"
+        # every rank takes the same branch (the collective sequences must match)
+        if d.max(1.0 if bad else 0.0) > 0:
+            mode = f"replicated-eager (zero1 graph failed on some rank: {bad})"
             trn = None
         torch.cuda.synchronize()
         d.barrier()
