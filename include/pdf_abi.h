@@ -188,6 +188,20 @@ int pdf_shard_step_c(pdf_ctx* ctx, const void* theta, const double* red2, void* 
 int pdf_shard_step_c_part(pdf_ctx* ctx, const void* theta, const double* red2, void* bucket, int32_t layer,
                           double* breakdown, void* stream);
 int pdf_net_offsets(const pdf_ctx* ctx, int64_t* offs);
+/* Reduce-scatter fused into the backward (float64, S = 1): like pdf_shard_step_c_part, but every
+ * g_W / g_b entry at flat parameter index f is stored, in the epilogue of the kernel that computes
+ * it, to rank o = f / shard at slot [rank][f - o shard] of that rank's receive buffer peers[o]
+ * (peers: DEVICE array of `world` pointers -- peer-mapped symmetric-memory addresses on a
+ * multi-GPU node; shard even, world * shard >= n_params).  After a cross-rank barrier,
+ * pdf_adam_gather on every rank sums its shard over the source ranks in rank order (recv =
+ * this rank's receive buffer, [world][shard]), applies Adam (m, v: [shard], step t from device
+ * memory) and writes the updated parameters into every rank's theta (thetas: DEVICE array of
+ * `world` pointers): the all-gather as peer stores. */
+int pdf_shard_step_c_scatter(pdf_ctx* ctx, const void* theta, const double* red2, double* const* peers,
+                             int32_t world, int32_t rank, int64_t shard, int32_t layer, double* breakdown,
+                             void* stream);
+int pdf_adam_gather(pdf_ctx* ctx, const double* recv, double* const* thetas, double* m, double* v, int32_t world,
+                    int32_t rank, int64_t shard, const int32_t* t_dev, void* stream);
 /* pdf_adam_step with the step t read from device memory (*t_dev, >= 1): capturable in a CUDA graph;
  * also flags a nonfinite gradient (network.py:221-222) */
 int pdf_adam_step_dev(pdf_ctx* ctx, void* theta, void* m, void* v, const void* grad, int64_t count,

@@ -37,7 +37,7 @@ EXPORTS = (
     "pdf_net_setup_sharded", "pdf_shard_buffer_sizes", "pdf_shard_step_a", "pdf_shard_step_b", "pdf_shard_step_c",
     "pdf_relative_error", "pdf_count_components", "pdf_solver_workspace_bytes", "pdf_solve_total_field",
     "pdf_bessel", "pdf_build_greens", "pdf_incident_fields", "pdf_shard_step_c_part", "pdf_net_offsets",
-    "pdf_adam_step_dev",
+    "pdf_adam_step_dev", "pdf_shard_step_c_scatter", "pdf_adam_gather",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
 
@@ -109,6 +109,8 @@ def lib():
         "pdf_shard_step_c_part": (ct.c_int, [vp, vp, vp, vp, i32, vp, vp]),
         "pdf_net_offsets": (ct.c_int, [vp, ct.POINTER(i64)]),
         "pdf_adam_step_dev": (ct.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
+        "pdf_shard_step_c_scatter": (ct.c_int, [vp, vp, vp, vp, i32, i32, i64, i32, vp, vp]),
+        "pdf_adam_gather": (ct.c_int, [vp, vp, vp, vp, vp, i32, i32, i64, vp, vp]),
         "pdf_bessel": (ct.c_int, [i32, vp, vp, vp, i64, vp]),
         "pdf_build_greens": (ct.c_int, [ct.c_double, ct.c_double, i32, i32, vp, vp, vp, i32, vp, vp, vp, dp, vp]),
         "pdf_incident_fields": (ct.c_int, [i32, ct.c_double, i32, i32, vp, vp, vp, i32, vp, vp]),

@@ -73,6 +73,10 @@ struct pdf_ctx {
   // spectrum chunk, data-GEMM pixel chunking
   int large, dgemm, NPV, chunk, dg_chunk, dg_nchunks, dg_nq;
   int split;         // pixel stage as numden / pixel_a / pixel_b (pdf_shard.cuh) in the training loop
+  // peer scatter of the unfused backward's gradient (pdf_shard_step_c_scatter), set around the call
+  double* const* sc_peers = nullptr;
+  int sc_me = 0;
+  long long sc_shard = 0;
   int xbwd;          // split network backward in the training loop (net_gh_x / net_adam_x)
   long long Np;
   size_t csz, rsz;   // complex / real element size
@@ -732,7 +736,10 @@ static int net_bwd_layer(pdf_ctx* c, const T* gz, const T* hin, int K, int N, T*
   a.m = m; a.v = v; a.grad = grad; a.step = c->step;
   a.lr = (T)c->d.lr; a.b1 = (T)c->d.adam_b1; a.b2 = (T)c->d.adam_b2; a.eps = (T)c->d.adam_eps;
   a.gzprev = gzprev; a.gzp_ss = (long long)c->rows * K; a.err = c->err;
+  a.peers = fused ? nullptr : c->sc_peers; a.peer_me = c->sc_me; a.peer_shard = c->sc_shard;
   if (K % Epc<T>::v || N % Epc<T>::v) return fail(PDF_EINVAL, "layer widths must be multiples of 16 bytes");
+  if (a.peers && (sizeof(T) != 8 || !env_int("PDF_NET_MMA", 1)))
+    return fail(PDF_EINVAL, "the peer-scattered backward needs the float64 DMMA kernels");
   static const int use_mma = env_int("PDF_NET_MMA", 1);
   if constexpr (sizeof(T) == 8) {
     if (use_mma) return bwd_mma_layer(c, a, fused != 0, st);
@@ -1688,6 +1695,33 @@ extern "C" int pdf_shard_step_c_part(pdf_ctx* c, const void* theta, const double
   if (!c || !theta || !red2 || !bucket || layer < 1 || layer > 3 || c->d.S != 1)
     return fail(PDF_EINVAL, "bad argument");
   return DISPATCH(c, shard_c_part_impl, c, theta, red2, bucket, (int)layer, breakdown, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_shard_step_c_scatter(pdf_ctx* c, const void* theta, const double* red2, double* const* peers,
+                                        int32_t world, int32_t rank, int64_t shard, int32_t layer, double* breakdown,
+                                        void* stream) {
+  if (!c || !theta || !red2 || !peers || world < 1 || rank < 0 || rank >= world || shard < 2 || (shard & 1) ||
+      shard * world < c->Np || layer < 1 || layer > 3 || c->d.S != 1 || c->d.dtype != PDF_F64)
+    return fail(PDF_EINVAL, "bad argument");
+  c->sc_peers = peers; c->sc_me = rank; c->sc_shard = shard;
+  // the bucket base is unused in scatter mode: any non-null pointer keeps shard_c_part_impl's arithmetic defined
+  const int r = shard_c_part_impl<double>(c, theta, red2, const_cast<void*>(theta), (int)layer, breakdown,
+                                          (cudaStream_t)stream);
+  c->sc_peers = nullptr;
+  return r;
+}
+
+extern "C" int pdf_adam_gather(pdf_ctx* c, const double* recv, double* const* thetas, double* m, double* v,
+                               int32_t world, int32_t rank, int64_t shard, const int32_t* t_dev, void* stream) {
+  if (!c || !recv || !thetas || !m || !v || !t_dev || world < 1 || rank < 0 || rank >= world || shard < 1 ||
+      shard * world < c->Np || c->d.dtype != PDF_F64)
+    return fail(PDF_EINVAL, "bad argument");
+  const int blocks = (int)std::min<long long>((shard + 255) / 256, 148LL * 8);
+  adam_gather_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(recv, thetas, m, v, world, rank, shard, c->Np,
+                                                               c->d.lr, c->d.adam_b1, c->d.adam_b2, c->d.adam_eps,
+                                                               (const int*)t_dev, c->err);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
 }
 
 extern "C" int pdf_net_offsets(const pdf_ctx* c, int64_t* offs) {

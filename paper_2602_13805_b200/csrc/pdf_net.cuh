@@ -212,7 +212,20 @@ struct NetBwdArgs {
   int* err;                           // [S]
   int tl;                             // timeline slot + 1 (0: off)
   int* snap;                          // split backward: *snap = *step (Adam t of this iteration) or null
+  // peer scatter (incidence sharding, unfused mode): g_W / g_b entry at flat index f goes to
+  // rank o = f / peer_shard, slot [peer_me][f - o peer_shard] of that rank's receive buffer
+  // peers[o] (a peer-mapped address on the multi-GPU box): the reduce-scatter of the gradient
+  // happens in the epilogue of the kernel that computes it
+  double* const* peers;
+  int peer_me;
+  long long peer_shard;
 };
+
+// destination of flat parameter index f in the peer-scatter layout
+__device__ __forceinline__ double* peer_slot(double* const* peers, int me, long long shard, long long f) {
+  const long long o = f / shard;
+  return peers[o] + (size_t)me * shard + (f - o * shard);
+}
 
 // Adam in the reference's operation order (network.py:252-257).  The bias
 // corrections are applied as products with 1/(1-b^t) and the remaining
@@ -569,6 +582,36 @@ __global__ void adam_flat_dev_kernel(T* p, T* m, T* v, const T* g, long long cou
     if (!isfinite(pp)) bits |= ERR_NONFINITE_PARAM;
     p[i] = pp; m[i] = mm; v[i] = vv;
   }
+  if (bits) atomicOr(err, bits);
+}
+
+// owner side of the peer-scattered gradient (incidence sharding): for this rank's
+// shard [me shard, (me + 1) shard) of the flat parameters, g = sum over source
+// ranks r of recv[r][i] (rank order), one Adam step (step t from device
+// memory), and the updated parameter written to every rank's theta (peer
+// stores: the all-gather of the parameters)
+__global__ void adam_gather_kernel(const double* __restrict__ recv, double* const* thetas, double* __restrict__ m,
+                                   double* __restrict__ v, int world, int me, long long shard, long long np,
+                                   double lr, double b1, double b2, double eps, const int* t_dev, int* err) {
+  const double t = (double)*t_dev;
+  const double bc1 = 1.0 / (1.0 - pow(b1, t)), bc2 = 1.0 / (1.0 - pow(b2, t));
+  const long long base = (long long)me * shard;
+  const double* own = thetas[me];
+  int bits = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < shard; i += (long long)gridDim.x * blockDim.x) {
+    const long long f = base + i;
+    if (f >= np) break;
+    double g = 0.0;
+    for (int r = 0; r < world; ++r) g += recv[(size_t)r * shard + i];
+    if (!isfinite(g)) bits |= ERR_NONFINITE_GRAD;
+    double p = own[f], mm = m[i], vv = v[i];
+    adam_one<double>(p, mm, vv, g, lr, b1, b2, eps, bc1, bc2);
+    if (!isfinite(p)) bits |= ERR_NONFINITE_PARAM;
+    m[i] = mm;
+    v[i] = vv;
+    for (int r = 0; r < world; ++r) thetas[r][f] = p;
+  }
+  __threadfence_system();
   if (bits) atomicOr(err, bits);
 }
 

@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
           thb[gn] = bp; mbb[gn] = bm; vbb[gn] = bv;
           if (gn + BM_NCH < ne) { bp = thb[gn + BM_NCH]; bm = mbb[gn + BM_NCH]; bv = vbb[gn + BM_NCH]; }
         } else {
-          a.grad[scene * a.th_ss + a.b_off + gn] = gb;
+          if (a.peers) *peer_slot(a.peers, a.peer_me, a.peer_shard, a.b_off + gn) = gb;
+          else a.grad[scene * a.th_ss + a.b_off + gn] = gb;
         }
       }
     }
@@ -498,6 +499,9 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
           *reinterpret_cast<double2*>(W + o) = p;
           *reinterpret_cast<double2*>(mW + o) = m2;
           *reinterpret_cast<double2*>(vW + o) = v2;
+        } else if (a.peers) {
+          *reinterpret_cast<double2*>(peer_slot(a.peers, a.peer_me, a.peer_shard, a.w_off + (long long)o)) =
+              make_double2(gw0, gw1);
         } else {
           *reinterpret_cast<double2*>(gW + o) = make_double2(gw0, gw1);
         }
@@ -536,6 +540,7 @@ __global__ void __launch_bounds__(WB * 32) net_bwd_mma_kernel(NetBwdArgs<double>
   } else {
     cp_async_wait<0>();
   }
+  if (a.peers) __threadfence_system();   // peer stores visible before the barrier that follows
   tl_mark(a.tl, 2);
 }
 

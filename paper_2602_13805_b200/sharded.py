@@ -307,3 +307,154 @@ class ShardedTrainer:
 
     def check_errors(self):
         self.s.dev.check_errors()
+
+
+# ---------------------------------------------------------------------------- peer-memory form
+def peer_shard_len(n_params: int, world: int) -> int:
+    """Per-rank shard of the flat parameters for the peer-scatter layout: even
+    (16-byte g_W pairs never straddle two owners) and world * shard >= n_params."""
+    s = -(-n_params // world)
+    return s + (s & 1)
+
+
+class PeerTrainer:
+    """Incidence sharding with the gradient reduce-scatter fused into the
+    backward kernels (the prompt's compute -> collective fusion).
+
+    Every rank runs step_a / red1 / step_b / red2 as `ShardedTrainer` does;
+    then `pdf_shard_step_c_scatter` (layers 3, 2, 1) stores each g_W / g_b
+    entry, in the epilogue of the DMMA kernel that computes it, straight into
+    the owner rank's receive buffer (peer stores over NVLink); after a
+    barrier `pdf_adam_gather` on every rank sums its shard over the source
+    ranks in rank order, applies Adam and writes the updated parameters into
+    every rank's parameter vector (the all-gather, again as peer stores), and
+    a second barrier closes the iteration.  No NCCL call moves gradient or
+    parameter bytes.
+
+    `shards` are either the ranks of one process emulated on one GPU (a list
+    of IncidenceShard over all views, `group=None`: the "peer" buffers are
+    local and the barriers are stream order -- no kernel waits for another)
+    or this rank's single shard on a multi-GPU node (`group` given): the
+    receive and parameter buffers are torch symmetric memory and their
+    peer-mapped addresses are exchanged once (`rendezvous`)."""
+
+    def __init__(self, shards, theta0: torch.Tensor, group=None, graph: bool = False, graph_iters: int = 10):
+        self.shards = list(shards)
+        self.group = group
+        self.graph_on, self.G, self.graph = graph, max(1, int(graph_iters)), None
+        dev0 = self.shards[0].dev
+        self.lib = dev0.lib
+        dd, rdt = dev0.device, dev0.rdt
+        if rdt != torch.float64:
+            raise ValueError("the peer-scatter path is float64")
+        np_ = theta0.numel()
+        if group is None:
+            self.world, self.ranks = len(self.shards), list(range(len(self.shards)))
+        else:
+            import torch.distributed as dist
+            self.world, self.ranks = dist.get_world_size(group), [dist.get_rank(group)]
+            if len(self.shards) != 1:
+                raise ValueError("one shard per process on a multi-GPU node")
+        W = self.world
+        self.np = np_
+        self.shard = peer_shard_len(np_, W)
+        n_pad = W * self.shard
+        if group is None:
+            self.recv = [torch.zeros(n_pad, dtype=rdt, device=dd) for _ in self.shards]
+            self.theta = [torch.zeros(n_pad, dtype=rdt, device=dd) for _ in self.shards]
+            recv_ptrs = [t.data_ptr() for t in self.recv]
+            th_ptrs = [t.data_ptr() for t in self.theta]
+        else:
+            import torch.distributed._symmetric_memory as symm
+            self.recv = [symm.empty(n_pad, dtype=rdt, device=dd)]
+            self.theta = [symm.empty(n_pad, dtype=rdt, device=dd)]
+            self.recv[0].zero_()
+            self.theta[0].zero_()
+            h_recv = symm.rendezvous(self.recv[0], group)
+            h_th = symm.rendezvous(self.theta[0], group)
+            recv_ptrs, th_ptrs = list(h_recv.buffer_ptrs), list(h_th.buffer_ptrs)
+            self._handles = (h_recv, h_th)
+        self.recv_peers = torch.tensor(recv_ptrs, dtype=torch.int64, device=dd)
+        self.theta_peers = torch.tensor(th_ptrs, dtype=torch.int64, device=dd)
+        for th in self.theta:
+            th[:np_].copy_(theta0.reshape(-1))
+        self.m = [torch.zeros(self.shard, dtype=rdt, device=dd) for _ in self.shards]
+        self.v = [torch.zeros(self.shard, dtype=rdt, device=dd) for _ in self.shards]
+        self.t_dev = torch.zeros(1, dtype=torch.int32, device=dd)
+        self._bar = torch.zeros(1, dtype=torch.float64, device=dd)
+        if group is not None:
+            self._barrier()
+
+    def _barrier(self):
+        if self.group is not None:          # stream-ordered: every rank's earlier kernels are done
+            import torch.distributed as dist
+            dist.all_reduce(self._bar, group=self.group)
+
+    def _reduce(self, what):
+        if self.group is None:
+            LocalShards()(self.shards, what)
+        else:
+            TorchDistReducer(self.group)(self.shards, what)
+
+    def iteration(self, trace_row: torch.Tensor | None = None):
+        for s, th in zip(self.shards, self.theta):
+            s.step_a(th)
+        self._reduce("red1")
+        for s in self.shards:
+            s.step_b()
+        self._reduce("red2")
+        for s, th, r in zip(self.shards, self.theta, self.ranks):
+            for L in (3, 2, 1):
+                N.check(self.lib.pdf_shard_step_c_scatter(
+                    s.dev.ctx, _ptr(th), _ptr(s.red2), _ptr(self.recv_peers), self.world, r, self.shard, L,
+                    _ptr(s.bd), _stream()))
+        if trace_row is not None:
+            trace_row.copy_(self.shards[0].bd[0])
+        self._barrier()
+        self.t_dev += 1
+        for s, rv, m, v, r in zip(self.shards, self.recv, self.m, self.v, self.ranks):
+            N.check(self.lib.pdf_adam_gather(s.dev.ctx, _ptr(rv), _ptr(self.theta_peers), _ptr(m), _ptr(v),
+                                             self.world, r, self.shard, _ptr(self.t_dev), _stream()))
+        self._barrier()
+
+    def _state(self):
+        return [*self.theta, *self.m, *self.v, self.t_dev]
+
+    def train(self, k: int) -> torch.Tensor:
+        """k iterations (graph=True: replayed from a CUDA graph of graph_iters
+        iterations that holds the library kernels and the NCCL barriers)."""
+        dd = self.theta[0].device
+        trace = torch.zeros(k, 6, dtype=torch.float64, device=dd)
+        done = 0
+        if self.graph_on and k >= self.G:
+            if self.graph is None:
+                saved = [x.clone() for x in self._state()]
+                for _ in range(2):                 # warm the collectives outside the capture
+                    self.iteration()
+                torch.cuda.synchronize()
+                for x, y in zip(self._state(), saved):
+                    x.copy_(y)
+                self._barrier()
+                self.gtrace = torch.zeros(self.G, 6, dtype=torch.float64, device=dd)
+                st = torch.cuda.Stream(device=dd)
+                st.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(self.G):
+                        self.iteration(self.gtrace[i])
+                self.graph = g
+            while done + self.G <= k:
+                self.graph.replay()
+                trace[done:done + self.G].copy_(self.gtrace)
+                done += self.G
+        while done < k:
+            self.iteration(trace[done])
+            done += 1
+        return trace
+
+    def params(self, rank: int = 0) -> torch.Tensor:
+        return self.theta[rank][: self.np]
+
+    def check_errors(self):
+        for s in self.shards:
+            s.dev.check_errors()

@@ -65,3 +65,58 @@ def test_zero1_trainer_single_rank_nccl(graph):
             dist.destroy_process_group()
     ref_tr = np.array([b.as_row() for b in ref.trace])
     np.testing.assert_allclose(trace, ref_tr, rtol=1e-9)
+
+
+@pytest.mark.parametrize("cfg_id,world,graph", [(1, 2, False), (1, 3, False), (3, 2, False), (1, 2, True)])
+def test_peer_scatter_emulated_ranks(cfg_id, world, graph):
+    """Reduce-scatter fused into the backward (pdf_shard_step_c_scatter: every
+    g_W / g_b entry stored by the kernel that computes it into its owner's
+    receive buffer) + owner-side Adam with the parameter all-gather as stores
+    (pdf_adam_gather), with `world` ranks emulated in one process on one GPU
+    (local buffers stand in for the peer-mapped ones, stream order for the
+    barriers): the iteration trace matches the unsharded run and every rank
+    ends with the same parameters."""
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, PeerTrainer
+    g = golden(f"cfg{cfg_id}")
+    st = Setup(cfg_baseline(cfg_id), plane=True)
+    cfg = st.cfg
+    k = 12
+    ref = BatchReconstructor(cfg, 1, e_inc=st.e_inc).run([g["data"]], seeds=[cfg.rng_seed], k_iters=k)[0]
+    shards = [IncidenceShard(st.ops, st.e_inc, g["data"], mf=cfg.m_f, beta=cfg.beta, lambdas=LAM, tau_b=cfg.tau_b,
+                             rank=r, world=world) for r in range(world)]
+    theta0 = torch.as_tensor(_theta0([cfg.rng_seed], 4 * cfg.m_f ** 2), device="cuda")
+    tr = PeerTrainer(shards, theta0, graph=graph, graph_iters=5)
+    trace = tr.train(k).cpu().numpy()
+    tr.check_errors()
+    np.testing.assert_allclose(trace, np.array([b.as_row() for b in ref.trace]), rtol=1e-9)
+    for r in range(1, world):
+        assert torch.equal(tr.params(r), tr.params(0))
+
+
+def test_peer_scatter_symmetric_memory_single_rank():
+    """The multi-GPU form of PeerTrainer -- torch symmetric memory buffers,
+    rendezvous of their peer addresses, NCCL barriers -- on a one-rank group."""
+    import torch.distributed as dist
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, PeerTrainer
+    g = golden("cfg1")
+    st = Setup(cfg_baseline(1), plane=True)
+    cfg = st.cfg
+    k = 8
+    ref = BatchReconstructor(cfg, 1, e_inc=st.e_inc).run([g["data"]], seeds=[cfg.rng_seed], k_iters=k)[0]
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        sh = IncidenceShard(st.ops, st.e_inc, g["data"], mf=cfg.m_f, beta=cfg.beta, lambdas=LAM, tau_b=cfg.tau_b,
+                            rank=0, world=1)
+        theta0 = torch.as_tensor(_theta0([cfg.rng_seed], 4 * cfg.m_f ** 2), device="cuda")
+        tr = PeerTrainer([sh], theta0, group=dist.group.WORLD, graph=True, graph_iters=4)
+        trace = tr.train(k).cpu().numpy()
+        tr.check_errors()
+    finally:
+        if own:
+            dist.destroy_process_group()
+    np.testing.assert_allclose(trace, np.array([b.as_row() for b in ref.trace]), rtol=1e-9)
