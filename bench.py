@@ -728,7 +728,7 @@ def run_ours(args, d: Dist):
     torch.cuda.synchronize()
     e2e_s = d.max((time.perf_counter() - t0) / args.steps)
     M = cfg.m1
-    h2d = data[0].nbytes + M * M * 16
+    h2d = data[0].nbytes + M * M * 16 + int(dev.n_params) * 8     # data, chi_true, the run's initial weights
     d2h = 3 * M * M * 16 + k * 6 * 8 + 6 * 8 + 8
 
     batched = batched_leg(args, d, e_inc, fp64, hbm, notes) if args.batch else None

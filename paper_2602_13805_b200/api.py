@@ -601,12 +601,6 @@ class BatchReconstructor:
             else:
                 slot = 0 if pre is None else 1 - pre[1]
                 pending = _theta0_async(seeds, self.m0_eff, self._pinned(slot).numpy())
-        dev.set_data(mats)
-        chi0, alpha0 = self._initialise()
-        if check_init and bool(dev.pole_flag):
-            for f in pending or ():
-                f.result()       # the pinned buffer must be idle before a later run reuses it
-            raise PoleError("beta*chi + 1 vanishes at some pixel")
         # persistent device state (theta, Adam moments, trace) for this batch shape
         bufs = self.__dict__.get("_dev_bufs")
         if bufs is None or bufs[3].shape[0] < max(k, 1):
@@ -618,10 +612,29 @@ class BatchReconstructor:
             self._dev_bufs = bufs
         theta, m, v, trace_buf = bufs
         trace = trace_buf[:max(k, 1)]
+        # initial weights already drawn (a prefetch): their upload runs on a copy stream
+        # while the GPU runs the initialisation
+        early = pending is not None and all(f.done() for f in pending)
+        if early:
+            cs = self.__dict__.setdefault("_copy_stream", torch.cuda.Stream(device=dev.device))
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                theta.copy_(self._pinned(slot), non_blocking=True)
+            up_done = torch.cuda.Event()
+            up_done.record(cs)
+        dev.set_data(mats)
+        chi0, alpha0 = self._initialise()
+        if check_init and bool(dev.pole_flag):
+            for f in pending or ():
+                f.result()       # the pinned buffer must be idle before a later run reuses it
+            raise PoleError("beta*chi + 1 vanishes at some pixel")
         if pending is not None:
-            for f in pending:
-                f.result()
-            theta.copy_(self._pinned(slot), non_blocking=True)
+            if early:
+                torch.cuda.current_stream().wait_event(up_done)
+            else:
+                for f in pending:
+                    f.result()
+                theta.copy_(self._pinned(slot), non_blocking=True)
             if self.theta_cache:
                 self._theta0 = {key: theta.clone()}
         else:
