@@ -24,7 +24,9 @@ class _SolverDevice:
         from dataclasses import replace
         from .engine import DeviceProblem
         M = ops.m1
-        one_rx = replace(ops, gs_matrix=np.ascontiguousarray(ops.gs_matrix[:1]))   # views / receivers unused
+        gs1 = ops.gs_matrix[:1]
+        gs1 = gs1.contiguous() if isinstance(gs1, torch.Tensor) else np.ascontiguousarray(gs1)
+        one_rx = replace(ops, gs_matrix=gs1)   # views / receivers unused (host or device operators)
         self.dev = DeviceProblem(one_rx, np.ones((1, M, M), complex), np.ones((1, 1), complex), mf=1, beta=6.0,
                                  lambdas=(0, 0, 0), tau_b=0.5)
         self.ws = None

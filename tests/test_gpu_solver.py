@@ -80,3 +80,15 @@ def test_batched_per_scene_fields_and_determinism():
     assert torch.equal(x[0], x0[0])           # scene 0 alone: same reductions, same result
     assert torch.equal(x[2], torch.as_tensor(b[2], device="cuda"))   # chi = 0: E = E_inc, no iteration
     assert float(res.max()) <= 1e-8 * 1.0001
+
+
+def test_solver_on_device_built_operators(g_solver):
+    """The forward solve runs on operators built in HBM (greens.build_greens_device)."""
+    from paper_2602_13805_b200.greens import build_greens_device, incident_fields_device
+    from paper_2602_13805_b200.solver import solve_fields_gpu
+    cfg, ops, einc, chi = _problem(64)
+    from paper_2602_13805_b200 import build_array, build_grid
+    grid, arr = build_grid(cfg), build_array(cfg)
+    dops = build_greens_device(cfg, arr, grid)
+    x, res, _ = solve_fields_gpu(chi.values, incident_fields_device(cfg, arr, grid, "line"), dops)
+    assert rel(x[0].cpu().numpy(), g_solver["x64"]) < 1e-7
