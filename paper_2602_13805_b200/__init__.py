@@ -6,12 +6,14 @@ The setup modules (config, geometry, scenes, operators) import without a GPU;
 the solver entry points load ``libpdfb200.so`` on first use and fail loudly
 if it is missing.
 """
-from .config import C0, CcoParams, ConfigError, ImagingConfig, config_from_dict, config_to_dict
+from .config import (C0, CcoParams, ConfigError, ImagingConfig, config_from_dict, config_hash, config_to_dict,
+                     load_config, save_config)
 from .geometry import AntennaArray, ComplexGrid, GridGeometry, build_array, build_grid, perturb_array
 from .operators import (FieldSet, GeometryError, GreensOperators, NoConvergenceError, ScatteredData,
                         SimulationResult, add_awgn, build_greens, incident_fields, plane_wave_fields,
                         simulate, solve_total_field, synthesize_scattered)
-from .scenes import Scene, SceneError, Shape, builtin_scene, ellipse, rasterize
+from .scenes import (Scene, SceneError, Shape, builtin_scene, ellipse, load_scene, rasterize, resolve_scene,
+                     save_scene, scene_from_dict, scene_to_dict)
 
 __version__ = "0.1.0"
 

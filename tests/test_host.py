@@ -367,3 +367,34 @@ def test_config_hash_matches_reference():
     cfg2 = ImagingConfig(frequency=C0, doi_side=2.0, m1=64, m2=64, n_tx=16, n_rx=32, ring_radius=3.0, m_f=8,
                          k_iters=500, rng_seed=1)
     assert config_hash(cfg2) == "f74b4a5e2a8a3f31"
+
+
+# ------------------------------------------------------------------ scene files (scenes.py:158-215)
+def test_scene_json_round_trip(tmp_path):
+    import json
+    from paper_2602_13805_b200 import builtin_scene, load_scene, save_scene, scene_from_dict, scene_to_dict
+    for name in ("austria", "case1", "case2", "case3", "case4"):
+        scene = builtin_scene(name, 3.0 + 0.5j)
+        assert scene_from_dict(scene_to_dict(scene)) == scene
+        path = tmp_path / f"{name}.json"
+        save_scene(path, scene)
+        assert load_scene(path) == scene
+    d = json.loads((tmp_path / "case4.json").read_text())
+    assert [s["kind"] for s in d["shapes"]] == ["annulus", "polygon", "disk"]
+    assert d["shapes"][0]["eps_r"] == [3.0, 0.5] and set(d["shapes"][0]) == {"kind", "eps_r", "center", "r_inner",
+                                                                              "r_outer"}
+
+
+def test_resolve_scene_specs(tmp_path):
+    from paper_2602_13805_b200 import SceneError, resolve_scene, save_scene, scene_from_dict
+    s = resolve_scene("austria:2")
+    assert len(s.shapes) == 3
+    assert resolve_scene("case3:5:0.8").shapes[0].eps_r == 5.0
+    path = tmp_path / "s.json"
+    save_scene(path, s)
+    assert resolve_scene(str(path)) == s
+    assert scene_from_dict({"shapes": [{"kind": "disk", "eps_r": 2, "center": [0, 0], "radius": 0.1}]}).shapes[0].eps_r == 2
+    with pytest.raises(SceneError):
+        scene_from_dict({"shapes": [{"kind": "blob", "eps_r": 2}]})
+    with pytest.raises(SceneError):
+        resolve_scene("nosuch:2")
