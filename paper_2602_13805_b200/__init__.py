@@ -10,6 +10,7 @@ from .config import (C0, CcoParams, ConfigError, ImagingConfig, config_from_dict
                      load_config, save_config)
 from .geometry import AntennaArray, ComplexGrid, GridGeometry, build_array, build_grid, perturb_array
 from .operators import (FieldSet, GeometryError, GreensOperators, NoConvergenceError, ScatteredData,
+                        SingularSystemError,
                         SimulationResult, add_awgn, build_greens, incident_fields, plane_wave_fields,
                         simulate, solve_total_field, synthesize_scattered)
 from .scenes import (Scene, SceneError, Shape, builtin_scene, ellipse, load_scene, rasterize, resolve_scene,
@@ -21,7 +22,8 @@ _API = ("LossBreakdown", "LossContext", "PipelineState", "SpectralBasis", "Netwo
         "ReconstructionResult", "BatchReconstructor", "pipeline_forward", "pipeline_backward", "grad_alpha",
         "loss_total", "init_network", "forward_net", "flatten_params", "unflatten_params", "grad_loss",
         "adam_step", "bp_initialize", "init_alpha", "recover_contrast", "apply_cco", "reconstruct",
-        "relative_error", "count_components", "PoleError", "ZeroDataError", "PhysicsLoss")
+        "relative_error", "count_components", "PoleError", "ZeroDataError", "PhysicsLoss", "truncate", "expand",
+        "truncate_adjoint_scale", "apply_gd", "apply_gd_adjoint", "apply_gs_adjoint")
 
 
 def __getattr__(name):

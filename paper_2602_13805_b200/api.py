@@ -10,6 +10,8 @@ functions (citations relative to /root/reference/pkg/src/pdfisp/):
   forward_net, flatten/unflatten      network.py:143-176
   grad_loss                           network.py:183-223
   AdamState, adam_step                network.py:230-264
+  truncate, expand                    spectral.py:56-87
+  apply_gd(_adjoint), apply_gs_adjoint forward.py:140-151, 303-306
   bp_initialize, init_alpha           reconstruct.py:52-153
   recover_contrast                    cie.py:83-99
   apply_cco                           filters.py:56-67
@@ -69,6 +71,85 @@ class SpectralBasis:
     @property
     def n_cells(self) -> int:
         return self.m1 * self.m2
+
+
+_BASIS_DEVS: dict = {}
+
+
+def _basis_device(basis: SpectralBasis) -> DeviceProblem:
+    """A geometry-free context for the spectral transforms of one basis."""
+    from .engine import GRID_SIZES
+    if basis.m1 != basis.m2 or basis.m1 not in GRID_SIZES:
+        raise ValueError(f"the GPU transforms need a square grid with edge in {GRID_SIZES}, "
+                         f"got ({basis.m1}, {basis.m2})")
+    key = (basis.m1, basis.m_f)
+    if key not in _BASIS_DEVS:
+        M = basis.m1
+        cfg = ImagingConfig(m1=M, m2=M, m_f=basis.m_f, n_tx=1, n_rx=1).validate()
+        ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
+        _BASIS_DEVS[key] = DeviceProblem(ops, np.ones((1, M, M), complex), np.ones((1, 1), complex),
+                                         mf=basis.m_f, beta=6.0, lambdas=(0, 0, 0), tau_b=0.5)
+    return _BASIS_DEVS[key]
+
+
+def truncate(basis: SpectralBasis, j_view) -> np.ndarray:
+    """Corner-block DFT coefficients, (..., m1, m2) -> (..., m0), forward DFT
+    unnormalised (spectral.py:56-65); computed by pdf_truncate."""
+    j_view = np.asarray(j_view)
+    if j_view.shape[-2:] != (basis.m1, basis.m2):
+        raise ValueError(f"expected trailing dims ({basis.m1}, {basis.m2})")
+    dev = _basis_device(basis)
+    return dev.truncate(_cdev(j_view, dev)).cpu().numpy()
+
+
+def expand(basis: SpectralBasis, alpha) -> np.ndarray:
+    """Image(s) whose DFT is alpha on the corner blocks, zero elsewhere, inverse
+    DFT carrying 1/(m1 m2) (spectral.py:68-79); computed by pdf_expand."""
+    alpha = np.asarray(alpha, dtype=np.complex128)
+    if alpha.shape[-1] != basis.m0:
+        raise ValueError(f"expected trailing dim {basis.m0}")
+    dev = _basis_device(basis)
+    return dev.expand(_cdev(alpha, dev)).cpu().numpy()
+
+
+def truncate_adjoint_scale(basis: SpectralBasis) -> float:
+    """<expand(a), x> = c <a, truncate(x)> with c = 1/(m1 m2) (spectral.py:82-87)."""
+    return 1.0 / (basis.m1 * basis.m2)
+
+
+def _ops_device(ops: GreensOperators) -> DeviceProblem:
+    views = np.ones((1, ops.m1, ops.m2), complex)
+    return _ONE_SHOT.get(("ops", id(ops)), (ops,),
+                         lambda: DeviceProblem(ops, views, np.ones((1, ops.n_rx), complex), mf=1, beta=6.0,
+                                               lambdas=(0, 0, 0), tau_b=0.5))
+
+
+def apply_gd(ops: GreensOperators, x) -> np.ndarray:
+    """G_D on (..., m1, m2) images (forward.py:140-146): pdf_apply_gd, one
+    zero-padded FFT convolution per image."""
+    x = np.asarray(x)
+    if x.shape[-2:] != (ops.m1, ops.m2):
+        raise ValueError(f"expected trailing dims ({ops.m1}, {ops.m2})")
+    dev = _ops_device(ops)
+    return dev.apply_gd(_cdev(x, dev)).cpu().numpy()
+
+
+def apply_gd_adjoint(ops: GreensOperators, x) -> np.ndarray:
+    """G_D^H (forward.py:149-151)."""
+    x = np.asarray(x)
+    if x.shape[-2:] != (ops.m1, ops.m2):
+        raise ValueError(f"expected trailing dims ({ops.m1}, {ops.m2})")
+    dev = _ops_device(ops)
+    return dev.apply_gd(_cdev(x, dev), adjoint=True).cpu().numpy()
+
+
+def apply_gs_adjoint(ops: GreensOperators, rows) -> np.ndarray:
+    """G_S^H on receiver vectors, (..., n_rx) -> (..., m1, m2) (forward.py:303-306)."""
+    rows = np.asarray(rows)
+    if rows.shape[-1] != ops.n_rx:
+        raise ValueError(f"expected trailing dim {ops.n_rx}")
+    dev = _ops_device(ops)
+    return dev.gs_adjoint(_cdev(rows, dev)).cpu().numpy()
 
 
 # ---------------------------------------------------------------------------- losses

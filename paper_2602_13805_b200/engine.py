@@ -118,7 +118,7 @@ class DeviceProblem:
         self.data = torch.as_tensor(data, dtype=cd, device=dev).contiguous()
         self.mask = None
         if mask is not None:
-            mk = np.broadcast_to(np.asarray(mask, dtype=float), data.shape)
+            mk = np.array(np.broadcast_to(np.asarray(mask, dtype=float), data.shape))
             self.mask = torch.as_tensor(mk, dtype=self.rdt, device=dev).contiguous()
         self.r_fixed = None
         if r_fixed is not None:

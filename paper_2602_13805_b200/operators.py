@@ -38,6 +38,12 @@ class NoConvergenceError(RuntimeError):
     pass
 
 
+class SingularSystemError(RuntimeError):
+    """Unrecoverable Krylov breakdown (forward.py:35-36).  Declared for import
+    compatibility: like the reference's BiCGStab, the GPU solver restarts on
+    breakdown and reports NoConvergenceError at the iteration cap instead."""
+
+
 @dataclass
 class FieldSet:
     views: np.ndarray

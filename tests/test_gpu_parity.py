@@ -253,3 +253,44 @@ def test_physics_loss_autograd_function():
     lm = dev.loss_value(a0 * (1 - h))[0][0, 5].item()
     fd = (lp - lm) / (2 * h)
     assert abs(s.grad.item() - fd) < 1e-6 * max(1.0, abs(fd)), (s.grad.item(), fd)
+
+
+def test_module_level_operator_drop_ins(tiny_setup, g_tiny, cfg1_setup):
+    """forward.apply_gd / apply_gd_adjoint / apply_gs_adjoint and
+    spectral.truncate / expand as module-level functions (reference signatures,
+    host arrays in and out), on the golden vectors and with extra leading dims."""
+    from oracle import pdf_oracle as O
+    from paper_2602_13805_b200 import (SpectralBasis, apply_gd, apply_gd_adjoint, apply_gs_adjoint, expand,
+                                       truncate, truncate_adjoint_scale)
+    g, ops, c = g_tiny, tiny_setup.ops, tiny_setup.cfg
+    basis = SpectralBasis(c.m1, c.m2, c.m_f)
+    assert rel(apply_gd(ops, g["x"]), g["gd_x"]) < 1e-12
+    assert rel(apply_gd_adjoint(ops, g["x"]), g["gdh_x"]) < 1e-12
+    assert rel(apply_gs_adjoint(ops, g["rows"]), g["gsh_rows"]) < 1e-12
+    assert rel(expand(basis, g["alpha"]), g["exp_alpha"]) < 1e-12
+    assert rel(truncate(basis, g["x"]), g["trunc_x"]) < 1e-12
+    # (2, 3, m1, m2) leading dims, cfg1 sizes, against the oracle
+    st = cfg1_setup
+    oo = oracle_ops(st)
+    M, mf = st.cfg.m1, st.cfg.m_f
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((2, 3, M, M)) + 1j * rng.standard_normal((2, 3, M, M))
+    assert apply_gd(st.ops, x).shape == x.shape
+    assert rel(apply_gd(st.ops, x), O.apply_gd(oo, x)) < 1e-12
+    assert rel(apply_gd_adjoint(st.ops, x), O.apply_gd_adj(oo, x)) < 1e-12
+    rows = rng.standard_normal((2, 3, st.cfg.n_rx)) + 0j
+    assert rel(apply_gs_adjoint(st.ops, rows), O.apply_gs_adj(oo, rows)) < 1e-12
+    b = SpectralBasis(M, M, mf)
+    a = truncate(b, x)
+    assert a.shape == (2, 3, b.m0) and rel(a, O.truncate(x, mf)) < 1e-12
+    assert rel(truncate(b, expand(b, a)), a) < 1e-12
+    # <expand(a), y> = c <a, truncate(y)>
+    lhs = np.vdot(expand(b, a[0, 0]), x[1, 2])
+    rhs = truncate_adjoint_scale(b) * np.vdot(a[0, 0], truncate(b, x[1, 2]))
+    assert abs(lhs - rhs) < 1e-12 * abs(lhs)
+    with pytest.raises(ValueError):
+        truncate(b, x[..., :-1])
+    with pytest.raises(ValueError):
+        expand(b, a[..., :-1])
+    with pytest.raises(ValueError):
+        apply_gd(st.ops, x[..., :-1, :])
