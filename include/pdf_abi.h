@@ -32,6 +32,17 @@
  *                       solve_total_field               forward.py:251-275
  *   pdf_relative_error  relative_error                  reconstruct.py:243-247
  *   pdf_count_components count_components               reconstruct.py:250-254
+ *   pdf_chi_to_r        chi_to_r / r_to_chi             cie.py:24-39
+ *   pdf_default_eps_reg default_eps_reg                 cie.py:42-50
+ *   pdf_pixel_ls        pixel_least_squares             cie.py:66-80
+ *   pdf_cie_fields      E = E_inc + G_D J, P, state     cie.py:92-114, losses.py:219-228
+ *                       residual (cie_state_residual)
+ *   pdf_masked_residual data residual                   losses.py:229-231
+ *   pdf_regularizers    loss_bound/tv/bridge + grads,   losses.py:121-196
+ *                       regularizer_chi_grad
+ *   pdf_box_mean        box_mean                        filters.py:16-33
+ *   pdf_guided_filter   guided_filter                   filters.py:36-53
+ *   pdf_cco_image       apply_cco on any m1 x m2        filters.py:56-67
  *   pdf_get_error       PoleError / FloatingPointError  cie.py:27-29, losses.py:239-243,
  *                                                       network.py:221-222, 260-261
  *
@@ -250,6 +261,43 @@ int pdf_relative_error(const double* eps_hat, const double* eps_true, int32_t st
                        double offset, double* out, void* stream);
 int pdf_count_components(const double* eps, int32_t stride, int32_t m1, int32_t m2, int32_t count, double offset,
                          double threshold, int32_t* labels, int32_t* out, void* stream);
+
+/* contrast-integral-equation algebra, regularisers and filters (cie.py, losses.py:121-196,
+ * filters.py:16-53), context-free, complex128 / float64 device arrays.  Elementwise maps use the
+ * reference's float64 operation order (numpy's Smith division, no FMA contraction).
+ *   pdf_chi_to_r        y = beta x / (beta x + 1) (inverse = 0) or x / (beta (1 - x)) (inverse = 1);
+ *                       *poles (device int32) = pixels whose denominator is below 1e-14 in modulus
+ *                       (the caller raises PoleError)
+ *   pdf_default_eps_reg *eps (device) = 1e-10 max_v ||E_v||^2 / n_pix over e [n_views][n_pix]
+ *   pdf_pixel_ls        per pixel: num = sum_v J_v conj(E_v), den = sum_v |E_v|^2 + *eps, chi = num / den,
+ *                       degenerate = den <= 10 *eps (each output may be NULL)
+ *   pdf_cie_fields      per view v: E = e_in[v * e_view_stride] (+ gdj[v] when not NULL), P = E + beta J,
+ *                       res = r_hat P - beta J (r_hat [n_pix] shared); each output may be NULL
+ *   pdf_masked_residual out = (a - b) * mask (mask float64, may be NULL)
+ *   pdf_regularizers    values [count][3] = (bound, tv, bridge) sums; unweighted contrast gradients
+ *                       g_bound / g_tv / g_bridge and g_total = l1 g_bound + l2 g_tv + l3 g_bridge
+ *                       (terms with a zero weight skipped); every output may be NULL
+ *   pdf_box_mean        (2r+1)^2 window means, edge-replicated, count images of m1 x m2 (radius >= 1)
+ *   pdf_guided_filter   guided_filter(inp, guide, r, eps_gf) per image; scratch = 2 count m1 m2 doubles
+ *   pdf_cco_image       apply_cco per complex image (self-guided filter of Re and Im, sigmoid gain);
+ *                       scratch = 4 count m1 m2 doubles */
+int pdf_chi_to_r(const void* x, void* y, int64_t n, double beta_re, double beta_im, int32_t inverse, int32_t* poles,
+                 void* stream);
+int pdf_default_eps_reg(const void* e, int32_t n_views, int64_t n_pix, double* eps, void* stream);
+int pdf_pixel_ls(const void* j, const void* e, int32_t n_views, int64_t n_pix, const double* eps, void* num,
+                 double* den, void* chi, uint8_t* degenerate, void* stream);
+int pdf_cie_fields(const void* j, const void* gdj, const void* e_in, int64_t e_view_stride, const void* r_hat,
+                   double beta_re, double beta_im, int32_t n_views, int64_t n_pix, void* e_out, void* p_out,
+                   void* res_out, void* stream);
+int pdf_masked_residual(const void* a, const void* b, const double* mask, void* out, int64_t n, void* stream);
+int pdf_regularizers(const void* chi, int32_t m1, int32_t m2, int32_t count, double tau_b, double eps_tv, double l1,
+                     double l2, double l3, double* values, void* g_bound, void* g_tv, void* g_bridge, void* g_total,
+                     void* stream);
+int pdf_box_mean(const double* img, double* out, int32_t m1, int32_t m2, int32_t radius, int32_t count, void* stream);
+int pdf_guided_filter(const double* inp, const double* guide, double* out, int32_t m1, int32_t m2, int32_t radius,
+                      double eps_gf, int32_t count, double* scratch, void* stream);
+int pdf_cco_image(const void* chi, void* out, int32_t m1, int32_t m2, int32_t count, double tau, double eta_max,
+                  double delta, int32_t radius, double eps_gf, double* scratch, void* stream);
 
 /* copies the per-scene sticky error words to host (synchronises stream), then clears them */
 int pdf_get_error(pdf_ctx* ctx, int32_t* err_host, void* stream);

@@ -23,11 +23,29 @@ _API = ("LossBreakdown", "LossContext", "PipelineState", "SpectralBasis", "Netwo
         "loss_total", "init_network", "forward_net", "flatten_params", "unflatten_params", "grad_loss",
         "adam_step", "bp_initialize", "init_alpha", "recover_contrast", "apply_cco", "reconstruct",
         "relative_error", "count_components", "PoleError", "ZeroDataError", "PhysicsLoss", "truncate", "expand",
-        "truncate_adjoint_scale", "apply_gd", "apply_gd_adjoint", "apply_gs_adjoint")
+        "truncate_adjoint_scale", "apply_gd", "apply_gd_adjoint", "apply_gs_adjoint", "ContrastRecovery")
+
+
+_CIE = ("chi_to_r", "r_to_chi", "default_eps_reg", "pixel_least_squares", "cie_state_residual")
+_FILTERS = ("box_mean", "guided_filter")
+_LOSSES = ("loss_data", "loss_state", "loss_bound", "loss_tv", "loss_bridge", "bound_chi_grad", "tv_chi_grad",
+           "bridge_chi_grad", "regularizer_chi_grad")
 
 
 def __getattr__(name):
     # the GPU API imports torch lazily so the setup modules stay light
+    if name in _CIE:
+        from . import cie
+        return getattr(cie, name)
+    if name in _FILTERS:
+        from . import filters
+        return getattr(filters, name)
+    if name in _LOSSES:
+        from . import losses
+        return getattr(losses, name)
+    if name == "CsiObjective":
+        from .reconstruct import CsiObjective
+        return CsiObjective
     if name in _API:
         from . import api
         return getattr(api, name)

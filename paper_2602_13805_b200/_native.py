@@ -37,7 +37,9 @@ EXPORTS = (
     "pdf_net_setup_sharded", "pdf_shard_buffer_sizes", "pdf_shard_step_a", "pdf_shard_step_b", "pdf_shard_step_c",
     "pdf_relative_error", "pdf_count_components", "pdf_solver_workspace_bytes", "pdf_solve_total_field",
     "pdf_bessel", "pdf_build_greens", "pdf_incident_fields", "pdf_shard_step_c_part", "pdf_net_offsets",
-    "pdf_adam_step_dev", "pdf_shard_step_c_scatter", "pdf_adam_gather",
+    "pdf_adam_step_dev", "pdf_shard_step_c_scatter", "pdf_adam_gather", "pdf_chi_to_r", "pdf_default_eps_reg",
+    "pdf_pixel_ls", "pdf_cie_fields", "pdf_masked_residual", "pdf_regularizers", "pdf_box_mean", "pdf_guided_filter",
+    "pdf_cco_image",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
 
@@ -118,6 +120,17 @@ def lib():
                                              ct.POINTER(i32), vp]),
         "pdf_relative_error": (ct.c_int, [vp, vp, i32, i64, i32, ct.c_double, vp, vp]),
         "pdf_count_components": (ct.c_int, [vp, i32, i32, i32, i32, ct.c_double, ct.c_double, vp, vp, vp]),
+        "pdf_chi_to_r": (ct.c_int, [vp, vp, i64, ct.c_double, ct.c_double, i32, vp, vp]),
+        "pdf_default_eps_reg": (ct.c_int, [vp, i32, i64, vp, vp]),
+        "pdf_pixel_ls": (ct.c_int, [vp, vp, i32, i64, vp, vp, vp, vp, vp, vp]),
+        "pdf_cie_fields": (ct.c_int, [vp, vp, vp, i64, vp, ct.c_double, ct.c_double, i32, i64, vp, vp, vp, vp]),
+        "pdf_masked_residual": (ct.c_int, [vp, vp, vp, vp, i64, vp]),
+        "pdf_regularizers": (ct.c_int, [vp, i32, i32, i32, ct.c_double, ct.c_double, ct.c_double, ct.c_double,
+                                        ct.c_double, vp, vp, vp, vp, vp, vp]),
+        "pdf_box_mean": (ct.c_int, [vp, vp, i32, i32, i32, i32, vp]),
+        "pdf_guided_filter": (ct.c_int, [vp, vp, vp, i32, i32, i32, ct.c_double, i32, vp, vp]),
+        "pdf_cco_image": (ct.c_int, [vp, vp, i32, i32, i32, ct.c_double, ct.c_double, ct.c_double, i32, ct.c_double,
+                                     vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)      # AttributeError names the missing symbol

@@ -32,6 +32,9 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import cie as _cie
+from .cie import ContrastRecovery
+from .filters import apply_cco  # noqa: F401  (filters.py:56-67, pdf_cco_image)
 from .config import CcoParams, ImagingConfig
 from .engine import DeviceProblem, check_config_supported
 from .errors import PoleError, ZeroDataError  # noqa: F401  (re-exported)
@@ -239,18 +242,6 @@ class LossContext:
 
 
 @dataclass
-class ContrastRecovery:
-    """recover_contrast with its reusable intermediates (cie.py:53-63)."""
-    chi: np.ndarray           # (m1, m2)
-    j_views: np.ndarray       # (n, m1, m2) currents expand(alpha)
-    e_views: np.ndarray       # (n, m1, m2) total fields E_inc + G_D J
-    numerator: np.ndarray     # (m1, m2) sum_i J_i conj(E_i)
-    denominator: np.ndarray   # (m1, m2) real, sum_i |E_i|^2 + eps_reg
-    eps_reg: float
-    degenerate: np.ndarray    # (m1, m2) bool, denominator <= 10 eps_reg
-
-
-@dataclass
 class PipelineState:
     """Intermediates of one composite-loss evaluation (losses.py:200-212), same fields.
 
@@ -276,16 +267,15 @@ def _cdev(x, dev: DeviceProblem):
 
 def _recovery_dev(dev: DeviceProblem, alpha_d: torch.Tensor, eps_reg: float | None = None):
     """(J, E, num, den, eps, chi) of cie.py:66-99 on the device for one scene's views
-    (alpha_d: (n, m0)), from the library's expand and G_D primitives."""
+    (alpha_d: (n, m0)): the library's expand and G_D, then pdf_cie_fields,
+    pdf_default_eps_reg and pdf_pixel_ls."""
     j = dev.expand(alpha_d)
     einc = dev.e_inc if dev.e_inc.dim() == 3 else dev.e_inc[0]
-    e = einc + dev.apply_gd(j)
-    pw = torch.sum((e.conj() * e).real, dim=(-1, -2))
-    eps = (1e-10 * pw.max() / (dev.M * dev.M)) if eps_reg is None else torch.tensor(float(eps_reg),
-                                                                                     dtype=dev.rdt, device=dev.device)
-    num = torch.sum(j * e.conj(), dim=0)
-    den = torch.sum((e.conj() * e).real, dim=0) + eps
-    return j, e, num, den, eps, num / den
+    (e,) = _cie.cie_fields_dev(j, einc, gdj=dev.apply_gd(j), want=("e",))
+    eps = _cie.default_eps_reg_dev(e) if eps_reg is None else torch.tensor(float(eps_reg), dtype=dev.rdt,
+                                                                            device=dev.device)
+    num, den, chi, _ = _cie.pixel_ls_dev(j, e, eps)
+    return j, e, num, den, eps, chi
 
 
 def _recovery_host(j, e, num, den, eps, chi) -> ContrastRecovery:
@@ -306,12 +296,9 @@ def pipeline_forward(alpha_hat: np.ndarray, ctx: LossContext) -> PipelineState:
     dev.check_errors()           # PoleError / FloatingPointError (named terms) as the reference raises them
     j, e, num, den, eps, chi = _recovery_dev(dev, a[0])
     beta = ctx.beta
-    r_hat = dev.r_fixed[0] if dev.r_fixed is not None else beta * chi / (beta * chi + 1.0)
-    p = e + beta * j
-    sres = r_hat * p - beta * j
-    dres = dev.gs_forward(j) - dev.data[0]
-    if dev.mask is not None:
-        dres = dres * dev.mask[0]
+    r_hat = dev.r_fixed[0] if dev.r_fixed is not None else _cie.chi_to_r_dev(chi, beta)
+    p, sres = _cie.cie_fields_dev(j, e, beta, r_hat=r_hat, want=("p", "res"))
+    dres = _cie.masked_residual_dev(dev.gs_forward(j), dev.data[0], None if dev.mask is None else dev.mask[0])
     return PipelineState(alpha_hat=alpha_hat, rec=_recovery_host(j, e, num, den, eps, chi),
                          r_hat=r_hat.cpu().numpy(), p_views=p.cpu().numpy(), state_res=sres.cpu().numpy(),
                          data_res=dres.cpu().numpy(),
@@ -899,25 +886,3 @@ def recover_contrast(alpha, e_inc, ops: GreensOperators, basis: SpectralBasis, e
     return _recovery_host(*parts) if full else parts[-1].cpu().numpy()
 
 
-def apply_cco(chi: np.ndarray, params: CcoParams) -> np.ndarray:
-    """Contrast-compensated operator (filters.py:56-67) on the GPU."""
-    from .engine import GRID_SIZES
-    chi = np.asarray(chi, dtype=np.complex128)
-    M = chi.shape[0]
-    if chi.ndim != 2 or chi.shape != (M, M) or M not in GRID_SIZES:
-        raise ValueError(f"apply_cco on the GPU needs a square image with edge in {GRID_SIZES}, got {chi.shape}")
-    dev = _cco_device(M)
-    out = dev.apply_cco(_cdev(chi[None], dev), params)
-    return out[0].cpu().numpy()
-
-
-_CCO_DEVS: dict = {}
-
-
-def _cco_device(M: int) -> DeviceProblem:
-    if M not in _CCO_DEVS:
-        cfg = ImagingConfig(m1=M, m2=M, m_f=1, n_tx=1, n_rx=1).validate()
-        ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
-        _CCO_DEVS[M] = DeviceProblem(ops, np.ones((1, M, M), complex), np.ones((1, 1), complex), mf=1, beta=6.0,
-                                     lambdas=(0, 0, 0), tau_b=0.5)
-    return _CCO_DEVS[M]

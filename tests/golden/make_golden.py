@@ -462,6 +462,64 @@ def make_cfg4more():
     make_cfg4(n_scenes=8, first=2)
 
 
+def make_algebra():
+    """Module-level CIE algebra, regularisers and filters (cie.py, losses.py:86-196,
+    filters.py) on odd shapes, and the state / data terms on the tiny setup."""
+    from pdfisp import cie, filters, losses
+    from pdfisp.config import CcoParams
+    rng = np.random.default_rng(41)
+    out = {}
+    chi = rng.uniform(0.0, 9.0, (40, 40)) + 1j * rng.uniform(0.0, 2.0, (40, 40))
+    chi[3, 4] = 0.0
+    out.update(ctr_chi=chi, ctr_r=cie.chi_to_r(chi, 6.0), ctr_back=cie.r_to_chi(cie.chi_to_r(chi, 6.0), 6.0),
+               ctr_rc=cie.chi_to_r(chi, 6.0 + 1.5j), ctr_rc_back=cie.r_to_chi(cie.chi_to_r(chi, 6.0 + 1.5j), 6.0 + 1.5j))
+    j = rng.standard_normal((5, 12, 20)) + 1j * rng.standard_normal((5, 12, 20))
+    e = rng.standard_normal((5, 12, 20)) + 1j * rng.standard_normal((5, 12, 20))
+    e[:, 2, 7] = 0.0
+    rec = cie.pixel_least_squares(j, e)
+    out.update(pls_j=j, pls_e=e, pls_chi=rec.chi, pls_num=rec.numerator, pls_den=rec.denominator,
+               pls_eps=np.array(rec.eps_reg), pls_deg=rec.degenerate, pls_eps_default=np.array(cie.default_eps_reg(e)))
+    rec2 = cie.pixel_least_squares(j, e, eps_reg=0.25)
+    out.update(pls2_chi=rec2.chi, pls2_den=rec2.denominator, pls2_deg=rec2.degenerate)
+    rc = rng.standard_normal((20, 28)) + 1j * rng.standard_normal((20, 28))
+    rc[5, 5] = 0.0
+    rc[6:9, 10:14] = 1.7 + 0.2j          # a flat bright patch for the bridge term
+    lam = (1e-3, 1e-5, 1e-5)
+    out.update(reg_chi=rc, reg_bound=np.array(losses.loss_bound(rc)), reg_tv=np.array(losses.loss_tv(rc)),
+               reg_bridge=np.array(losses.loss_bridge(rc, 0.5)), reg_gb=losses.bound_chi_grad(rc),
+               reg_gt=losses.tv_chi_grad(rc), reg_gr=losses.bridge_chi_grad(rc, 0.5),
+               reg_g=losses.regularizer_chi_grad(rc, lam, 0.5), reg_g_l2=losses.regularizer_chi_grad(rc, (0, 1, 0), 0.5))
+    for k, (shape, r) in enumerate([((7, 9), 1), ((12, 5), 2), ((6, 6), 4), ((64, 48), 2)]):
+        img = rng.standard_normal(shape)
+        out[f"box{k}_img"], out[f"box{k}_r"], out[f"box{k}_out"] = img, np.array(r), filters.box_mean(img, r)
+    gi, gg = rng.standard_normal((10, 11)), rng.standard_normal((10, 11))
+    out.update(gf_inp=gi, gf_guide=gg, gf_out=filters.guided_filter(gi, gg, 2, 1e-3))
+    cc = 0.05 * (rng.standard_normal((12, 12)) + 1j * rng.standard_normal((12, 12)))
+    plateau = np.zeros((16, 16), dtype=complex)
+    plateau[4:12, 4:12] = 7.0
+    big = rng.uniform(0, 4, (30, 50)) + 1j * rng.uniform(0, 1, (30, 50))
+    p = CcoParams(tau=3.0, eta_max=0.1, delta=0.5, gf_radius=2, gf_eps=1e-3)
+    out.update(cco_small=cc, cco_small_out=filters.apply_cco(cc, p), cco_plateau_out=filters.apply_cco(plateau, p),
+               cco_big=big, cco_big_out=filters.apply_cco(big, CcoParams()))
+    # state / data terms on the tiny setup (reference tests/conftest.py:43-57)
+    cfg = ImagingConfig(m1=16, m2=16, m_f=3, n_tx=8, n_rx=8).validate()
+    grid, arr = build_grid(cfg), build_array(cfg)
+    ops = build_greens(cfg, arr, grid)
+    e_inc = incident_fields(cfg, arr, grid)
+    basis = SpectralBasis(16, 16, 3)
+    alpha = rng.standard_normal((8, basis.m0)) + 1j * rng.standard_normal((8, basis.m0))
+    r_hat = cie.chi_to_r(0.3 * (rng.random((16, 16)) + 1j * rng.random((16, 16))), 6.0)
+    mat = rng.standard_normal((8, 8)) + 1j * rng.standard_normal((8, 8))
+    mask = rng.random((8, 8)) > 0.3
+    data = ScatteredData(matrix=mat * mask, mask=mask)
+    out.update(st_alpha=alpha, st_rhat=r_hat,
+               st_res=cie.cie_state_residual(alpha, r_hat, e_inc.views, ops, basis, 6.0),
+               st_loss=np.array(losses.loss_state(alpha, r_hat, e_inc.views, ops, basis, 6.0)),
+               dt_mat=mat, dt_mask=mask, dt_loss=np.array(losses.loss_data(alpha, data, ops, basis)),
+               dt_loss_plain=np.array(losses.loss_data(alpha, ScatteredData(matrix=mat), ops, basis)))
+    save("algebra", **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["tiny", "cfg1", "cfg2", "cfg3", "cfg4"]
     for w in which:

@@ -157,3 +157,23 @@ def test_metrics_match_reference():
         assert O.count_components(g[f"extra{k}"] + 1.0, thr) == want, k
     for k, want in enumerate(g["rels"]):
         assert abs(O.relative_error(g["rel_a"][k].real + 1.0, g["rel_b"][k].real + 1.0) - want) < 1e-15
+
+
+# ------------------------------------------------------------------ regularisers and filters (losses.py:115-196,
+# filters.py:16-67) on odd shapes, golden algebra.npz
+def test_oracle_regularisers_and_filters_match_reference():
+    from conftest import golden
+    g = golden("algebra")
+    c = g["reg_chi"]
+    b, t, r = O.reg_values(c, 0.5)
+    assert abs(b - g["reg_bound"]) <= 1e-14 * abs(g["reg_bound"])
+    assert abs(t - g["reg_tv"]) <= 1e-13 * abs(g["reg_tv"])
+    assert abs(r - g["reg_bridge"]) <= 1e-13 * abs(g["reg_bridge"])
+    assert rel(O.reg_grad(c, (1e-3, 1e-5, 1e-5), 0.5), g["reg_g"]) < 1e-13
+    assert rel(O.reg_grad(c, (0, 1, 0), 0.5), g["reg_gt"]) < 1e-13
+    assert rel(O.reg_grad(c, (0, 0, 1), 0.5), g["reg_gr"]) < 1e-13
+    for k in range(4):
+        assert rel(O.box_mean(g[f"box{k}_img"], int(g[f"box{k}_r"])), g[f"box{k}_out"]) < 1e-14
+    assert rel(O.guided(g["gf_inp"], g["gf_guide"], 2, 1e-3), g["gf_out"]) < 1e-13
+    assert rel(O.cco(g["cco_small"]), g["cco_small_out"]) < 1e-13
+    assert rel(O.cco(g["cco_big"]), g["cco_big_out"]) < 1e-13
