@@ -23,6 +23,8 @@
  *   pdf_truncate        truncate                        spectral.py:56-65
  *   pdf_apply_cco       apply_cco                       filters.py:56-67
  *   pdf_shard_step_a/b/c(_part)  one incidence-sharded iteration  losses.py:215-306, network.py:183-223
+ *   pdf_net_layer_fwd/bwd, pdf_shard_tp_a/c  the same iteration with a    network.py:107-120, 183-223
+ *                       tensor-parallel network (weight slices per rank)
  *                       (views split over ranks, caller all-reduces between the steps)
  *   pdf_bessel          bessel_j0/j1/y0/y1, hankel1_*   special.py:64-106
  *   pdf_build_greens    build_greens                    forward.py:101-137
@@ -213,6 +215,34 @@ int pdf_shard_step_c_scatter(pdf_ctx* ctx, const void* theta, const double* red2
                              void* stream);
 int pdf_adam_gather(pdf_ctx* ctx, const double* recv, double* const* thetas, double* m, double* v, int32_t world,
                     int32_t rank, int64_t shard, const int32_t* t_dev, void* stream);
+
+/* tensor-parallel network for the incidence-sharded scene (SURVEY 8(e)'s alternative to the gradient
+ * exchange; sharded.TensorParallelTrainer), float64, one scene per context.  Layer L on this rank
+ * holds a slice of W_L ([N][K] row-major, out x in) in the caller's flat parameter vector `theta`:
+ * W1 / W3 output rows (column-parallel), W2 input columns (row-parallel).  The context supplies the
+ * row count (its views; a network context holds all views of the scene) and scratch.
+ *   pdf_net_features   copies the context's network input x0 [rows][D0] and output gains cout [D0]
+ *   pdf_net_layer_fwd  out[r][n] = f(sum_k in[r][k] W[n][k]), W = theta + w_off, b = theta + b_off:
+ *                      mode 0 f = tanh(z + b), 2 f = z + b, 3 f = z (b unused)
+ *   pdf_net_layer_bwd  grad[w_off + n K + k] = sum_r gz[r][n] hin[r][k]; grad[b_off + n] = sum_r gz[r][n];
+ *                      gin[r][k] = (sum_n gz[r][n] W[n][k]) (1 - hin[r][k]^2) when gin is not NULL
+ *   pdf_bias_tanh      x[r][n] = tanh(x[r][n] + bias[n]) in place (after the row-parallel all-reduce)
+ *   pdf_shard_tp_a     step a of the sharded iteration with the network output read from the
+ *                      column-block buffer Y[w][rows_all][N_w] (block w = output columns
+ *                      [w blk, w blk + N_w), N_w = min(blk, D0 - w blk)); this context's views are rows
+ *                      row0 .. row0 + n - 1 of the scene
+ *   pdf_shard_tp_c     step c without the network: writes this context's rows of the gradient with
+ *                      respect to the network output into the same block layout GY (other rows untouched) */
+int pdf_net_features(const pdf_ctx* ctx, void* x0, void* cout, void* stream);
+int pdf_net_layer_fwd(pdf_ctx* ctx, const void* in, int32_t K, int32_t N, const void* theta, int64_t w_off,
+                      int64_t b_off, void* out, int32_t mode, void* stream);
+int pdf_net_layer_bwd(pdf_ctx* ctx, const void* gz, const void* hin, int32_t K, int32_t N, const void* theta,
+                      int64_t w_off, int64_t b_off, void* grad, void* gin, void* stream);
+int pdf_bias_tanh(void* x, const void* bias, int64_t rows, int32_t n, void* stream);
+int pdf_shard_tp_a(pdf_ctx* ctx, const void* Y, int32_t blk, int32_t rows_all, int32_t row0, double* red1,
+                   void* stream);
+int pdf_shard_tp_c(pdf_ctx* ctx, const double* red2, void* GY, int32_t blk, int32_t rows_all, int32_t row0,
+                   double* breakdown, void* stream);
 /* pdf_adam_step with the step t read from device memory (*t_dev, >= 1): capturable in a CUDA graph;
  * also flags a nonfinite gradient (network.py:221-222) */
 int pdf_adam_step_dev(pdf_ctx* ctx, void* theta, void* m, void* v, const void* grad, int64_t count,

@@ -39,7 +39,8 @@ EXPORTS = (
     "pdf_bessel", "pdf_build_greens", "pdf_incident_fields", "pdf_shard_step_c_part", "pdf_net_offsets",
     "pdf_adam_step_dev", "pdf_shard_step_c_scatter", "pdf_adam_gather", "pdf_chi_to_r", "pdf_default_eps_reg",
     "pdf_pixel_ls", "pdf_cie_fields", "pdf_masked_residual", "pdf_regularizers", "pdf_box_mean", "pdf_guided_filter",
-    "pdf_cco_image",
+    "pdf_cco_image", "pdf_net_features", "pdf_net_layer_fwd", "pdf_net_layer_bwd", "pdf_bias_tanh",
+    "pdf_shard_tp_a", "pdf_shard_tp_c",
 )
 PHASES = ("fwd_l1", "fwd_l2", "fwd_l3", "view_fwd", "pixel", "view_bwd", "finalize", "bwd_l3", "bwd_l2", "bwd_l1")
 
@@ -129,6 +130,12 @@ def lib():
                                         ct.c_double, vp, vp, vp, vp, vp, vp]),
         "pdf_box_mean": (ct.c_int, [vp, vp, i32, i32, i32, i32, vp]),
         "pdf_guided_filter": (ct.c_int, [vp, vp, vp, i32, i32, i32, ct.c_double, i32, vp, vp]),
+        "pdf_net_features": (ct.c_int, [vp, vp, vp, vp]),
+        "pdf_net_layer_fwd": (ct.c_int, [vp, vp, i32, i32, vp, i64, i64, vp, i32, vp]),
+        "pdf_net_layer_bwd": (ct.c_int, [vp, vp, vp, i32, i32, vp, i64, i64, vp, vp, vp]),
+        "pdf_bias_tanh": (ct.c_int, [vp, vp, i64, i32, vp]),
+        "pdf_shard_tp_a": (ct.c_int, [vp, vp, i32, i32, i32, vp, vp]),
+        "pdf_shard_tp_c": (ct.c_int, [vp, vp, vp, i32, i32, i32, vp, vp]),
         "pdf_cco_image": (ct.c_int, [vp, vp, i32, i32, i32, ct.c_double, ct.c_double, ct.c_double, i32, ct.c_double,
                                      vp, vp]),
     }

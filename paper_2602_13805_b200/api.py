@@ -413,6 +413,20 @@ def _net_device(n: int, m_f: int, joint: bool) -> DeviceProblem:
     return _NET_DEVS[key]
 
 
+def _net_device_lr(n: int, m_f: int, lr: float) -> DeviceProblem:
+    """As _net_device (non-joint), with the learning rate its Adam applies."""
+    key = (n, m_f, False, float(lr))
+    if key not in _NET_DEVS:
+        M = 16
+        while M < 2 * m_f:
+            M *= 2
+        cfg = ImagingConfig(m1=M, m2=M, m_f=m_f, n_tx=n, n_rx=1).validate()
+        ops = build_greens(cfg, build_array(cfg), build_grid(cfg))
+        _NET_DEVS[key] = DeviceProblem(ops, np.ones((n, M, M), complex), np.ones((n, 1), complex), mf=m_f,
+                                       beta=cfg.beta, lambdas=(0, 0, 0), tau_b=0.5, lr=float(lr))
+    return _NET_DEVS[key]
+
+
 def _theta(params: NetworkParams, dev: DeviceProblem) -> torch.Tensor:
     return torch.as_tensor(flatten_params(params), dtype=dev.rdt, device=dev.device)[None].contiguous()
 

@@ -1711,6 +1711,140 @@ extern "C" int pdf_shard_step_c_scatter(pdf_ctx* c, const void* theta, const dou
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// tensor-parallel network (SURVEY 8(e)'s alternative to the gradient exchange;
+// sharded.TensorParallelTrainer): the layers run on weight slices held in the
+// caller's flat parameter vector, the physics of this context's views takes the
+// network output from / gives its gradient to a column-block buffer
+// Y[w][rows_all][N_w] (block w = output columns [w blk, w blk + N_w)).
+
+namespace {
+
+__device__ __forceinline__ long long tp_index(int col, int blk, int D0, int rows_all, int grow) {
+  const int w = col / blk, j = col - w * blk, nw = min(blk, D0 - w * blk);
+  return (long long)w * rows_all * blk + (long long)grow * nw + j;
+}
+
+template <typename T>
+__global__ void tp_merge_kernel(const T* __restrict__ Y, int blk, int rows_all, int row0, int n, int D0, int M0,
+                                const T* __restrict__ cout, const C<T>* __restrict__ alpha0,
+                                C<T>* __restrict__ alpha_hat) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * D0) return;
+  const int r = (int)(i / D0), col = (int)(i % D0);
+  const T yv = Y[tp_index(col, blk, D0, rows_all, row0 + r)] * cout[col];
+  const int half = D0 / 2, m = col < half ? col : col - half;
+  const size_t off = (size_t)r * M0 + m;
+  T* dst = reinterpret_cast<T*>(alpha_hat + off);
+  const T* src = reinterpret_cast<const T*>(alpha0 + off);
+  if (col < half) dst[0] = src[0] + yv; else dst[1] = src[1] + yv;
+}
+
+template <typename T>
+__global__ void tp_scatter_kernel(const T* __restrict__ gy, T* __restrict__ GY, int blk, int rows_all, int row0, int n,
+                                  int D0) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * D0) return;
+  const int r = (int)(i / D0), col = (int)(i % D0);
+  GY[tp_index(col, blk, D0, rows_all, row0 + r)] = gy[i];
+}
+
+__global__ void bias_tanh_kernel(double* __restrict__ x, const double* __restrict__ b, long long total, int n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) x[i] = tanh(x[i] + b[i % n]);
+}
+
+}  // namespace
+
+static bool tp_ok(const pdf_ctx* c, int blk, int rows_all, int row0) {
+  return c && c->d.S == 1 && !c->d.joint && c->d.dtype == PDF_F64 && blk >= 1 && blk <= c->D0 && row0 >= 0 &&
+         row0 + c->d.n <= rows_all;
+}
+
+extern "C" int pdf_net_features(const pdf_ctx* c, void* x0, void* cout, void* stream) {
+  if (!c || c->d.S != 1) return fail(PDF_EINVAL, "pdf_net_features: one-scene context required");
+  const size_t el = c->d.dtype == PDF_F64 ? sizeof(double) : sizeof(float);
+  if (x0) CK_CUDA(cudaMemcpyAsync(x0, c->x0, (size_t)c->rows * c->D0 * el, cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream));
+  if (cout) CK_CUDA(cudaMemcpyAsync(cout, c->cout, (size_t)c->D0 * el, cudaMemcpyDeviceToDevice,
+                                    (cudaStream_t)stream));
+  return PDF_OK;
+}
+
+extern "C" int pdf_net_layer_fwd(pdf_ctx* c, const void* in, int32_t K, int32_t N, const void* theta, int64_t w_off,
+                                 int64_t b_off, void* out, int32_t mode, void* stream) {
+  if (!c || !in || !theta || !out || K < 2 || N < 2 || (K & 1) || (N & 1) || c->d.S != 1 ||
+      c->d.dtype != PDF_F64 || !(mode == 0 || mode == 2 || mode == 3) || (mode != 3 && b_off < 0) ||
+      !env_int("PDF_NET_MMA", 1))
+    return fail(PDF_EINVAL, "pdf_net_layer_fwd: bad arguments (float64, even widths, mode 0/2/3)");
+  NetFwdArgs<double> a = {};
+  a.rows = c->rows; a.K = K; a.N = N;
+  a.in = (const double*)in; a.in_ss = (long long)c->rows * K;
+  a.theta = (const double*)theta; a.th_ss = 0; a.w_off = w_off; a.b_off = mode == 3 ? 0 : b_off;
+  a.out = (double*)out; a.out_ss = (long long)c->rows * N; a.final_layer = mode;
+  a.w_early = 0;   // the slice may have been written by the launch right before
+  return fwd_mma_layer(c, a, (cudaStream_t)stream);
+}
+
+extern "C" int pdf_net_layer_bwd(pdf_ctx* c, const void* gz, const void* hin, int32_t K, int32_t N,
+                                 const void* theta, int64_t w_off, int64_t b_off, void* grad, void* gin,
+                                 void* stream) {
+  if (!c || !gz || !hin || !theta || !grad || K < 2 || N < 2 || (K & 1) || (N & 1) || b_off < 0 || c->d.S != 1 ||
+      c->d.dtype != PDF_F64 || !env_int("PDF_NET_MMA", 1))
+    return fail(PDF_EINVAL, "pdf_net_layer_bwd: bad arguments (float64, even widths)");
+  double* const* const peers = c->sc_peers;
+  c->sc_peers = nullptr;
+  const int r = net_bwd_layer<double>(c, (const double*)gz, (const double*)hin, K, N,
+                                      const_cast<double*>((const double*)theta), w_off, b_off, nullptr, nullptr,
+                                      (double*)grad, 0, (double*)gin, (cudaStream_t)stream);
+  c->sc_peers = peers;
+  return r;
+}
+
+extern "C" int pdf_bias_tanh(void* x, const void* bias, int64_t rows, int32_t n, void* stream) {
+  if (!x || !bias || rows < 1 || n < 1) return fail(PDF_EINVAL, "pdf_bias_tanh: bad arguments");
+  const long long tot = rows * n;
+  bias_tanh_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>((double*)x, (const double*)bias,
+                                                                                   tot, n);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
+}
+
+extern "C" int pdf_shard_tp_a(pdf_ctx* c, const void* Y, int32_t blk, int32_t rows_all, int32_t row0, double* red1,
+                              void* stream) {
+  if (!tp_ok(c, blk, rows_all, row0) || !Y || !red1) return fail(PDF_EINVAL, "pdf_shard_tp_a: bad arguments");
+  const cudaStream_t st = (cudaStream_t)stream;
+  const long long tot = (long long)c->d.n * c->D0;
+  tp_merge_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+      (const double*)Y, blk, rows_all, row0, c->d.n, c->D0, c->M0, (const double*)c->cout,
+      (const C<double>*)c->alpha0, (C<double>*)c->alpha_hat);
+  CK_CUDA(cudaGetLastError());
+  TRY(phys_forward<double>(c, c->alpha_hat, st));
+  ShardArgs<double> a = shard_args<double>(c, red1, nullptr);
+  const int img = c->M * c->M;
+  void* args[] = {&a};
+  CK_CUDA(plain_launch(shard_numden_kernel<double>, dim3((img + 255) / 256, 1), dim3(256), 0, st, args));
+  return PDF_OK;
+}
+
+extern "C" int pdf_shard_tp_c(pdf_ctx* c, const double* red2, void* GY, int32_t blk, int32_t rows_all, int32_t row0,
+                              double* breakdown, void* stream) {
+  if (!tp_ok(c, blk, rows_all, row0) || !red2 || !GY) return fail(PDF_EINVAL, "pdf_shard_tp_c: bad arguments");
+  const cudaStream_t st = (cudaStream_t)stream;
+  ShardArgs<double> a = shard_args<double>(c, nullptr, const_cast<double*>(red2));
+  void* args[] = {&a};
+  CK_CUDA(plain_launch(shard_pixel_b_kernel<double>, dim3(c->M / c->TX, c->M, 1), dim3(PIX_NW * 32), 0, st, args));
+  TRY(phys_backward<double>(c, nullptr, c->gy, st));
+  FinalizeArgs f = fin_args(c, breakdown, nullptr);
+  shard_finalize_kernel<<<1, 128, 0, st>>>(f, red2, (size_t)c->M * c->M);
+  CK_CUDA(cudaGetLastError());
+  const long long tot = (long long)c->d.n * c->D0;
+  tp_scatter_kernel<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>((const double*)c->gy, (double*)GY, blk,
+                                                                           rows_all, row0, c->d.n, c->D0);
+  CK_CUDA(cudaGetLastError());
+  return PDF_OK;
+}
+
 extern "C" int pdf_adam_gather(pdf_ctx* c, const double* recv, double* const* thetas, double* m, double* v,
                                int32_t world, int32_t rank, int64_t shard, const int32_t* t_dev, void* stream) {
   if (!c || !recv || !thetas || !m || !v || !t_dev || world < 1 || rank < 0 || rank >= world || shard < 1 ||

@@ -37,7 +37,8 @@ struct NetFwdArgs {
   const T* theta; long long th_ss;    // [S][Np]
   long long w_off, b_off;
   T* out; long long out_ss;           // [S][rows][N]   (tanh layers)
-  int final_layer;
+  int final_layer;                    // 0 tanh(z + b); 1 final: alpha_hat = alpha0 + merge((z + b) * cout);
+                                      // 2 z + b; 3 z (float64 DMMA kernels; tensor-parallel slices)
   // final layer: alpha_hat = alpha0 + merge(y * cout)
   const T* cout;                      // [S][N]
   const C<T>* alpha0;                 // [S][n][M0]

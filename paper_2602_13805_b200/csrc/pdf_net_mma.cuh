@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
       for (int c = 0; c < 2; ++c) part[(warp * NT * 8 + 8 * j + 2 * t + c) * RPM + 8 * i + g] = acc[i][j][c];
   cluster.sync();
 
-  const double* bias = a.theta + scene * a.th_ss + a.b_off;
+  const double* bias = a.theta + scene * a.th_ss + (a.final_layer == 3 ? 0 : a.b_off);
   const int total = FM_WARPS * NT * 8 * RPM;
   for (int e = rank * 256 + tid; e < total; e += CK * 256) {
     const int wo = e / RPM, r = e % RPM;
@@ -150,9 +150,9 @@ __global__ void __launch_bounds__(256) net_fwd_mma_kernel(NetFwdArgs<double> a) 
     double z = 0.0;
 #pragma unroll 8
     for (int c = 0; c < CK; ++c) z += cluster.map_shared_rank(part, c)[e];
-    z += bias[gn];
-    if (!a.final_layer) {
-      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+    if (a.final_layer != 3) z += bias[gn];
+    if (a.final_layer != 1) {
+      a.out[scene * a.out_ss + (size_t)r * N + gn] = a.final_layer ? z : tanh(z);
     } else {
       const double yv = z * a.cout[(size_t)scene * N + gn];
       const int half = N / 2;
@@ -278,16 +278,16 @@ __global__ void __launch_bounds__(XW * 32, 1) net_fwd_x_kernel(NetFwdArgs<double
 #pragma unroll
     for (int c = 0; c < 2; ++c) red[(warp * RPM + 8 * i + g) * 8 + 2 * t + c] = acc[i][c];
   __syncthreads();
-  const double* bias = a.theta + scene * a.th_ss + a.b_off;
+  const double* bias = a.theta + scene * a.th_ss + (a.final_layer == 3 ? 0 : a.b_off);
   for (int e = tid; e < RPM * 8; e += THR) {
     const int r = e >> 3, col = e & 7, gn = n0 + col;
     if (gn >= N || r >= rows) continue;
     double z = 0.0;
 #pragma unroll
     for (int w = 0; w < XW; ++w) z += red[(w * RPM + r) * 8 + col];
-    z += bias[gn];
-    if (!a.final_layer) {
-      a.out[scene * a.out_ss + (size_t)r * N + gn] = tanh(z);
+    if (a.final_layer != 3) z += bias[gn];
+    if (a.final_layer != 1) {
+      a.out[scene * a.out_ss + (size_t)r * N + gn] = a.final_layer ? z : tanh(z);
     } else {
       const double yv = z * a.cout[(size_t)scene * N + gn];
       const int half = N / 2;

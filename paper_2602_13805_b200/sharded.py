@@ -458,3 +458,284 @@ class PeerTrainer:
     def check_errors(self):
         for s in self.shards:
             s.dev.check_errors()
+
+
+# ---------------------------------------------------------------------------- tensor-parallel network
+def tp_split(total: int, world: int) -> tuple[int, list[tuple[int, int]]]:
+    """Block size and (start, size) of every rank's slice of `total` units:
+    blocks of ceil(total / world) rounded up to even (16-byte rows), the last
+    one shorter.  Raises when a rank would get nothing."""
+    blk = -(-total // world)
+    blk += blk & 1
+    parts = [(min(r * blk, total), min((r + 1) * blk, total) - min(r * blk, total)) for r in range(world)]
+    if any(n <= 0 for _, n in parts):
+        raise ValueError(f"{world} ranks leave some rank without a slice of {total} units")
+    return blk, parts
+
+
+def tp_full_offsets(H: int, D0: int) -> list[int]:
+    """Offsets of W1, b1, W2, b2, W3, b3 and the end in the flat parameter vector
+    (network.py:158-166 order; W_L stored [out][in])."""
+    o = [0, H * D0]
+    o.append(o[-1] + H)
+    o.append(o[-1] + H * H)
+    o.append(o[-1] + H)
+    o.append(o[-1] + D0 * H)
+    o.append(o[-1] + D0)
+    return o
+
+
+def tp_local_offsets(H: int, D0: int, hr: int, dr: int) -> list[int]:
+    """Offsets of one rank's W1 rows [hr][D0], b1 slice, W2 columns [H][hr], b2 [H],
+    W3 rows [dr][H], b3 slice, and the end."""
+    o = [0, hr * D0]
+    o.append(o[-1] + hr)
+    o.append(o[-1] + H * hr)
+    o.append(o[-1] + H)
+    o.append(o[-1] + dr * H)
+    o.append(o[-1] + dr)
+    return o
+
+
+def tp_local_params(th: torch.Tensor, H: int, D0: int, hpart, dpart) -> torch.Tensor:
+    """One rank's parameters in the local layout, cut from the full flat vector."""
+    (h0, hr), (c0, dr) = hpart, dpart
+    f = tp_full_offsets(H, D0)
+    W1, W2, W3 = th[f[0]:f[1]].view(H, D0), th[f[2]:f[3]].view(H, H), th[f[4]:f[5]].view(D0, H)
+    return torch.cat([W1[h0:h0 + hr].reshape(-1), th[f[1] + h0:f[1] + h0 + hr], W2[:, h0:h0 + hr].reshape(-1),
+                      th[f[3]:f[4]], W3[c0:c0 + dr].reshape(-1), th[f[5] + c0:f[5] + c0 + dr]])
+
+
+def tp_assemble(locals_, H: int, D0: int, hparts, dparts) -> torch.Tensor:
+    """The full flat vector from every rank's local vector (b2 taken from rank 0)."""
+    f = tp_full_offsets(H, D0)
+    th = torch.zeros(f[6], dtype=locals_[0].dtype, device=locals_[0].device)
+    W1, W2, W3 = th[f[0]:f[1]].view(H, D0), th[f[2]:f[3]].view(H, H), th[f[4]:f[5]].view(D0, H)
+    for r in reversed(range(len(locals_))):
+        (h0, hr), (c0, dr), p = hparts[r], dparts[r], locals_[r]
+        lo = tp_local_offsets(H, D0, hr, dr)
+        W1[h0:h0 + hr] = p[lo[0]:lo[1]].view(hr, D0)
+        th[f[1] + h0:f[1] + h0 + hr] = p[lo[1]:lo[2]]
+        W2[:, h0:h0 + hr] = p[lo[2]:lo[3]].view(H, hr)
+        th[f[3]:f[4]] = p[lo[3]:lo[4]]
+        W3[c0:c0 + dr] = p[lo[4]:lo[5]].view(dr, H)
+        th[f[5] + c0:f[5] + c0 + dr] = p[lo[5]:lo[6]]
+    return th
+
+
+def tp_to_blocks(y: torch.Tensor, blk: int, world: int) -> torch.Tensor:
+    """(rows, D0) -> the column-block layout Y[w][rows][N_w] (flat, world * rows * blk
+    entries) that pdf_shard_tp_a reads and pdf_shard_tp_c writes."""
+    rows, D0 = y.shape
+    out = torch.zeros(world * rows * blk, dtype=y.dtype, device=y.device)
+    for w in range(world):
+        c0 = w * blk
+        nw = min(blk, D0 - c0)
+        if nw > 0:
+            out[w * rows * blk:w * rows * blk + rows * nw] = y[:, c0:c0 + nw].reshape(-1)
+    return out
+
+
+def tp_from_blocks(Y: torch.Tensor, rows: int, D0: int, blk: int) -> torch.Tensor:
+    """Inverse of tp_to_blocks."""
+    y = torch.empty(rows, D0, dtype=Y.dtype, device=Y.device)
+    for w in range(-(-D0 // blk)):
+        c0 = w * blk
+        nw = min(blk, D0 - c0)
+        y[:, c0:c0 + nw] = Y[w * rows * blk:w * rows * blk + rows * nw].view(rows, nw)
+    return y
+
+
+class TensorParallelTrainer:
+    """Incidence sharding with a tensor-parallel network (SURVEY 8(e)'s
+    alternative to exchanging the network gradient).
+
+    The widths are [D0, H, H, D0] (network.py:61; W_L stored [out][in]).  Rank
+    r holds rows h_r of W1 / b1 (column-parallel), columns h_r of W2 with all
+    of b2 (row-parallel), rows d_r of W3 / b3, and their Adam state: 1/W of
+    the parameters, updated locally.  One iteration, for all views of the
+    scene on every rank's network slice and its own views' physics:
+
+      h1_r = tanh(x0 W1_r^T + b1_r)           local
+      z2   = sum_r h1_r W2_r^T                all-reduce (rows x H)
+      h2   = tanh(z2 + b2)                    local (replicated)
+      Y_r  = h2 W3_r^T + b3_r                 all-reduce of the column blocks (rows x D0)
+      physics of own views (tp_a, red1, step_b, red2, tp_c) -> the gradient rows of Y
+      GY                                       all-reduce of the row blocks (rows x D0)
+      g_W3_r, g_b3_r; g_z2 = sum_r (GY_r W3_r)(1 - h2^2)   all-reduce (rows x H)
+      g_W2_r, g_b2, g_z1_r = (g_z2 W2_r)(1 - h1_r^2)       local
+      g_W1_r, g_b1_r                                        local
+      Adam on this rank's slices
+
+    Per iteration and rank the collectives move 2 (rows x H) + 2 (rows x D0)
+    doubles plus the physics' red1 / red2 (at config 5: 2.4 + 2.4 + 1.2 + 1.2
+    MB + 2.6 MB), instead of the 268 MB gradient reduce-scatter and the 268 MB
+    parameter all-gather of the ZeRO-1 forms; weights, Adam state and network
+    FLOPs are 1/W per rank.  All network arithmetic runs in the library's DMMA
+    layer kernels (pdf_net_layer_fwd / _bwd).
+
+    `shards` are all ranks of one process emulated on one GPU (a list of
+    IncidenceShard over all views, `group=None`: the collectives become
+    rank-order sums; no kernel waits for another) or this rank's single shard
+    with a torch.distributed `group` (NCCL)."""
+
+    def __init__(self, shards, theta0: torch.Tensor, group=None, graph: bool = False, graph_iters: int = 10,
+                 lr: float = 1e-2):
+        from .api import _net_device_lr
+        self.shards = list(shards)
+        self.group = group
+        self.graph_on, self.G, self.graph = graph, max(1, int(graph_iters)), None
+        s0 = self.shards[0]
+        if s0.dev.rdt != torch.float64:
+            raise ValueError("the tensor-parallel network is float64")
+        if group is None:
+            self.world, self.ranks = len(self.shards), list(range(len(self.shards)))
+        else:
+            import torch.distributed as dist
+            self.world, self.ranks = dist.get_world_size(group), [dist.get_rank(group)]
+            if len(self.shards) != 1:
+                raise ValueError("one shard per process on a multi-GPU node")
+        W = self.world
+        self.rows = s0.n_all
+        # a geometry-free context that runs the network kernels over all views of the scene
+        self.net = _net_device_lr(self.rows, s0.dev.mf, lr)
+        lib, nc = self.net.lib, self.net.ctx
+        self.lib = lib
+        rows, d0, hid, np_ = ct.c_int32(), ct.c_int32(), ct.c_int32(), ct.c_int64()
+        N.check(lib.pdf_net_dims(nc, ct.byref(rows), ct.byref(d0), ct.byref(hid), ct.byref(np_)))
+        self.D0, self.H, self.np = d0.value, hid.value, np_.value
+        if theta0.numel() != self.np:
+            raise ValueError("theta0 does not match the network of this scene")
+        dd = s0.dev.device
+        N.check(lib.pdf_net_setup(nc, _ptr(s0.alpha0_all), _stream()))
+        self.x0 = torch.empty(self.rows, self.D0, dtype=torch.float64, device=dd)
+        N.check(lib.pdf_net_features(nc, _ptr(self.x0), None, _stream()))
+        self.hblk, self.hparts = tp_split(self.H, W)
+        self.dblk, self.dparts = tp_split(self.D0, W)
+        th = theta0.detach().to(dd, torch.float64).reshape(-1)
+        self.st = [self._rank_state(th, r, dd) for r in self.ranks]
+        self.t_dev = torch.zeros(1, dtype=torch.int32, device=dd)
+
+    # ------------------------------------------------------------------ layout
+    def _rank_state(self, th, r, dd):
+        hr, dr = self.hparts[r][1], self.dparts[r][1]
+        p = tp_local_params(th, self.H, self.D0, self.hparts[r], self.dparts[r]).contiguous()
+        z = lambda *shape: torch.zeros(*shape, dtype=torch.float64, device=dd)   # noqa: E731
+        W, R = self.world, self.rows
+        return {"r": r, "hr": hr, "dr": dr, "off": tp_local_offsets(self.H, self.D0, hr, dr), "theta": p,
+                "m": z(p.numel()), "v": z(p.numel()), "grad": z(p.numel()), "h1": z(R, hr), "z2": z(R, self.H),
+                "Y": z(W * R * self.dblk), "GY": z(W * R * self.dblk), "gz2": z(R, self.H), "gz1": z(R, hr)}
+
+    def params(self) -> torch.Tensor:
+        """The full flat parameter vector (emulated ranks: assembled from every rank's slices)."""
+        if self.group is not None:
+            raise NotImplementedError("assemble with an all-gather on a multi-GPU node")
+        return tp_assemble([s["theta"] for s in self.st], self.H, self.D0, self.hparts, self.dparts)
+
+    # ------------------------------------------------------------------ collectives
+    def _sum(self, key):
+        """All-reduce (SUM) of every rank's buffer `key`."""
+        if self.group is None:
+            t = self.st[0][key].clone()
+            for s in self.st[1:]:
+                t += s[key]
+            for s in self.st:
+                s[key].copy_(t)
+        else:
+            import torch.distributed as dist
+            dist.all_reduce(self.st[0][key], op=dist.ReduceOp.SUM, group=self.group)
+
+    def _reduce_phys(self, what):
+        if self.group is None:
+            LocalShards()(self.shards, what)
+        else:
+            TorchDistReducer(self.group)(self.shards, what)
+
+    # ------------------------------------------------------------------ one iteration
+    def _fwd(self, s, inp, K, Nn, w, b, out, mode):
+        N.check(self.lib.pdf_net_layer_fwd(self.net.ctx, _ptr(inp), K, Nn, _ptr(s["theta"]), w, b, _ptr(out), mode,
+                                           _stream()))
+
+    def _bwd(self, s, gz, hin, K, Nn, w, b, gin):
+        N.check(self.lib.pdf_net_layer_bwd(self.net.ctx, _ptr(gz), _ptr(hin), K, Nn, _ptr(s["theta"]), w, b,
+                                           _ptr(s["grad"]), None if gin is None else _ptr(gin), _stream()))
+
+    def iteration(self, trace_row: torch.Tensor | None = None):
+        R, H, D0 = self.rows, self.H, self.D0
+        for s in self.st:
+            o = s["off"]
+            self._fwd(s, self.x0, D0, s["hr"], o[0], o[1], s["h1"], 0)
+            self._fwd(s, s["h1"], s["hr"], H, o[2], -1, s["z2"], 3)
+        self._sum("z2")
+        for s in self.st:
+            o = s["off"]
+            N.check(self.lib.pdf_bias_tanh(_ptr(s["z2"]), _ptr(s["theta"][o[3]:]), R, H, _stream()))   # z2 -> h2
+            s["Y"].zero_()
+            yb = s["Y"][s["r"] * R * self.dblk:]
+            self._fwd(s, s["z2"], H, s["dr"], o[4], o[5], yb, 2)
+        self._sum("Y")
+        for sh, s in zip(self.shards, self.st):
+            N.check(self.lib.pdf_shard_tp_a(sh.dev.ctx, _ptr(s["Y"]), self.dblk, R, sh.own.start, _ptr(sh.red1),
+                                            _stream()))
+        self._reduce_phys("red1")
+        for sh in self.shards:
+            sh.step_b()
+        self._reduce_phys("red2")
+        for sh, s in zip(self.shards, self.st):
+            s["GY"].zero_()
+            N.check(self.lib.pdf_shard_tp_c(sh.dev.ctx, _ptr(sh.red2), _ptr(s["GY"]), self.dblk, R, sh.own.start,
+                                            _ptr(sh.bd), _stream()))
+        if trace_row is not None:
+            trace_row.copy_(self.shards[0].bd[0])
+        self._sum("GY")
+        for s in self.st:
+            o = s["off"]
+            gy = s["GY"][s["r"] * R * self.dblk:]
+            self._bwd(s, gy, s["z2"], H, s["dr"], o[4], o[5], s["gz2"])
+        self._sum("gz2")
+        self.t_dev += 1
+        for s in self.st:
+            o = s["off"]
+            self._bwd(s, s["gz2"], s["h1"], s["hr"], H, o[2], o[3], s["gz1"])
+            self._bwd(s, s["gz1"], self.x0, D0, s["hr"], o[0], o[1], None)
+            N.check(self.lib.pdf_adam_step_dev(self.net.ctx, _ptr(s["theta"]), _ptr(s["m"]), _ptr(s["v"]),
+                                               _ptr(s["grad"]), s["theta"].numel(), _ptr(self.t_dev), _stream()))
+
+    def _state(self):
+        return [x for s in self.st for x in (s["theta"], s["m"], s["v"])] + [self.t_dev]
+
+    def train(self, k: int) -> torch.Tensor:
+        """k iterations (graph=True: replayed from a CUDA graph of graph_iters iterations
+        holding the library kernels and the collectives); returns the trace [k][6]."""
+        dd = self.x0.device
+        trace = torch.zeros(k, 6, dtype=torch.float64, device=dd)
+        done = 0
+        if self.graph_on and k >= self.G:
+            if self.graph is None:
+                saved = [x.clone() for x in self._state()]
+                for _ in range(2):                 # warm the collectives outside the capture
+                    self.iteration()
+                torch.cuda.synchronize()
+                for x, y in zip(self._state(), saved):
+                    x.copy_(y)
+                self.gtrace = torch.zeros(self.G, 6, dtype=torch.float64, device=dd)
+                st = torch.cuda.Stream(device=dd)
+                st.wait_stream(torch.cuda.current_stream())
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for i in range(self.G):
+                        self.iteration(self.gtrace[i])
+                self.graph = g
+            while done + self.G <= k:
+                self.graph.replay()
+                trace[done:done + self.G].copy_(self.gtrace)
+                done += self.G
+        while done < k:
+            self.iteration(trace[done])
+            done += 1
+        return trace
+
+    def check_errors(self):
+        for s in self.shards:
+            s.dev.check_errors()
+        self.net.check_errors()

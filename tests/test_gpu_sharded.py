@@ -120,3 +120,59 @@ def test_peer_scatter_symmetric_memory_single_rank():
         if own:
             dist.destroy_process_group()
     np.testing.assert_allclose(trace, np.array([b.as_row() for b in ref.trace]), rtol=1e-9)
+
+
+@pytest.mark.parametrize("cfg_id,world,graph", [(1, 2, False), (1, 3, False), (3, 2, False), (1, 2, True)])
+def test_tensor_parallel_emulated_ranks(cfg_id, world, graph):
+    """Tensor-parallel network (W1 / W3 rows, W2 columns per rank; SURVEY 8(e)'s
+    alternative) with incidence-sharded physics, `world` ranks emulated in one
+    process on one GPU: the iteration trace matches the unsharded run and the
+    assembled parameters match the one-rank tensor-parallel run."""
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, TensorParallelTrainer
+    g = golden(f"cfg{cfg_id}")
+    st = Setup(cfg_baseline(cfg_id), plane=True)
+    cfg = st.cfg
+    k = 12
+    ref = BatchReconstructor(cfg, 1, e_inc=st.e_inc).run([g["data"]], seeds=[cfg.rng_seed], k_iters=k)[0]
+    theta0 = torch.as_tensor(_theta0([cfg.rng_seed], 4 * cfg.m_f ** 2), device="cuda")
+
+    def run(w):
+        shards = [IncidenceShard(st.ops, st.e_inc, g["data"], mf=cfg.m_f, beta=cfg.beta, lambdas=LAM,
+                                 tau_b=cfg.tau_b, rank=r, world=w) for r in range(w)]
+        tr = TensorParallelTrainer(shards, theta0, graph=graph, graph_iters=4, lr=cfg.learn_rate)
+        trace = tr.train(k).cpu().numpy()
+        tr.check_errors()
+        return trace, tr.params()
+
+    trace, params = run(world)
+    np.testing.assert_allclose(trace, np.array([b.as_row() for b in ref.trace]), rtol=1e-9)
+    _, params1 = run(1)
+    assert float(torch.max(torch.abs(params - params1))) < 1e-9 * float(torch.max(torch.abs(params1)))
+
+
+def test_tensor_parallel_single_rank_nccl():
+    """The torch.distributed form (NCCL all-reduces, CUDA-graph captured) on a one-rank group."""
+    import torch.distributed as dist
+    from paper_2602_13805_b200.api import BatchReconstructor, _theta0
+    from paper_2602_13805_b200.sharded import IncidenceShard, TensorParallelTrainer
+    g = golden("cfg1")
+    st = Setup(cfg_baseline(1), plane=True)
+    cfg = st.cfg
+    k = 8
+    ref = BatchReconstructor(cfg, 1, e_inc=st.e_inc).run([g["data"]], seeds=[cfg.rng_seed], k_iters=k)[0]
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        sh = IncidenceShard(st.ops, st.e_inc, g["data"], mf=cfg.m_f, beta=cfg.beta, lambdas=LAM, tau_b=cfg.tau_b,
+                            rank=0, world=1)
+        theta0 = torch.as_tensor(_theta0([cfg.rng_seed], 4 * cfg.m_f ** 2), device="cuda")
+        tr = TensorParallelTrainer([sh], theta0, group=dist.group.WORLD, graph=True, graph_iters=4, lr=cfg.learn_rate)
+        trace = tr.train(k).cpu().numpy()
+        tr.check_errors()
+    finally:
+        if own:
+            dist.destroy_process_group()
+    np.testing.assert_allclose(trace, np.array([b.as_row() for b in ref.trace]), rtol=1e-9)

@@ -398,3 +398,85 @@ def test_resolve_scene_specs(tmp_path):
         scene_from_dict({"shapes": [{"kind": "blob", "eps_r": 2}]})
     with pytest.raises(SceneError):
         resolve_scene("nosuch:2")
+
+
+_TP = r'''
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch, torch.distributed as dist
+from paper_2602_13805_b200.sharded import (tp_split, tp_local_params, tp_assemble, tp_full_offsets,
+                                           tp_local_offsets, tp_to_blocks, tp_from_blocks)
+from paper_2602_13805_b200.shard import shard_range
+dist.init_process_group("gloo")
+r, W = dist.get_rank(), dist.get_world_size()
+torch.manual_seed(0)
+rows, D0, H = 9, 10, 22                      # D0, H split unevenly over 2 ranks (blocks 6 + 4, 12 + 10)
+f = tp_full_offsets(H, D0)
+th = torch.randn(f[6], dtype=torch.float64) * 0.3
+x0 = torch.randn(rows, D0, dtype=torch.float64)
+t = torch.randn(rows, D0, dtype=torch.float64)
+# full network + loss 0.5 ||y - t||^2, autograd
+p = th.clone().requires_grad_(True)
+W1, b1 = p[f[0]:f[1]].view(H, D0), p[f[1]:f[2]]
+W2, b2 = p[f[2]:f[3]].view(H, H), p[f[3]:f[4]]
+W3, b3 = p[f[4]:f[5]].view(D0, H), p[f[5]:f[6]]
+y_ref = torch.tanh(torch.tanh(x0 @ W1.T + b1) @ W2.T + b2) @ W3.T + b3
+(0.5 * ((y_ref - t) ** 2).sum()).backward()
+# tensor-parallel: this rank's slices, the collectives of TensorParallelTrainer.iteration
+hb, hp = tp_split(H, W)
+db, dp = tp_split(D0, W)
+(h0, hr), (c0, dr) = hp[r], dp[r]
+lo = tp_local_offsets(H, D0, hr, dr)
+q = tp_local_params(th, H, D0, hp[r], dp[r])
+W1r, b1r = q[lo[0]:lo[1]].view(hr, D0), q[lo[1]:lo[2]]
+W2r, b2_ = q[lo[2]:lo[3]].view(H, hr), q[lo[3]:lo[4]]
+W3r, b3r = q[lo[4]:lo[5]].view(dr, H), q[lo[5]:lo[6]]
+h1r = torch.tanh(x0 @ W1r.T + b1r)
+z2 = h1r @ W2r.T
+dist.all_reduce(z2)
+h2 = torch.tanh(z2 + b2_)
+Y = torch.zeros(W * rows * db, dtype=torch.float64)
+Y[r * rows * db:r * rows * db + rows * dr] = (h2 @ W3r.T + b3r).reshape(-1)
+dist.all_reduce(Y)
+y = tp_from_blocks(Y, rows, D0, db)
+assert torch.allclose(y, y_ref, rtol=1e-13, atol=1e-13), (y - y_ref).abs().max()
+own = shard_range(rows, r, W)                # the "physics" of own views gives their gradient rows
+gy_own = torch.zeros(rows, D0, dtype=torch.float64)
+gy_own[own.start:own.stop] = (y - t)[own.start:own.stop]
+GY = tp_to_blocks(gy_own, db, W)
+dist.all_reduce(GY)
+gyr = GY[r * rows * db:r * rows * db + rows * dr].view(rows, dr)
+g = torch.zeros_like(q)
+g[lo[4]:lo[5]] = (gyr.T @ h2).reshape(-1)
+g[lo[5]:lo[6]] = gyr.sum(0)
+gz2 = (gyr @ W3r) * (1 - h2 ** 2)
+dist.all_reduce(gz2)
+g[lo[2]:lo[3]] = (gz2.T @ h1r).reshape(-1)
+g[lo[3]:lo[4]] = gz2.sum(0)
+gz1 = (gz2 @ W2r) * (1 - h1r ** 2)
+g[lo[0]:lo[1]] = (gz1.T @ x0).reshape(-1)
+g[lo[1]:lo[2]] = gz1.sum(0)
+sizes = [tp_local_offsets(H, D0, hp[k][1], dp[k][1])[6] for k in range(W)]
+mx = max(sizes)                              # gloo gathers equal sizes: pad
+parts = [torch.zeros(mx, dtype=torch.float64) for _ in sizes]
+dist.all_gather(parts, torch.cat([g, torch.zeros(mx - g.numel(), dtype=torch.float64)]))
+gfull = tp_assemble([pp[:n] for pp, n in zip(parts, sizes)], H, D0, hp, dp)
+err = float((gfull - p.grad).abs().max() / p.grad.abs().max())
+assert err < 1e-13, err
+if r == 0:
+    print("OK", err)
+'''
+
+
+def test_tensor_parallel_network_algebra_with_gloo(tmp_path):
+    """The tensor-parallel decomposition TensorParallelTrainer runs (slices,
+    column-block layout, the four all-reduces) reproduces the full network's
+    output and parameter gradient with two gloo ranks."""
+    script = tmp_path / "tp.py"
+    script.write_text(_TP)
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT="29533")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", str(script), ROOT]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=240)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "OK" in out.stdout
