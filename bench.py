@@ -464,12 +464,13 @@ def leg_rooflines(dev, theta0, fp64, hbm, notes, args) -> dict:
 def large_leg(args, d: Dist, fp64, hbm, notes):
     """BASELINE config 5: one 256x256 scene, 72 incidences / receivers, m_f = 16.
     N = 1: the whole scene on one GPU (CUDA-graph replay).  N > 1: incidences
-    sharded over the ranks, three NCCL allreduces per iteration (sharded.py)."""
+    sharded over the ranks (sharded.py), timed in three forms (peer-scatter,
+    zero1-nccl, tensor-parallel); the fastest is the headline."""
     import torch
     from paper_2602_13805_b200 import build_grid, plane_wave_fields
     from paper_2602_13805_b200.api import BatchReconstructor, _theta0
-    from paper_2602_13805_b200.sharded import (IncidenceShard, PeerTrainer, ShardedTrainer, TorchDistReducer,
-                                               run_sharded)
+    from paper_2602_13805_b200.sharded import (IncidenceShard, PeerTrainer, ShardedTrainer, TensorParallelTrainer,
+                                               TorchDistReducer, run_sharded)
     from paper_2602_13805_b200.workloads import baseline_config, baseline_scene, synthesize_gpu
     k = args.large_iters
     cfg = baseline_config(5, k_iters=k)
@@ -516,17 +517,21 @@ def large_leg(args, d: Dist, fp64, hbm, notes):
             err = f"{type(ex).__name__}: {ex}"
         if d.max(1.0 if err else 0.0) > 0:
             raise RuntimeError(err or "incidence-shard setup failed on another rank")
-        # two multi-GPU forms, each timed over the same k iterations (CUDA-graph replay):
+        # three multi-GPU forms, each timed over the same k iterations (CUDA-graph replay):
         #   peer-scatter: the gradient reduce-scatter fused into the backward kernels (g_W / g_b
         #     stored by the DMMA epilogue into the owner rank's symmetric-memory receive buffer over
         #     NVLink), owner-side Adam with the parameter all-gather as peer stores
         #   zero1-nccl: per-layer reduce-scatter (NCCL) on a comm stream overlapping the next
         #     layer's backward, sharded Adam, NCCL all-gather
+        #   tensor-parallel: W1 / W3 rows and W2 columns per rank with their Adam state; four
+        #     activation-sized all-reduces instead of any gradient / parameter exchange
         # every rank takes the same branches (the collective sequences must match)
         import torch.distributed as tdist
         forms = {}
         makers = (("peer-scatter", lambda: PeerTrainer([sh], theta0, group=tdist.group.WORLD, graph=True)),
-                  ("zero1-nccl", lambda: ShardedTrainer(sh, theta0, graph=True)))
+                  ("zero1-nccl", lambda: ShardedTrainer(sh, theta0, graph=True)),
+                  ("tensor-parallel", lambda: TensorParallelTrainer([sh], theta0, group=tdist.group.WORLD, graph=True,
+                                                                    lr=c.learn_rate)))
         tr = None
         for name, make in makers:
             try:
