@@ -117,7 +117,41 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   C<T> x[E];
 #pragma unroll
   for (int k = 0; k < E; ++k) x[k] = czero<T>();
-  if constexpr (MODE == VIEW_FWD && sizeof(T) == 8) {
+  bool even_done = false;   // FWD split path: the even half of the padded spectrum is written with the expansion
+  if constexpr (MODE == VIEW_FWD && sizeof(T) == 8 && SPLIT) {
+    // J = expand(alpha) rows y0..y0+7 (spectral.py:68-79).  V = Tr A (the
+    // contraction over the row frequencies) is a small complex GEMM on the
+    // FP64 tensor cores; the contraction over the column frequencies is an
+    // inverse length-M FFT of the K nonzero coefficients, placed at the
+    // slots the warp FFT's permuted order assigns to their frequencies.
+    // Those same coefficients, times M, ARE the even half of the padded
+    // row's spectrum (F_M of the row), so only the odd half needs a forward
+    // transform below.
+    const C<T>* al = a.alpha + (size_t)v * M0;
+    for (int i = tid; i < M0; i += blockDim.x) A[i] = al[vl_corner_slot(i / K, i % K, mf)];
+    __syncthreads();
+    cgemm_dmma(VL_ROWS, K, K,
+               [&](int yl, int u) { return conj_<T>(twm[(vl_corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]); },
+               [&](int u, int w) { return A[u * K + w]; }, [&](int yl, int w, C<T> val) { V[yl * K + w] = val; });
+    __syncthreads();
+    const T inv = T(1) / (T(M) * T(M));
+    C<T> t[EH];
+#pragma unroll
+    for (int q = 0; q < EH; ++q) {
+      const int f = spectrum_slot_freq(lane, q, EH);
+      const int w = f < mf ? f : (f >= M - mf ? f - (M - 2 * mf) : -1);
+      t[q] = w >= 0 ? cscale<T>(V[warp * K + w], inv) : czero<T>();
+      tile[(q * 32 + lane) * TP + warp] = cscale<T>(t[q], T(M));
+    }
+    warp_fft_inv<T, EH>(t, ltwh, lane);
+    C<T>* jrow = a.J + (size_t)v * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < EH; ++k) {
+      x[k] = t[k];
+      jrow[lane + 32 * k] = t[k];
+    }
+    even_done = true;
+  } else if constexpr (MODE == VIEW_FWD && sizeof(T) == 8) {
     // J = expand(alpha) rows y0..y0+7 (spectral.py:68-79): V = Tr A, J = V T as
     // complex GEMMs on the FP64 tensor cores, J staged through `tile`
     const C<T>* al = a.alpha + (size_t)v * M0;
@@ -183,11 +217,13 @@ __global__ void __launch_bounds__(256) vl_rows_kernel(VLArgs<T> a) {
   if constexpr (SPLIT) {
     // zero padding: X[2m] = F_{P/2}(x)[m], X[2m+1] = F_{P/2}(x w^n)[m], w = exp(-2 pi i / P)
     C<T> t[EH];
+    if (!even_done) {
 #pragma unroll
-    for (int k = 0; k < EH; ++k) t[k] = x[k];
-    warp_fft_fwd<T, EH>(t, ltwh, lane);
+      for (int k = 0; k < EH; ++k) t[k] = x[k];
+      warp_fft_fwd<T, EH>(t, ltwh, lane);
 #pragma unroll
-    for (int q = 0; q < EH; ++q) tile[(q * 32 + lane) * TP + warp] = t[q];
+      for (int q = 0; q < EH; ++q) tile[(q * 32 + lane) * TP + warp] = t[q];
+    }
 #pragma unroll
     for (int k = 0; k < EH; ++k) t[k] = cmul<T>(x[k], tw[lane + 32 * k]);
     warp_fft_fwd<T, EH>(t, ltwh, lane);
@@ -301,8 +337,8 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   }
   __syncthreads();
   C<T> x[E];
+  LaneTw<T, (SPLIT ? E / 2 : 1)> lt;
   if constexpr (SPLIT) {
-    LaneTw<T, E / 2> lt;
     lt.load(twh, lane);
     C<T> t[EH];
 #pragma unroll
@@ -336,6 +372,27 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
     }
     const double tot = block_sum_d<T>(nrm, red);
     if (tid == 0) a.norms[(size_t)v * a.NPV + blockIdx.x] = tot;
+  } else if constexpr (MODE == VIEW_BWD && sizeof(T) == 8 && SPLIT) {
+    // g_J row = g_J_local + G_D^H g_E; the truncation's contraction over x
+    // (spectral.py:56-65), U[yl][w] = F_M(g_J row)[f_w], is one forward
+    // length-M FFT of the row (in registers) whose K corner frequencies are
+    // picked from the slots holding them; the contraction over the rows stays
+    // a small complex GEMM
+    C<T> t[EH];
+#pragma unroll
+    for (int k = 0; k < KH; ++k) t[k] = cadd<T>(a.gJloc[rowoff + lane + 32 * k], conj_<T>(x[k]));
+    warp_fft_fwd<T, EH>(t, lt, lane);
+#pragma unroll
+    for (int q = 0; q < EH; ++q) {
+      const int f = spectrum_slot_freq(lane, q, EH);
+      const int w = f < mf ? f : (f >= M - mf ? f - (M - 2 * mf) : -1);
+      if (w >= 0) U[warp * K + w] = t[q];
+    }
+    __syncthreads();
+    C<T>* gp = a.gpart + ((size_t)v * a.NPV + blockIdx.x) * M0;
+    cgemm_dmma(K, K, VL_ROWS,
+               [&](int u, int yl) { return twm[(vl_corner_freq<T>(u, mf, M) * (y0 + yl)) & (M - 1)]; },
+               [&](int yl, int w) { return U[yl * K + w]; }, [&](int u, int w, C<T> val) { gp[u * K + w] = val; });
   } else if constexpr (MODE == VIEW_BWD) {
     __syncthreads();                     // S is reused as the g_J rows
     C<T>* rows = S;

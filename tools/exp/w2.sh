@@ -1,0 +1,4 @@
+cd /root/repo
+NVTX="--nvtx --nvtx-include iters/" bash tools/ncu_box.sh r02w_full_cfg5_adam 'net_adam_x' 1 -- python tools/prof_step.py --cfg 5 --iters 1
+python tools/ncu_sum.py gpurun_out/r02w_full_cfg5_adam.raw.csv > gpurun_out/r02w_full_cfg5_adam_summary.txt
+tail -3 gpurun_out/r02w_full_cfg5_adam.log
