@@ -153,7 +153,7 @@ static void plan(pdf_ctx* c, Ws& w) {
   c->h2b = c->xbwd ? w.take<T>((size_t)d.S * c->rows * c->H) : nullptr;
   c->tsnap = c->xbwd ? w.take<int>(1) : nullptr;
   c->tsnap_b = c->xbwd ? w.take<int>(1) : nullptr;
-  c->gad = c->xbwd && !c->large ? w.take<C<T>>(SN * c->M0) : nullptr;
+  c->gad = c->xbwd ? w.take<C<T>>(SN * c->M0) : nullptr;
   c->red1 = c->split ? w.take<double>((size_t)d.S * (3 * img + 1)) : nullptr;
   c->red2 = c->split ? w.take<double>((size_t)d.S * (2 * img + 2)) : nullptr;
   c->dloss = w.take<double>(SN);
@@ -354,7 +354,7 @@ static cudaError_t vl_chunk(pdf_ctx* c, VLArgs<T>& a, int cnt, cudaStream_t st) 
   void* args[] = {&a};
   cudaError_t e = plain_launch(vl_rows_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256),
                                vl_rows_smem<T>(E, c->d.mf), st, args);
-  if (e == cudaSuccess) e = plain_launch(vl_cols_kernel<T, E>, dim3(P / 8, cnt), dim3(256), 0, st, args);
+  if (e == cudaSuccess) e = plain_launch(vl_cols_kernel<T, E>, dim3(P / 8, cnt), dim3(256), vl_cols_smem<T>(E), st, args);
   if (e == cudaSuccess)
     e = plain_launch(vl_out_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256), vl_out_smem<T>(E, c->d.mf), st,
                      args);
@@ -410,7 +410,7 @@ static int vl_forward(pdf_ctx* c, const void* alpha_hat, cudaStream_t st) {
   a.einc = (const C<T>*)c->d.e_inc; a.einc_scene_stride = c->d.e_inc_scene_stride;
   a.E = (C<T>*)c->E_; a.norms = c->norms;
   TRY((vl_conv<T, VIEW_FWD>(c, a, c->d.S * c->d.n, st)));
-  return data_term<T>(c, alpha_hat, st);
+  return c->skip_data ? PDF_OK : data_term<T>(c, alpha_hat, st);
 }
 
 template <typename T>
@@ -420,6 +420,7 @@ static int vl_backward(pdf_ctx* c, void* galpha, void* gy, cudaStream_t st, cons
   TRY((vl_conv<T, VIEW_BWD>(c, a, c->d.S * c->d.n, st)));
   a.galpha = (C<T>*)galpha; a.gy = (T*)gy; a.cout = (const T*)c->cout; a.joint = c->d.joint;
   a.grows = (const C<T>*)c->grows; a.hs = (const C<T>*)c->hs;
+  a.gad = c->gad_ready ? (const C<T>*)c->gad : nullptr;
   a.fin = fin; a.do_fin = do_fin ? 1 : 0;
   void* args[] = {&a};
   cudaError_t e = plain_launch(vl_trunc_reduce_kernel<T>, dim3((c->M0 + 255) / 256, c->d.S * c->d.n), dim3(256), 0,
@@ -990,7 +991,9 @@ static int iteration(pdf_ctx* c, void* theta, void* m, void* v, void* grad, doub
   mark();
   // side branch: the data term D = alpha H^T - d and its g_alpha part need only
   // alpha_hat; they overlap the view and pixel kernels of the main chain
-  const bool dfork = fork && c->dfork_ok && c->gad && run();
+  // (large-grid path, any row count: the same side branch beside the view passes)
+  const bool lfork = sizeof(T) == 8 && c->capturing && fused && c->large && c->side && c->gad && c->dgemm;
+  const bool dfork = ((fork && c->dfork_ok) || lfork) && c->gad && run();
   if (dfork) {
     CK_CUDA(cudaEventRecord(c->ev_vf, st));
     CK_CUDA(cudaStreamWaitEvent(c->side, c->ev_vf, 0));

@@ -61,6 +61,7 @@ struct VLArgs {
   int joint;
   const C<T>* grows;           // [S*n][R] data-residual gradient rows
   const C<T>* hs;              // [R][M0] spectral receiver operator (pdf_aux.cuh)
+  const C<T>* gad;             // [S*n][M0] data part of g_alpha (slot order, gad_kernel) or null: computed here
   FinalizeArgs fin;
   int do_fin;
   int tl;                      // timeline slot + 1 (0: off)
@@ -76,6 +77,12 @@ template <typename T>
 __host__ __device__ inline size_t vl_rows_smem(int E, int mf) {
   const int P = 32 * E, M = P / 2, K = 2 * mf;
   return ((size_t)P + P / 2 + M + (size_t)P * (VL_ROWS + 1) + (size_t)K * K + (size_t)VL_ROWS * K) * sizeof(C<T>);
+}
+
+// cols pass: the warps' kernel-spectrum columns (float64 split path)
+template <typename T>
+__host__ __device__ inline size_t vl_cols_smem(int E) {
+  return sizeof(T) == 8 && E >= 4 ? (size_t)8 * 32 * E * sizeof(C<T>) : 0;
 }
 
 template <typename T>
@@ -263,6 +270,16 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
     // y[n] = F^-1(K_e F(x))[n] + w^-n F^-1(K_o F(x w^n))[n] for the first P/2 outputs
     LaneTw<T, E / 2> lt;
     lt.load(twh, lane);
+    if constexpr (sizeof(T) == 8) {
+      // the column's kernel spectrum (constant) streams into shared memory while
+      // the previous pass drains; lane l copies exactly the entries it reads
+      extern __shared__ __align__(16) unsigned char smem_raw[];
+      C<T>* khs = reinterpret_cast<C<T>*>(smem_raw) + (size_t)warp * P;
+#pragma unroll
+      for (int q = 0; q < E; ++q) cp_async16(khs + q * 32 + lane, kh + q * 32 + lane, true);
+      cp_async_commit();
+      kh = khs;
+    }
     pdl_wait();
   tl_mark(a.tl, 1);
     C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
@@ -272,6 +289,7 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
 #pragma unroll
     for (int k = 0; k < EH; ++k) t[k] = xin[k];
     warp_fft_fwd<T, EH>(t, lt, lane);
+    if constexpr (sizeof(T) == 8) cp_async_wait<0>();
 #pragma unroll
     for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[q * 32 + lane]);
     warp_fft_inv<T, EH>(t, lt, lane);
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
 
 // ---------------------------------------------------------------------------
 template <typename T, int E, int MODE>
-__global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
+__global__ void __launch_bounds__(256, 2) vl_out_kernel(VLArgs<T> a) {
   tl_mark(a.tl, 0);
   TlExit tl_exit_{a.tl};
   constexpr int P = 32 * E, M = P / 2, KH = E / 2, SP = P + 1;
@@ -328,12 +346,31 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
   for (int i = tid; i < P; i += blockDim.x) tw[i] = a.twP[i];
   for (int i = tid; i < P / 2; i += blockDim.x) twh[i] = a.twP[2 * i];
   for (int i = tid; i < M; i += blockDim.x) twm[i] = a.twM[i];
+  // forward: the epilogue's second operand (E_inc, constant) is requested before the
+  // dependency wait (the adjoint's g_J local rows are read at their use: registers)
+  const size_t rowoff = (size_t)v * img + (size_t)y * M;
+  C<T> epi[KH];
+  if constexpr (MODE == VIEW_FWD) {
+    const C<T>* ei = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img + (size_t)y * M;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) epi[k] = ei[lane + 32 * k];
+  }
   pdl_wait();
   tl_mark(a.tl, 1);
   const C<T>* in = a.spec + (size_t)vr * P * M + y0;
-  for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
-    const int pos = i / VL_ROWS, yl = i % VL_ROWS;
-    S[yl * SP + pos] = in[(size_t)pos * M + yl];
+  if constexpr (sizeof(C<T>) == 16) {
+    // 8 consecutive rows of one spectrum position = 128 bytes: all pieces in flight at once
+    for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
+      const int pos = i / VL_ROWS, yl = i % VL_ROWS;
+      cp_async16(S + yl * SP + pos, in + (size_t)pos * M + yl, true);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else {
+    for (int i = tid; i < P * VL_ROWS; i += blockDim.x) {
+      const int pos = i / VL_ROWS, yl = i % VL_ROWS;
+      S[yl * SP + pos] = in[(size_t)pos * M + yl];
+    }
   }
   __syncthreads();
   C<T> x[E];
@@ -359,14 +396,12 @@ __global__ void __launch_bounds__(256) vl_out_kernel(VLArgs<T> a) {
     warp_fft_inv<T, E>(x, ltw, lane);
   }
   pdl_trigger();
-  const size_t rowoff = (size_t)v * img + (size_t)y * M;
   if constexpr (MODE == VIEW_FWD) {
     double nrm = 0.0;
-    const C<T>* ei = a.einc + (size_t)scene * a.einc_scene_stride + (size_t)view * img + (size_t)y * M;
 #pragma unroll
     for (int k = 0; k < KH; ++k) {
       const int col = lane + 32 * k;
-      const C<T> e = cadd<T>(ei[col], x[k]);
+      const C<T> e = cadd<T>(epi[k], x[k]);
       a.E[rowoff + col] = e;
       nrm += (double)cabs2<T>(e);
     }
@@ -465,7 +500,8 @@ __global__ void __launch_bounds__(256) vl_trunc_reduce_kernel(VLArgs<T> a) {
   acc = cscale<T>(acc, T(1) / (T(M) * T(M)));
   const int u = i / K, w = i % K;
   const int slot = vl_corner_slot(u, w, mf);
-  acc = cadd<T>(acc, data_adjoint_at<T>(a.grows + (size_t)v * a.R, a.hs, a.R, M0, slot, 0, 1));
+  acc = cadd<T>(acc, a.gad ? a.gad[(size_t)v * M0 + slot]
+                           : data_adjoint_at<T>(a.grows + (size_t)v * a.R, a.hs, a.R, M0, slot, 0, 1));
   if (a.galpha) a.galpha[(size_t)v * M0 + slot] = acc;
   if (a.gy) {
     const int D0 = 2 * M0 * (a.joint ? a.n : 1);
