@@ -583,6 +583,9 @@ static int fwd_mma_layer(pdf_ctx* c, NetFwdArgs<double>& a, cudaStream_t st) {
   const int kmax = (K + FM_KCH - 1) / FM_KCH;
   int CK = 1;
   while (CK < cap && 2 * CK <= kmax && base * CK < 2 * 148) CK *= 2;
+  // a grid that spills into a second, partly filled wave of 2 CTAs per SM is
+  // slower than half the split in one wave (cfg5, N = 4096: 512 CTAs 114 us, 256 CTAs 107 us)
+  if (CK > 1 && base * CK > 2 * 148 && base * CK / 2 >= (2 * 148 * 4) / 5) CK /= 2;
   a.ks = ((K + CK - 1) / CK + FM_KCH - 1) / FM_KCH * FM_KCH;
   const dim3 grid((N + 64 * NT - 1) / (64 * NT), CK, S);
   cudaError_t e;
@@ -845,6 +848,9 @@ static int gh_x_layer(pdf_ctx* c, const double* gz, const double* hin, int K, in
     const int kbs = (K + gt_kb(ktw) - 1) / gt_kb(ktw);
     int nsl = 1;
     while (nsl < GH_NSL && (long long)kbs * nsl * c->d.S < 2 * 148 && N / (2 * nsl) >= 2 * GT_NC) nsl *= 2;
+    if (nsl > 1 && (long long)kbs * nsl * c->d.S > 2 * 148 &&
+        (long long)kbs * nsl * c->d.S / 2 >= (2 * 148 * 4) / 5)
+      nsl /= 2;   // one full wave instead of a second, partly filled one (cfg5: g_h2 160 -> 142 us)
     g.nsl = nsl;
     g.ns = ((N + nsl - 1) / nsl + GT_NC - 1) / GT_NC * GT_NC;
     g.gz = gz; g.gz_ss = (long long)c->rows * N;
