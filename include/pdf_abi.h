@@ -129,10 +129,12 @@ int pdf_ctx_destroy(pdf_ctx* ctx);
 
 /* network geometry: rows, d0 (= input/output width), hidden, n_params per scene */
 int pdf_net_dims(const pdf_ctx* ctx, int32_t* rows, int32_t* d0, int32_t* hidden, int64_t* n_params);
-/* kernel paths chosen at create (bits): PDF_PATH_LARGE_GRID, PDF_PATH_DATA_GEMM, PDF_PATH_SPLIT_BWD */
+/* kernel paths chosen at create (bits): PDF_PATH_LARGE_GRID, PDF_PATH_DATA_GEMM, PDF_PATH_SPLIT_BWD;
+ * bits 8-11: CTAs per view of the cluster path (8 / 4: thread-block clusters, 1: one CTA per view) */
 #define PDF_PATH_LARGE_GRID 1
 #define PDF_PATH_DATA_GEMM 2
 #define PDF_PATH_SPLIT_BWD 4
+#define PDF_PATH_VIEW_CLUSTER_SHIFT 8
 int pdf_ctx_paths(const pdf_ctx* ctx, int32_t* paths);
 
 /* physics: alpha_hat [S][n][m0] -> g_alpha [S][n][m0] (NULL = skip), breakdown [S][6] f64

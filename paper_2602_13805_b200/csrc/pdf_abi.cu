@@ -184,8 +184,14 @@ static int derive(pdf_ctx* c, const pdf_desc* d) {
   // 8-CTA clusters while one wave holds every view (latency), 4 once the batch
   // fills the GPU (half the cluster barriers per unit of work; measured -22%
   // view time at 128 scenes)
-  c->CS = env_int("PDF_VIEW_CLUSTER", (long long)d->S * d->n * 8 <= 4 * 148 ? 8 : 4);
-  if (c->CS != 4 && c->CS != 8) return fail(PDF_EINVAL, "view cluster size must be 4 or 8");
+  // ... and one 16-warp CTA per view (no cluster, every transpose in the CTA's
+  // own shared memory) once there are several views per SM and the view's
+  // half-pruned spectrum fits (float64: M <= 64)
+  const long long nviews = (long long)d->S * d->n;
+  const bool solo_ok = d->dtype == PDF_F64 && c->M <= 64 && c->M >= 32;
+  c->CS = env_int("PDF_VIEW_CLUSTER", nviews * 8 <= 4 * 148 ? 8 : (solo_ok && nviews >= 4 * 148 ? 1 : 4));
+  if (c->CS != 4 && c->CS != 8 && !(c->CS == 1 && solo_ok))
+    return fail(PDF_EINVAL, "view cluster size must be 4 or 8 (or 1: float64, M <= 64)");
   c->rows = d->joint ? 1 : d->n;
   c->D0 = 2 * c->M0 * (d->joint ? d->n : 1);
   c->H = 2 * c->D0;
@@ -308,7 +314,7 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
   // registers, so under PDL they wait for the previous kernel to drain
   // (measured +8 us per view kernel at cfg2)
   static const int vt = env_int("PDF_VIEW_THREADS", 256);
-  const int nthr = std::min(vt, VIEW_MAX_THREADS);
+  const int nthr = c->CS == 1 ? VIEW_SOLO_THREADS : std::min(vt, VIEW_MAX_THREADS);
   dim3 grid(c->CS, count), block(nthr), cl(c->CS, 1, 1);
   switch (c->E * 100 + c->CS) {
 #define VCASE(EE, CC)                                               \
@@ -319,8 +325,9 @@ static int launch_view(pdf_ctx* c, ViewArgs<T>& a, int count, cudaStream_t st) {
     break;                                                          \
   }
     VCASE(1, 4) VCASE(1, 8) VCASE(2, 4) VCASE(2, 8) VCASE(4, 4) VCASE(4, 8) VCASE(8, 4) VCASE(8, 8)
+    VCASE(2, 1) VCASE(4, 1)
 #undef VCASE
-    default: return fail(PDF_EINVAL, "unsupported FFT size / view cluster size (4 or 8)");
+    default: return fail(PDF_EINVAL, "unsupported FFT size / view cluster size (1, 4 or 8)");
   }
   if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("view kernel: ") + cudaGetErrorString(e));
   return PDF_OK;
@@ -1173,7 +1180,7 @@ extern "C" int pdf_ctx_destroy(pdf_ctx* c) {
 extern "C" int pdf_ctx_paths(const pdf_ctx* c, int32_t* paths) {
   if (!c || !paths) return fail(PDF_EINVAL, "null argument");
   *paths = (c->large ? PDF_PATH_LARGE_GRID : 0) | (c->dgemm ? PDF_PATH_DATA_GEMM : 0) |
-           (c->xbwd ? PDF_PATH_SPLIT_BWD : 0);
+           (c->xbwd ? PDF_PATH_SPLIT_BWD : 0) | (c->large ? 0 : c->CS << PDF_PATH_VIEW_CLUSTER_SHIFT);
   return PDF_OK;
 }
 

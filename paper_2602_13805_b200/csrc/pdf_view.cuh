@@ -70,6 +70,7 @@ struct ViewArgs {
 };
 
 constexpr int VIEW_MAX_THREADS = 256;
+constexpr int VIEW_SOLO_THREADS = 512;   // CS = 1: one 16-warp CTA per view
 
 template <typename T>
 struct ViewSmem {
@@ -97,8 +98,11 @@ __host__ __device__ inline size_t view_smem_bytes(int M, int mf, int R, int CS) 
   // K^ columns and the E_inc / g_J-local rows; 4-CTA clusters (batches) keep
   // two CTAs per SM and read them from L2 in place
   const size_t stage = CS == 8 ? (size_t)(P / CS) * P + (size_t)rp * M : 0;
-  size_t pre = stage + (size_t)32 * (VIEW_MAX_THREADS / 32) + (size_t)M0 / CS + 1;
-  size_t n = (size_t)P + M + (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M + a + pre + xch;
+  size_t pre = stage + (size_t)32 * (VIEW_SOLO_THREADS / 32) + (size_t)M0 / CS + 1;
+  // CS = 1 (one CTA per view, batches): both transpose buffers and the row buffer
+  // are the same M x (P + 1) array (every stage works in place, row or column wise)
+  const size_t bufs = CS == 1 ? (size_t)M * (P + 1) : (size_t)M * (P / CS + 1) + (size_t)rp * (P + 1) + (size_t)rp * M;
+  size_t n = (size_t)P + M + bufs + a + pre + xch;
   return n * sizeof(C<T>) + 64 * sizeof(double);
 }
 
@@ -122,7 +126,7 @@ __device__ inline double block_sum_d(double v, double* red) {
 }
 
 template <typename T, int E, int MODE, int CSZ>
-__global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
+__global__ void __launch_bounds__(CSZ == 1 ? VIEW_SOLO_THREADS : VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int P = 32 * E;
   cg::cluster_group cluster = cg::this_cluster();
@@ -145,14 +149,18 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   s.tw = p; p += P;
   s.twm = p; p += M;
   const int cpp = cp + 1, Pp = P + 1;       // padded pitches of the transpose buffers
+  // CS = 1: bufA = bufB = rows, one M x (P + 1) array (cpp == Pp): a warp reads a
+  // whole row / column into registers before it writes the transformed one back
+  constexpr bool SOLO = CS == 1;
+  constexpr int RP = SOLO ? P + 1 : M;      // pitch of the row buffer
   s.bufA = p; p += (size_t)M * cpp;
-  s.bufB = p; p += (size_t)rp * Pp;
-  s.rows = p; p += (size_t)rp * M;
+  s.bufB = SOLO ? s.bufA : p; p += SOLO ? 0 : (size_t)rp * Pp;
+  s.rows = SOLO ? s.bufA : p; p += SOLO ? 0 : (size_t)rp * M;
   s.small = p; p += (size_t)M0 + (size_t)rp * K;
   constexpr bool PRE = CS == 8;   // staged constants (view_smem_bytes)
   s.khs = p; p += PRE ? (size_t)cp * P : 0;
   s.pre = p; p += PRE ? (size_t)rp * M : 0;
-  s.dsum = p; p += (size_t)32 * (VIEW_MAX_THREADS / 32) + M0 / CS + 1;
+  s.dsum = p; p += (size_t)32 * (VIEW_SOLO_THREADS / 32) + M0 / CS + 1;
   const int opr = (M0 + CS - 1) / CS;   // truncation outputs owned per rank
   C<T>* xch = p; p += ((size_t)CS * a.R > (size_t)CS * opr ? (size_t)CS * a.R : (size_t)CS * opr);
   double* red = reinterpret_cast<double*>(p);
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
                  [&](int w, int x) { return conj_<T>(tw_[(corner_freq<T>(w, mf, M) * x) & (M - 1)]); },
                  [&](int yl, int x, C<T> val) {
                    val = cscale<T>(val, inv);
-                   s.rows[yl * M + x] = val;
+                   s.rows[yl * RP + x] = val;
                    Jg[yl * M + x] = val;
                  });
     } else {
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
           acc = cadd<T>(acc, cmulc<T>(V[yl * K + w], s.twm[(f * x) & (M - 1)]));
         }
         acc = cscale<T>(acc, inv);
-        s.rows[i] = acc;
+        s.rows[yl * RP + x] = acc;
         Jg[i] = acc;
       }
     }
@@ -240,13 +248,13 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
       cp_async_commit();
     }
     const C<T>* g = a.gE + (size_t)v * img + (size_t)y0 * M;
-    for (int i = tid; i < rp * M; i += blockDim.x) s.rows[i] = conj_<T>(g[i]);
+    for (int i = tid; i < rp * M; i += blockDim.x) s.rows[(i / M) * RP + (i % M)] = conj_<T>(g[i]);
     __syncthreads();
   } else {
     const C<T>* g = a.x + (size_t)v * img + (size_t)y0 * M;
     for (int i = tid; i < rp * M; i += blockDim.x) {
       C<T> t = g[i];
-      s.rows[i] = a.conj_in ? conj_<T>(t) : t;
+      s.rows[(i / M) * RP + (i % M)] = a.conj_in ? conj_<T>(t) : t;
     }
     __syncthreads();
   }
@@ -258,7 +266,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const int col = lane + 32 * k;
-      x[k] = (k < KH && lane_ok) ? s.rows[yl * M + col] : czero<T>();
+      x[k] = (k < KH && lane_ok) ? s.rows[yl * RP + col] : czero<T>();
     }
     warp_fft_fwd<T, E>(x, ltw, lane);
 #pragma unroll
@@ -274,7 +282,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   // term (receivers rank, rank + CS, ...; H rows from L2) then runs while the
   // other CTAs finish theirs, and the wait acquires everyone's scatter.
   tl_stage(a.tl, 1);
-  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  if constexpr (!SOLO) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   if (MODE == VIEW_BWD && !a.gad) {
     // G_S^H g_rows through H (pdf_aux.cuh) for my outputs i = rank + CS*o,
     // while the other CTAs finish their stage-A scatter; warp w sums
@@ -330,7 +338,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
   }
   cp_async_wait<0>();   // K^ columns, E_inc / g_J local rows (own copies: a CTA barrier follows)
   __syncthreads();
-  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if constexpr (!SOLO) asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 
   tl_stage(a.tl, 2);
   // ---------------- stage B: columns: FFT, x K^, inverse FFT ---------------
@@ -363,7 +371,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
     }
   }
   tl_stage(a.tl, 3);
-  cluster.sync();   // also publishes the data partials (written before this arrive) to rank 0
+  if constexpr (SOLO) __syncthreads(); else cluster.sync();   // also publishes the data partials (written before this arrive) to rank 0
 
   if (MODE == VIEW_FWD && a.do_data && rank == 0 && tid == 0) {
     double t = 0.0;
@@ -392,7 +400,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
         nrm += (double)cabs2<T>(e);
       } else if constexpr (MODE == VIEW_BWD) {
         const C<T> gl = PRE ? s.pre[yl * M + col] : a.gJloc[rowoff + col];
-        s.rows[yl * M + col] = cadd<T>(gl, conj_<T>(x[k]));
+        s.rows[yl * RP + col] = cadd<T>(gl, conj_<T>(x[k]));
       } else {
         a.y[rowoff + col] = a.conj_out ? conj_<T>(x[k]) : x[k];
       }
@@ -423,7 +431,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
     if constexpr (sizeof(T) == 8) {
       const C<T>* tw_ = s.twm;
       const C<T>* rw = s.rows;
-      cgemm_dmma(rp, K, M, [&](int yl, int x) { return rw[yl * M + x]; },
+      cgemm_dmma(rp, K, M, [&](int yl, int x) { return rw[yl * RP + x]; },
                  [&](int x, int w) { return tw_[(corner_freq<T>(w, mf, M) * x) & (M - 1)]; },
                  [&](int yl, int w, C<T> val) { U[yl * K + w] = val; });
       __syncthreads();
@@ -437,10 +445,10 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
         C<T> acc = czero<T>();
         C<T> acc1 = czero<T>(), acc2 = czero<T>(), acc3 = czero<T>();
         for (int x = 0; x < M; x += 4) {   // M is a multiple of 4: four independent chains
-          acc = cadd<T>(acc, cmul<T>(s.rows[yl * M + x], s.twm[(f * x) & (M - 1)]));
-          acc1 = cadd<T>(acc1, cmul<T>(s.rows[yl * M + x + 1], s.twm[(f * (x + 1)) & (M - 1)]));
-          acc2 = cadd<T>(acc2, cmul<T>(s.rows[yl * M + x + 2], s.twm[(f * (x + 2)) & (M - 1)]));
-          acc3 = cadd<T>(acc3, cmul<T>(s.rows[yl * M + x + 3], s.twm[(f * (x + 3)) & (M - 1)]));
+          acc = cadd<T>(acc, cmul<T>(s.rows[yl * RP + x], s.twm[(f * x) & (M - 1)]));
+          acc1 = cadd<T>(acc1, cmul<T>(s.rows[yl * RP + x + 1], s.twm[(f * (x + 1)) & (M - 1)]));
+          acc2 = cadd<T>(acc2, cmul<T>(s.rows[yl * RP + x + 2], s.twm[(f * (x + 2)) & (M - 1)]));
+          acc3 = cadd<T>(acc3, cmul<T>(s.rows[yl * RP + x + 3], s.twm[(f * (x + 3)) & (M - 1)]));
         }
         acc = cadd<T>(cadd<T>(acc, acc1), cadd<T>(acc2, acc3));
         U[i] = acc;
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(VIEW_MAX_THREADS) view_kernel(ViewArgs<T> a) {
       }
     }
     tl_stage(a.tl, 6);
-    cluster.sync();
+    if constexpr (SOLO) __syncthreads(); else cluster.sync();
     tl_stage(a.tl, 7);
     const T inv = T(1) / (T(M) * T(M));
     for (int i = rank + CS * tid; i < M0; i += CS * blockDim.x) {

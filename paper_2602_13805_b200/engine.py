@@ -178,6 +178,7 @@ class DeviceProblem:
         if hasattr(self.lib, "pdf_ctx_paths"):
             N.check(self.lib.pdf_ctx_paths(self.ctx, ct.byref(paths)))
         self.large_grid, self.data_gemm, self.split_bwd = (bool(paths.value & b) for b in (1, 2, 4))
+        self.view_cluster = (paths.value >> 8) & 15   # CTAs per view of the cluster path (0: large-grid path)
         self.bd = torch.zeros(S, 6, dtype=torch.float64, device=dev)
 
     def __del__(self):
@@ -187,6 +188,11 @@ class DeviceProblem:
                 self.ctx = None
         except Exception:
             pass
+
+    def paths(self) -> dict:
+        """Kernel paths the library chose for this problem (pdf_ctx_paths)."""
+        return {"large_grid": self.large_grid, "data_gemm": self.data_gemm, "split_bwd": self.split_bwd,
+                "view_cluster": self.view_cluster}
 
     # ------------------------------------------------------------------ helpers
     def cplx(self, *shape):

@@ -207,3 +207,50 @@ def test_captured_graph_with_side_branches_matches_eager(tiny_setup, n):
     (tg, lg), (te, le) = out
     assert np.allclose(lg, le, rtol=1e-9, atol=0)
     assert np.abs(tg - te).max() < 1e-9
+
+
+# ---------------------------------------------------------------------------
+# One 16-warp CTA per view (PDF_VIEW_CLUSTER=1, what batches of >= 592 views of
+# M <= 64 run): the same goldens as the cluster path.
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_forced_single_cta_view_path_single_step(monkeypatch, cfg_id):
+    monkeypatch.setenv("PDF_VIEW_CLUSTER", "1")
+    g = golden(f"cfg{cfg_id}")
+    st = Setup(cfg_baseline(cfg_id), plane=True)
+    dev = _single_step_checks(st, g)
+    assert dev.paths()["view_cluster"] == 1
+
+
+def test_forced_single_cta_view_path_apply_gd_matches_cluster_path(monkeypatch):
+    st = Setup(cfg_baseline(2), plane=True)
+    g = golden("cfg2")
+    rng = np.random.default_rng(5)
+    x = torch.as_tensor(rng.standard_normal((5, 64, 64)) + 1j * rng.standard_normal((5, 64, 64)), device="cuda")
+    small = _dev(st, g["data"])
+    y0, y1 = small.apply_gd(x), small.apply_gd(x, adjoint=True)
+    monkeypatch.setenv("PDF_VIEW_CLUSTER", "1")
+    solo = _dev(st, g["data"])
+    z0, z1 = solo.apply_gd(x), solo.apply_gd(x, adjoint=True)
+    assert rel(z0.cpu().numpy(), y0.cpu().numpy()) < 1e-13
+    assert rel(z1.cpu().numpy(), y1.cpu().numpy()) < 1e-13
+
+
+def test_batch_of_600_views_takes_the_single_cta_path_and_matches_single_scenes():
+    """38 config-4 scenes x 16 views = 608 views: the batch runs one CTA per
+    view; each scene's loss and gradient agree with the same scene alone
+    (8-CTA clusters, pinned to the reference by the tests above) to 1e-10."""
+    gs = [golden(f"cfg4_s{i % 10}") for i in range(38)]
+    st = Setup(cfg_baseline(4), plane=True)
+    batch = _dev(st, np.stack([x["data"] for x in gs]))
+    assert batch.paths()["view_cluster"] == 1
+    a0 = torch.as_tensor(np.stack([x["alpha0"] for x in gs]), device="cuda")
+    ga, bd = batch.loss_grad(a0)
+    batch.check_errors()
+    ga, bd = ga.cpu().numpy(), bd.cpu().numpy()
+    for i in (0, 7, 37):
+        one = _dev(st, gs[i]["data"][None])
+        assert one.paths()["view_cluster"] == 8
+        g1, b1 = one.loss_grad(a0[i:i + 1])
+        one.check_errors()
+        assert rel(ga[i], g1[0].cpu().numpy()) < 1e-10
+        np.testing.assert_allclose(bd[i], b1[0].cpu().numpy(), rtol=1e-10)
