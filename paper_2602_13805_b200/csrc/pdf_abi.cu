@@ -16,6 +16,7 @@
 #include "pdf_net_mma.cuh"
 #include "pdf_pixel.cuh"
 #include "pdf_shard.cuh"
+#include "pdf_pixel_stream.cuh"
 #include "pdf_view.cuh"
 #include "pdf_view_large.cuh"
 
@@ -471,6 +472,30 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   // 1/4 142, 1/8 151, 2/4 150, 2/8 160 us; cfg2 8.2-8.9 us for all)
   const long long rows1 = (long long)(c->M / c->TX) * c->M * c->d.S;
   const bool batch = rows1 > 4 * 148;
+  // throughput regime: three streaming kernels (pdf_pixel_stream.cuh; cfg4 579 -> 367 us, cfg5 142 -> 86 us)
+  static const int stream_env = env_int("PDF_PIX_STREAM", 1);
+  if (batch && stream_env) {
+    PixStreamArgs<T> q = {};
+    q.p = p;
+    const size_t img = (size_t)c->M * c->M;
+    q.sums = c->pix;
+    q.coef = c->pix + (size_t)c->d.S * img * 4;
+    void* qargs[] = {&q};
+    // (chunks of scenes sized for the L2, so that the gradient pass re-reads J, E
+    // from it, measured slower: 372 us in one launch, 398 / 431 / 620 us in
+    // chunks of 80 / 40 / 20 MiB -- the per-chunk launches' ramps and tails)
+    cudaError_t e = plain_launch(pix_sums_kernel<T>, dim3((unsigned)(img / 32), c->d.S), dim3(256), 0, st, qargs);
+    q.p.tl = 0;
+    if (e == cudaSuccess)
+      e = plain_launch(pix_point_kernel<T, GRAD, 4>, dim3(c->M / c->TX, c->M / 4, c->d.S), dim3(128), 0, st, qargs);
+    if (GRAD && e == cudaSuccess) {
+      q.p.tl = p.tl;
+      e = plain_launch(pix_grad_kernel<T>, dim3((unsigned)((img + 255) / 256), (c->d.n + PG_VIEWS - 1) / PG_VIEWS, c->d.S),
+                       dim3(256), 0, st, qargs);
+    }
+    if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("pixel kernels (stream): ") + cudaGetErrorString(e));
+    return PDF_OK;
+  }
   static const int ty_env = env_int("PDF_PIX_TY", 0);
   const int ty = ty_env == 1 || ty_env == 2 ? ty_env : (batch && c->d.n <= 16 ? 2 : 1);
   static const int pw_env = env_int("PDF_PIX_WARPS", 0);

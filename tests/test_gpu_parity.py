@@ -73,6 +73,31 @@ def test_grad_alpha_tiny(tiny_setup, g_tiny, variant):
     np.testing.assert_allclose(bdd[0].cpu().numpy(), bd, rtol=1e-10)
 
 
+@pytest.mark.parametrize("variant", ["plain", "frozen", "mask"])
+def test_grad_alpha_tiny_batch_streaming_pixel_path(tiny_setup, g_tiny, variant):
+    """40 copies of the tiny scene in one batch: enough image rows for the
+    streaming per-pixel kernels (pdf_pixel_stream.cuh: view sums, closed-form
+    state term / R-chain, one gradient pass) -- same goldens, same tolerance."""
+    g, S = g_tiny, 40
+    rep = lambda x: np.repeat(np.asarray(x)[None], S, axis=0)
+    if variant == "plain":
+        dev, want, bd = _dev(tiny_setup, rep(g["data"])), g["g_alpha"], g["bd"]
+    elif variant == "frozen":
+        dev, want, bd = _dev(tiny_setup, rep(g["data"]), r_fixed=rep(g["r0"])), g["g_frozen"], g["bd_frozen"]
+    else:
+        dev = _dev(tiny_setup, rep(g["data"] * g["mask"]), mask=rep(g["mask"]))
+        want, bd = g["g_mask"], g["bd_mask"]
+    ga, bdd = dev.loss_grad(_t(rep(g["alpha"]), dev))
+    dev.check_errors()
+    for i in (0, 17, 39):
+        assert rel(ga[i].cpu().numpy(), want) < 1e-10
+        np.testing.assert_allclose(bdd[i].cpu().numpy(), bd, rtol=1e-10)
+    # loss-only entry (no gradient pass) and chi
+    bd2, chi = dev.loss_value(_t(rep(g["alpha"]), dev), want_chi=True)
+    np.testing.assert_allclose(bd2[39].cpu().numpy(), bd, rtol=1e-10)
+    assert torch.equal(chi[0], chi[39])
+
+
 def test_grad_alpha_cfg1(cfg1_setup, g_cfg1):
     g = g_cfg1
     dev = _dev(cfg1_setup, g["data"])
