@@ -1,0 +1,4 @@
+cd /root/repo
+python -m pytest tests/test_gpu_large.py -m gpu -q -x 2>&1 | tail -3
+python tools/timeline.py --cfg 5 2>&1 | grep "iteration period\|^bwd_l1 "
+python tools/timeline.py --cfg 3 2>&1 | grep "iteration period\|^bwd_l1 "
