@@ -360,9 +360,12 @@ template <typename T, int E, int MODE>
 static cudaError_t vl_chunk(pdf_ctx* c, VLArgs<T>& a, int cnt, cudaStream_t st) {
   constexpr int P = 32 * E, M = P / 2;
   void* args[] = {&a};
+  a.nview = cnt;
   cudaError_t e = plain_launch(vl_rows_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256),
                                vl_rows_smem<T>(E, c->d.mf), st, args);
-  if (e == cudaSuccess) e = plain_launch(vl_cols_kernel<T, E>, dim3(P / 8, cnt), dim3(256), vl_cols_smem<T>(E), st, args);
+  const int nvc = sizeof(T) == 8 && E >= 4 ? 2 : 1;   // views per CTA of the cols pass
+  if (e == cudaSuccess)
+    e = plain_launch(vl_cols_kernel<T, E>, dim3(P / 8, (cnt + nvc - 1) / nvc), dim3(256), vl_cols_smem<T>(E), st, args);
   if (e == cudaSuccess)
     e = plain_launch(vl_out_kernel<T, E, MODE>, dim3(M / VL_ROWS, cnt), dim3(256), vl_out_smem<T>(E, c->d.mf), st,
                      args);

@@ -36,6 +36,7 @@ template <typename T>
 struct VLArgs {
   int M, mf, R, n, NPV;       // NPV = M / VL_ROWS partials per view
   int v0;                      // first global view (scene * n + view) of this chunk
+  int nview;                   // views in this chunk (cols pass: two views per CTA)
   const C<T>* khat;            // permuted, 1/P^2-scaled kernel spectrum [P col pos][P row pos]
   const C<T>* twP;
   const C<T>* twM;
@@ -82,7 +83,7 @@ __host__ __device__ inline size_t vl_rows_smem(int E, int mf) {
 // cols pass: the warps' kernel-spectrum columns (float64 split path)
 template <typename T>
 __host__ __device__ inline size_t vl_cols_smem(int E) {
-  return sizeof(T) == 8 && E >= 4 ? (size_t)8 * 32 * E * sizeof(C<T>) : 0;
+  return sizeof(T) == 8 && E >= 4 ? (size_t)8 * (32 * E + 16 * E) * sizeof(C<T>) : 0;   // K^ columns + the second view's inputs
 }
 
 template <typename T>
@@ -282,28 +283,56 @@ __global__ void __launch_bounds__(256, (E >= 4 ? 2 : 1)) vl_cols_kernel(VLArgs<T
     }
     pdl_wait();
   tl_mark(a.tl, 1);
-    C<T>* col = a.spec + ((size_t)blockIdx.y * P + pos) * M;
-    C<T> xin[EH], r[EH], t[EH];
+    // float64: two views per CTA (the same kernel-spectrum columns serve both);
+    // the second view's column streams into shared memory while the first is
+    // transformed, and the first's stores drain behind the second's transforms
+    constexpr int NV = sizeof(T) == 8 ? 2 : 1;
+    const int v0 = blockIdx.y * NV;
+    C<T>* xs = nullptr;
+    if constexpr (NV == 2) {
+      extern __shared__ __align__(16) unsigned char smem_raw2[];
+      xs = reinterpret_cast<C<T>*>(smem_raw2) + (size_t)8 * P + (size_t)warp * M;
+      if (v0 + 1 < a.nview) {
+        const C<T>* c1 = a.spec + ((size_t)(v0 + 1) * P + pos) * M;
 #pragma unroll
-    for (int k = 0; k < EH; ++k) xin[k] = col[lane + 32 * k];
+        for (int k = 0; k < EH; ++k) cp_async16(xs + lane + 32 * k, c1 + lane + 32 * k, true);
+      }
+      cp_async_commit();
+    }
+#pragma unroll 1
+    for (int vi = 0; vi < NV; ++vi) {
+      if (v0 + vi >= a.nview) break;
+      C<T>* col = a.spec + ((size_t)(v0 + vi) * P + pos) * M;
+      C<T> xin[EH], r[EH], t[EH];
+      if (vi == 0) {
 #pragma unroll
-    for (int k = 0; k < EH; ++k) t[k] = xin[k];
-    warp_fft_fwd<T, EH>(t, lt, lane);
-    if constexpr (sizeof(T) == 8) cp_async_wait<0>();
+        for (int k = 0; k < EH; ++k) xin[k] = col[lane + 32 * k];
+      } else {
+        cp_async_wait<0>();   // (lane l reads the entries it copied)
 #pragma unroll
-    for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[q * 32 + lane]);
-    warp_fft_inv<T, EH>(t, lt, lane);
+        for (int k = 0; k < EH; ++k) xin[k] = xs[lane + 32 * k];
+      }
 #pragma unroll
-    for (int k = 0; k < EH; ++k) r[k] = t[k];
+      for (int k = 0; k < EH; ++k) t[k] = xin[k];
+      warp_fft_fwd<T, EH>(t, lt, lane);
+      if constexpr (sizeof(T) == 8) {
+        if (vi == 0) cp_async_wait<1>();   // the kernel-spectrum column (older group)
+      }
 #pragma unroll
-    for (int k = 0; k < EH; ++k) t[k] = cmul<T>(xin[k], tw[lane + 32 * k]);
-    warp_fft_fwd<T, EH>(t, lt, lane);
+      for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[q * 32 + lane]);
+      warp_fft_inv<T, EH>(t, lt, lane);
 #pragma unroll
-    for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[P / 2 + q * 32 + lane]);
-    warp_fft_inv<T, EH>(t, lt, lane);
-    pdl_trigger();
+      for (int k = 0; k < EH; ++k) r[k] = t[k];
 #pragma unroll
-    for (int k = 0; k < EH; ++k) col[lane + 32 * k] = cadd<T>(r[k], cmulc<T>(t[k], tw[lane + 32 * k]));
+      for (int k = 0; k < EH; ++k) t[k] = cmul<T>(xin[k], tw[lane + 32 * k]);
+      warp_fft_fwd<T, EH>(t, lt, lane);
+#pragma unroll
+      for (int q = 0; q < EH; ++q) t[q] = cmul<T>(t[q], kh[P / 2 + q * 32 + lane]);
+      warp_fft_inv<T, EH>(t, lt, lane);
+      if (vi == NV - 1 || v0 + vi + 1 >= a.nview) pdl_trigger();
+#pragma unroll
+      for (int k = 0; k < EH; ++k) col[lane + 32 * k] = cadd<T>(r[k], cmulc<T>(t[k], tw[lane + 32 * k]));
+    }
     return;
   }
   LaneTw<T, E> ltw;
