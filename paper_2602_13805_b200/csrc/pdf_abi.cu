@@ -979,8 +979,25 @@ static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStrea
   const dim3 grid((unsigned)items, c->d.S);
   void* args[] = {&a};
   const int MT = (c->rows + 7) / 8;
-  const size_t smem = adam_x_smem_bytes(MT);
   cudaError_t e;
+  // many rows, one scene: the persistent warp-specialised form (bulk-copy ring)
+  static const int ring_env = env_int("PDF_ADAM_RING", 1);
+  bool aligned = true;
+  for (int l = 0; l < 3; ++l)
+    if (a.L[l].items && (a.L[l].N % AX_NB || a.L[l].K % (AX_ST * 8))) aligned = false;
+  if (ring_env && c->d.S == 1 && MT >= 5 && aligned && items > 2 * 148) {
+    const size_t rs = adam_ring_smem_bytes(MT);
+    const dim3 rgrid(148);
+    switch (MT) {
+#define RCASE(MM) case MM: e = plain_launch(net_adam_ring_kernel<MM>, rgrid, dim3(AR_THREADS), rs, st, args); break;
+      RCASE(5) RCASE(6) RCASE(7) RCASE(8) RCASE(9)
+      default: e = plain_launch(net_adam_ring_kernel<10>, rgrid, dim3(AR_THREADS), rs, st, args); break;
+#undef RCASE
+    }
+    if (e != cudaSuccess) return fail(PDF_ECUDA, std::string("net adam (ring): ") + cudaGetErrorString(e));
+    return PDF_OK;
+  }
+  const size_t smem = adam_x_smem_bytes(MT);
   switch (MT) {
 #define ACASE(MM) case MM: e = plain_launch(net_adam_x_kernel<MM>, grid, dim3(256), smem, st, args); break;
     ACASE(1) ACASE(2) ACASE(3) ACASE(4) ACASE(5) ACASE(6) ACASE(7) ACASE(8) ACASE(9)

@@ -82,6 +82,21 @@ __device__ __forceinline__ void bulk_copy_multicast(void* dst, const void* src, 
       : "memory");
 }
 
+// global -> this CTA's shared memory (TMA engine, 1-D bulk copy), completion in bytes on `bar`
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, void* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
 // 16-byte asynchronous global -> shared copy (LDGSTS); zero-fills when !pred
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);

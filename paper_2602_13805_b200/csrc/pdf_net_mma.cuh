@@ -795,6 +795,217 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
   tl_mark(a.tl, 2);
 }
 
+// The same update as a persistent, warp-specialised kernel for many rows
+// (config 5: 72 rows, 33.6 M parameters): one CTA per SM walks its share of
+// the (n-block, k-strip) items; four loader warps feed a two-stage shared-memory
+// ring with the item's W, m, v tiles (64 rows x 256 bytes each), the strip's
+// h columns and the block's g_z columns (16-byte cp.async pieces whose
+// completion arrives on the stage's mbarrier; as 1-D bulk copies of one row
+// each -- 336 TMA instructions per item -- the kernel ran at 10 us per item,
+// 1 136 us), so the next item's 108 KB stream in while
+// the eight compute warps run the current item's DMMA product and Adam
+// arithmetic and store W, m, v straight from registers.  net_adam_x_kernel
+// above requests everything of an item at once and then computes: with two
+// CTAs per SM its loads, arithmetic and stores barely overlap (0.49 of HBM).
+// Row pitches: W / m / v tiles 34 doubles, h 36, g_z 68 (conflict-free 16-byte
+// and fragment reads).  Used when N % 64 == 0 and K % 32 == 0 for every layer.
+constexpr int AR_WP = AX_ST * 8 + 2;
+constexpr int AR_CW = 8;                        // compute warps (16 = two per n-tile measured no faster)
+constexpr int AR_THREADS = (AR_CW + 4) * 32;    // + four loader warps
+__host__ __device__ constexpr size_t adam_ring_stage_doubles(int MT) {
+  return (size_t)3 * AX_NB * AR_WP + (size_t)8 * MT * (AX_HP + AX_GP);
+}
+__host__ __device__ constexpr size_t adam_ring_smem_bytes(int MT) {
+  return 2 * adam_ring_stage_doubles(MT) * sizeof(double) + 64;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArgs a) {
+  constexpr int RPM = 8 * MT, NS = RPM / 4;
+  constexpr int CW = AR_CW, JW = AX_ST * 8 / CW;   // compute warps; k-tiles per warp (two warps per n-tile)
+  constexpr int HP = AX_HP, GP = AX_GP, WP = AR_WP;
+  constexpr size_t STG = adam_ring_stage_doubles(MT);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + 2 * STG);   // full[2], empty[2]
+  __shared__ double bc_s[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int rows = a.rows;
+  tl_mark(a.tl, 0);
+  if (tid == 0) {
+    const double tt = (double)(a.tsnap ? *a.tsnap : *a.step);
+    bc_s[0] = 1.0 / (1.0 - pow(a.b1, tt));
+    bc_s[1] = 1.0 / (1.0 - pow(a.b2, tt));
+    mbar_init(&bars[0], 128);   // one (asynchronous) arrival per loader thread
+    mbar_init(&bars[1], 128);
+    mbar_init(&bars[2], CW);    // one arrival per compute warp
+    mbar_init(&bars[3], CW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  // rows beyond `rows` of the h / g_z stages stay zero for the whole kernel
+  for (int st = 0; st < 2; ++st) {
+    double* hS = ring + st * STG + 3 * AX_NB * WP;
+    double* gS = hS + RPM * HP;
+    for (int i = tid; i < (RPM - rows) * HP; i += blockDim.x) hS[(size_t)rows * HP + i] = 0.0;
+    for (int i = tid; i < (RPM - rows) * GP; i += blockDim.x) gS[(size_t)rows * GP + i] = 0.0;
+  }
+  __syncthreads();
+  const int total = a.L[0].items + a.L[1].items + a.L[2].items;
+  // item sequence of this CTA: runs of AR_RUN consecutive items (consecutive
+  // k-strips of one n-block share the g_z block: it is copied once per run and
+  // stage), the runs dealt round-robin so every CTA starts with the layers
+  // whose g_z is oldest
+  constexpr int AR_RUN = 8;
+  const int nseq = (total + AR_RUN * (int)gridDim.x - 1) / (AR_RUN * (int)gridDim.x) * AR_RUN;
+  auto item_at = [&](int q) { return (q / AR_RUN) * (AR_RUN * (int)gridDim.x) + (int)blockIdx.x * AR_RUN + (q % AR_RUN); };
+  double* __restrict__ th = a.theta;
+  double* __restrict__ mm = a.m;
+  double* __restrict__ vv = a.v;
+  auto decode = [&](int item, int& li, int& local) {
+    li = 0;
+    local = item;
+    while (li < 2 && local >= a.L[li].items) { local -= a.L[li].items; ++li; }
+  };
+
+  if (warp >= CW) {
+    // ---------------- loader warps (4): 16-byte cp.async pieces, completion on the stage's mbarrier
+    const int lt = tid - CW * 32;   // 0 .. 127
+    bool waited = false;
+    int ring_it = 0;
+    int gz_key[2] = {-1, -1};   // (layer, n-block) whose g_z block each stage holds
+    for (int q = 0; q < nseq; ++q) {
+      const int item = item_at(q);
+      if (item >= total) continue;
+      int li, local;
+      decode(item, li, local);
+      const AdamLayer& L = a.L[li];
+      if (local >= L.nblk * L.strips) continue;   // bias item: no ring stage
+      if (L.wait && !waited) { pdl_wait(); waited = true; }
+      const int st = ring_it & 1;
+      mbar_wait(&bars[2 + st], ((ring_it >> 1) & 1) ^ 1);   // stage free (first round passes)
+      const int nb = local / L.strips, k0 = (local % L.strips) * AX_ST * 8, n0 = nb * AX_NB;
+      double* Wt = ring + st * STG;
+      double* hS = Wt + 3 * AX_NB * WP;
+      double* gS = hS + RPM * HP;
+      const int K = L.K, N = L.N;
+      {
+        // W, m, v tiles: 64 rows x 16 pieces each; thread lt takes piece lt % 16 of rows lt / 16 + 8 i
+        const int seg = lt & 15, r0 = lt >> 4;
+        const double* bw = th + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
+        const double* bm = mm + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
+        const double* bv = vv + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
+        double* dw = Wt + (size_t)r0 * WP + 2 * seg;
+#pragma unroll
+        for (int i = 0; i < AX_NB / 8; ++i) {
+          cp_async16(dw + (size_t)(8 * i) * WP, bw + (size_t)(8 * i) * K, true);
+          cp_async16(dw + (size_t)(AX_NB + 8 * i) * WP, bm + (size_t)(8 * i) * K, true);
+          cp_async16(dw + (size_t)(2 * AX_NB + 8 * i) * WP, bv + (size_t)(8 * i) * K, true);
+        }
+        // h strip: rows x 16 pieces
+        for (int r = r0; r < rows; r += 8) cp_async16(hS + (size_t)r * HP + 2 * seg, L.hin + (size_t)r * K + k0 + 2 * seg, true);
+        // g_z block: rows x 32 pieces, unless this stage still holds it
+        const int key = li * 65536 + nb;
+        if (gz_key[st] != key) {
+          gz_key[st] = key;
+          const int sg2 = lt & 31, q0 = lt >> 5;
+          for (int r = q0; r < rows; r += 4)
+            cp_async16(gS + (size_t)r * GP + 2 * sg2, L.gz + (size_t)r * N + n0 + 2 * sg2, true);
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bars[st])) : "memory");
+      ++ring_it;
+    }
+    tl_mark(a.tl, 2);
+    return;
+  }
+
+  // ---------------- compute warps ----------------
+  const double ibc1 = bc_s[0], ibc2 = bc_s[1];
+  int errbits = 0;
+  bool waited = false, marked = false;
+  int ring_it = 0;
+  for (int q = 0; q < nseq; ++q) {
+    const int item = item_at(q);
+    if (item >= total) continue;
+    int li, local;
+    decode(item, li, local);
+    const AdamLayer& L = a.L[li];
+    const int K = L.K, N = L.N;
+    const int wc = L.nblk * L.strips;
+    if (local < wc) {
+      const int st = ring_it & 1;
+      mbar_wait(&bars[st], (ring_it >> 1) & 1);
+      if (!marked) { tl_mark(a.tl, 1); marked = true; }
+      const int nb = local / L.strips, k0 = (local % L.strips) * AX_ST * 8;
+      const int wn = warp % 8, j0 = (warp / 8) * JW;   // n-tile, first k-tile of this warp
+      const int n = nb * AX_NB + wn * 8 + g;
+      const double* Wt = ring + st * STG;
+      const double* hS = Wt + 3 * AX_NB * WP;
+      const double* gS = hS + RPM * HP;
+      double2 wp[JW], wm[JW], wv[JW];
+#pragma unroll
+      for (int j = 0; j < JW; ++j) {
+        const size_t o = (size_t)(wn * 8 + g) * WP + (j0 + j) * 8 + 2 * t;
+        wp[j] = *reinterpret_cast<const double2*>(Wt + o);
+        wm[j] = *reinterpret_cast<const double2*>(Wt + (size_t)AX_NB * WP + o);
+        wv[j] = *reinterpret_cast<const double2*>(Wt + (size_t)2 * AX_NB * WP + o);
+      }
+      double ga[NS];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) ga[s] = gS[(4 * s + t) * GP + wn * 8 + g];   // A[g][t] = g_z[4s + t][n]
+      constexpr int NA = NS >= 12 ? 3 : (NS >= 4 ? 2 : 1);
+      double dg[JW][2];
+#pragma unroll
+      for (int j = 0; j < JW; ++j) {
+        double e0[NA], e1[NA];
+#pragma unroll
+        for (int q = 0; q < NA; ++q) e0[q] = e1[q] = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) dmma(e0[s % NA], e1[s % NA], ga[s], hS[(4 * s + t) * HP + (j0 + j) * 8 + g]);   // B[t][g] = h[4s + t][k]
+        double d0 = e0[0], d1 = e1[0];
+#pragma unroll
+        for (int q = 1; q < NA; ++q) { d0 += e0[q]; d1 += e1[q]; }
+        dg[j][0] = d0;
+        dg[j][1] = d1;
+      }
+      // every shared-memory read of this stage is done: hand it back to the loader
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[2 + st]);
+#pragma unroll
+      for (int j = 0; j < JW; ++j) {
+        const double d0 = dg[j][0], d1 = dg[j][1];
+        if (!isfinite(d0) || !isfinite(d1)) errbits |= ERR_NONFINITE_GRAD;
+        adam_one<double>(wp[j].x, wm[j].x, wv[j].x, d0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        adam_one<double>(wp[j].y, wm[j].y, wv[j].y, d1, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        if (!isfinite(wp[j].x) || !isfinite(wp[j].y)) errbits |= ERR_NONFINITE_PARAM;
+        const size_t o = L.w_off + (size_t)n * K + k0 + (j0 + j) * 8 + 2 * t;
+        *reinterpret_cast<double2*>(th + o) = wp[j];
+        *reinterpret_cast<double2*>(mm + o) = wm[j];
+        *reinterpret_cast<double2*>(vv + o) = wv[j];
+      }
+      ++ring_it;
+    } else {
+      // bias item: outputs 256 * (local - wc) + tid (network.py:213,217)
+      const int bn = (local - wc) * 256 + tid;
+      if (L.wait && !waited) { pdl_wait(); waited = true; }
+      if (!marked) { tl_mark(a.tl, 1); marked = true; }
+      if (tid < 256 && bn < N) {
+        const size_t o = L.b_off + bn;
+        double p = th[o], m1 = mm[o], v1 = vv[o];
+        double gb = 0.0;
+        for (int r = 0; r < rows; ++r) gb += L.gz[(size_t)r * N + bn];
+        if (!isfinite(gb)) errbits |= ERR_NONFINITE_GRAD;
+        adam_one<double>(p, m1, v1, gb, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
+        if (!isfinite(p)) errbits |= ERR_NONFINITE_PARAM;
+        th[o] = p; mm[o] = m1; vv[o] = v1;
+      }
+    }
+  }
+  if (errbits) atomicOr(&a.err[0], errbits);
+  tl_mark(a.tl, 2);
+}
+
 // g_h = g_z W_old for many rows or wide layers (network.py:210-212): CTA =
 // all rows x 64 outputs (one 8-wide k-tile per warp), n reduction in chunks
 // of 32 staged with cp.async (double-buffered), split over grid.y slices;
