@@ -797,9 +797,10 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
 
 // The same update as a persistent, warp-specialised kernel for many rows
 // (config 5: 72 rows, 33.6 M parameters): one CTA per SM walks its share of
-// the (n-block, k-strip) items; four loader warps feed a two-stage shared-memory
-// ring with the item's W, m, v tiles (64 rows x 256 bytes each), the strip's
-// h columns and the block's g_z columns (16-byte cp.async pieces whose
+// the (n-block, k-strip) items; four loader warps feed a three-stage shared-memory
+// ring with the item's W, m, v tiles (64 rows x 256 bytes each) and the strip's
+// h columns -- the block's g_z columns take a stage of their own at the start
+// of a run of k-strips -- (16-byte cp.async pieces whose
 // completion arrives on the stage's mbarrier; as 1-D bulk copies of one row
 // each -- 336 TMA instructions per item -- the kernel ran at 10 us per item,
 // 1 136 us), so the next item's 108 KB stream in while
@@ -812,22 +813,26 @@ __global__ void __launch_bounds__(256) net_adam_x_kernel(NetAdamArgs a) {
 constexpr int AR_WP = AX_ST * 8 + 2;
 constexpr int AR_CW = 8;                        // compute warps (16 = two per n-tile measured no faster)
 constexpr int AR_THREADS = (AR_CW + 4) * 32;    // + four loader warps
+constexpr int AR_NST = 3;                       // ring stages: two items' W / m / v in flight beside the one in use
+// a stage holds an item's W / m / v tiles and h columns, or (first step of a
+// run of k-strips) the n-block's g_z columns, which the compute warps copy
+// into their A-fragment registers for the whole run
 __host__ __device__ constexpr size_t adam_ring_stage_doubles(int MT) {
-  return (size_t)3 * AX_NB * AR_WP + (size_t)8 * MT * (AX_HP + AX_GP);
+  return (size_t)3 * AX_NB * AR_WP + (size_t)8 * MT * AX_HP;
 }
 __host__ __device__ constexpr size_t adam_ring_smem_bytes(int MT) {
-  return 2 * adam_ring_stage_doubles(MT) * sizeof(double) + 64;
+  return AR_NST * adam_ring_stage_doubles(MT) * sizeof(double) + 128;
 }
 
 template <int MT>
 __global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArgs a) {
   constexpr int RPM = 8 * MT, NS = RPM / 4;
-  constexpr int CW = AR_CW, JW = AX_ST * 8 / CW;   // compute warps; k-tiles per warp (two warps per n-tile)
-  constexpr int HP = AX_HP, GP = AX_GP, WP = AR_WP;
+  constexpr int HP = AX_HP, GP = AX_GP, WP = AR_WP, NST = AR_NST, JW = AX_ST;
   constexpr size_t STG = adam_ring_stage_doubles(MT);
+  static_assert((size_t)RPM * GP <= (size_t)3 * AX_NB * WP, "the g_z block must fit the W / m / v part of a stage");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + 2 * STG);   // full[2], empty[2]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(ring + NST * STG);   // full[NST], empty[NST]
   __shared__ double bc_s[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -837,25 +842,22 @@ __global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArg
     const double tt = (double)(a.tsnap ? *a.tsnap : *a.step);
     bc_s[0] = 1.0 / (1.0 - pow(a.b1, tt));
     bc_s[1] = 1.0 / (1.0 - pow(a.b2, tt));
-    mbar_init(&bars[0], 128);   // one (asynchronous) arrival per loader thread
-    mbar_init(&bars[1], 128);
-    mbar_init(&bars[2], CW);    // one arrival per compute warp
-    mbar_init(&bars[3], CW);
+    for (int st = 0; st < NST; ++st) {
+      mbar_init(&bars[st], 128);           // one (asynchronous) arrival per loader thread
+      mbar_init(&bars[NST + st], AR_CW);   // one arrival per compute warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // rows beyond `rows` of the h / g_z stages stay zero for the whole kernel
-  for (int st = 0; st < 2; ++st) {
+  // rows beyond `rows` of the h part of every stage stay zero for the whole kernel
+  for (int st = 0; st < NST; ++st) {
     double* hS = ring + st * STG + 3 * AX_NB * WP;
-    double* gS = hS + RPM * HP;
     for (int i = tid; i < (RPM - rows) * HP; i += blockDim.x) hS[(size_t)rows * HP + i] = 0.0;
-    for (int i = tid; i < (RPM - rows) * GP; i += blockDim.x) gS[(size_t)rows * GP + i] = 0.0;
   }
   __syncthreads();
   const int total = a.L[0].items + a.L[1].items + a.L[2].items;
   // item sequence of this CTA: runs of AR_RUN consecutive items (consecutive
-  // k-strips of one n-block share the g_z block: it is copied once per run and
-  // stage), the runs dealt round-robin so every CTA starts with the layers
-  // whose g_z is oldest
+  // k-strips of one n-block share the g_z block), the runs dealt round-robin so
+  // every CTA starts with the layers whose g_z is oldest
   constexpr int AR_RUN = 8;
   const int nseq = (total + AR_RUN * (int)gridDim.x - 1) / (AR_RUN * (int)gridDim.x) * AR_RUN;
   auto item_at = [&](int q) { return (q / AR_RUN) * (AR_RUN * (int)gridDim.x) + (int)blockIdx.x * AR_RUN + (q % AR_RUN); };
@@ -868,50 +870,51 @@ __global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArg
     while (li < 2 && local >= a.L[li].items) { local -= a.L[li].items; ++li; }
   };
 
-  if (warp >= CW) {
+  if (warp >= AR_CW) {
     // ---------------- loader warps (4): 16-byte cp.async pieces, completion on the stage's mbarrier
-    const int lt = tid - CW * 32;   // 0 .. 127
+    const int lt = tid - AR_CW * 32;   // 0 .. 127
     bool waited = false;
-    int ring_it = 0;
-    int gz_key[2] = {-1, -1};   // (layer, n-block) whose g_z block each stage holds
+    int ring_it = 0, gz_key = -1;
     for (int q = 0; q < nseq; ++q) {
       const int item = item_at(q);
       if (item >= total) continue;
       int li, local;
       decode(item, li, local);
-      const AdamLayer& L = a.L[li];
+      const AdamLayer L = a.L[li];
       if (local >= L.nblk * L.strips) continue;   // bias item: no ring stage
       if (L.wait && !waited) { pdl_wait(); waited = true; }
-      const int st = ring_it & 1;
-      mbar_wait(&bars[2 + st], ((ring_it >> 1) & 1) ^ 1);   // stage free (first round passes)
       const int nb = local / L.strips, k0 = (local % L.strips) * AX_ST * 8, n0 = nb * AX_NB;
+      const int K = L.K, N = L.N;
+      const int key = li * 65536 + nb;
+      if (key != gz_key) {
+        // a new n-block: its g_z columns take a stage of their own
+        gz_key = key;
+        const int st = ring_it % NST;
+        mbar_wait(&bars[NST + st], ((ring_it / NST) & 1) ^ 1);
+        double* gS = ring + st * STG;
+        const int sg2 = lt & 31, q0 = lt >> 5;   // rows x 32 pieces
+        for (int r = q0; r < rows; r += 4)
+          cp_async16(gS + (size_t)r * GP + 2 * sg2, L.gz + (size_t)r * N + n0 + 2 * sg2, true);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bars[st])) : "memory");
+        ++ring_it;
+      }
+      const int st = ring_it % NST;
+      mbar_wait(&bars[NST + st], ((ring_it / NST) & 1) ^ 1);   // stage free (the first round passes)
       double* Wt = ring + st * STG;
       double* hS = Wt + 3 * AX_NB * WP;
-      double* gS = hS + RPM * HP;
-      const int K = L.K, N = L.N;
       {
         // W, m, v tiles: 64 rows x 16 pieces each; thread lt takes piece lt % 16 of rows lt / 16 + 8 i
         const int seg = lt & 15, r0 = lt >> 4;
-        const double* bw = th + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
-        const double* bm = mm + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
-        const double* bv = vv + L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
+        const size_t go = L.w_off + (size_t)(n0 + r0) * K + k0 + 2 * seg;
         double* dw = Wt + (size_t)r0 * WP + 2 * seg;
 #pragma unroll
         for (int i = 0; i < AX_NB / 8; ++i) {
-          cp_async16(dw + (size_t)(8 * i) * WP, bw + (size_t)(8 * i) * K, true);
-          cp_async16(dw + (size_t)(AX_NB + 8 * i) * WP, bm + (size_t)(8 * i) * K, true);
-          cp_async16(dw + (size_t)(2 * AX_NB + 8 * i) * WP, bv + (size_t)(8 * i) * K, true);
+          cp_async16(dw + (size_t)(8 * i) * WP, th + go + (size_t)(8 * i) * K, true);
+          cp_async16(dw + (size_t)(AX_NB + 8 * i) * WP, mm + go + (size_t)(8 * i) * K, true);
+          cp_async16(dw + (size_t)(2 * AX_NB + 8 * i) * WP, vv + go + (size_t)(8 * i) * K, true);
         }
         // h strip: rows x 16 pieces
         for (int r = r0; r < rows; r += 8) cp_async16(hS + (size_t)r * HP + 2 * seg, L.hin + (size_t)r * K + k0 + 2 * seg, true);
-        // g_z block: rows x 32 pieces, unless this stage still holds it
-        const int key = li * 65536 + nb;
-        if (gz_key[st] != key) {
-          gz_key[st] = key;
-          const int sg2 = lt & 31, q0 = lt >> 5;
-          for (int r = q0; r < rows; r += 4)
-            cp_async16(gS + (size_t)r * GP + 2 * sg2, L.gz + (size_t)r * N + n0 + 2 * sg2, true);
-        }
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&bars[st])) : "memory");
       ++ring_it;
@@ -924,54 +927,65 @@ __global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArg
   const double ibc1 = bc_s[0], ibc2 = bc_s[1];
   int errbits = 0;
   bool waited = false, marked = false;
-  int ring_it = 0;
+  int ring_it = 0, gz_key = -1;
+  double ga[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) ga[s] = 0.0;
   for (int q = 0; q < nseq; ++q) {
     const int item = item_at(q);
     if (item >= total) continue;
     int li, local;
     decode(item, li, local);
-    const AdamLayer& L = a.L[li];
+    const AdamLayer L = a.L[li];
     const int K = L.K, N = L.N;
     const int wc = L.nblk * L.strips;
     if (local < wc) {
-      const int st = ring_it & 1;
-      mbar_wait(&bars[st], (ring_it >> 1) & 1);
-      if (!marked) { tl_mark(a.tl, 1); marked = true; }
       const int nb = local / L.strips, k0 = (local % L.strips) * AX_ST * 8;
-      const int wn = warp % 8, j0 = (warp / 8) * JW;   // n-tile, first k-tile of this warp
-      const int n = nb * AX_NB + wn * 8 + g;
+      const int n = nb * AX_NB + warp * 8 + g;
+      const int key = li * 65536 + nb;
+      if (key != gz_key) {
+        gz_key = key;
+        const int st = ring_it % NST;
+        mbar_wait(&bars[st], (ring_it / NST) & 1);
+        if (!marked) { tl_mark(a.tl, 1); marked = true; }
+        const double* gS = ring + st * STG;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) ga[s] = 4 * s + t < rows ? gS[(4 * s + t) * GP + warp * 8 + g] : 0.0;   // A[g][t] = g_z[4s + t][n]
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[NST + st]);
+        ++ring_it;
+      }
+      const int st = ring_it % NST;
+      mbar_wait(&bars[st], (ring_it / NST) & 1);
       const double* Wt = ring + st * STG;
       const double* hS = Wt + 3 * AX_NB * WP;
-      const double* gS = hS + RPM * HP;
       double2 wp[JW], wm[JW], wv[JW];
 #pragma unroll
       for (int j = 0; j < JW; ++j) {
-        const size_t o = (size_t)(wn * 8 + g) * WP + (j0 + j) * 8 + 2 * t;
+        const size_t o = (size_t)(warp * 8 + g) * WP + j * 8 + 2 * t;
         wp[j] = *reinterpret_cast<const double2*>(Wt + o);
         wm[j] = *reinterpret_cast<const double2*>(Wt + (size_t)AX_NB * WP + o);
         wv[j] = *reinterpret_cast<const double2*>(Wt + (size_t)2 * AX_NB * WP + o);
       }
-      double ga[NS];
-#pragma unroll
-      for (int s = 0; s < NS; ++s) ga[s] = gS[(4 * s + t) * GP + wn * 8 + g];   // A[g][t] = g_z[4s + t][n]
       constexpr int NA = NS >= 12 ? 3 : (NS >= 4 ? 2 : 1);
       double dg[JW][2];
 #pragma unroll
       for (int j = 0; j < JW; ++j) {
         double e0[NA], e1[NA];
 #pragma unroll
-        for (int q = 0; q < NA; ++q) e0[q] = e1[q] = 0.0;
+        for (int qq = 0; qq < NA; ++qq) e0[qq] = e1[qq] = 0.0;
 #pragma unroll
-        for (int s = 0; s < NS; ++s) dmma(e0[s % NA], e1[s % NA], ga[s], hS[(4 * s + t) * HP + (j0 + j) * 8 + g]);   // B[t][g] = h[4s + t][k]
+        for (int s = 0; s < NS; ++s) dmma(e0[s % NA], e1[s % NA], ga[s], hS[(4 * s + t) * HP + j * 8 + g]);   // B[t][g] = h[4s + t][k]
         double d0 = e0[0], d1 = e1[0];
 #pragma unroll
-        for (int q = 1; q < NA; ++q) { d0 += e0[q]; d1 += e1[q]; }
+        for (int qq = 1; qq < NA; ++qq) { d0 += e0[qq]; d1 += e1[qq]; }
         dg[j][0] = d0;
         dg[j][1] = d1;
       }
       // every shared-memory read of this stage is done: hand it back to the loader
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[2 + st]);
+      if (lane == 0) mbar_arrive(&bars[NST + st]);
+      ++ring_it;
 #pragma unroll
       for (int j = 0; j < JW; ++j) {
         const double d0 = dg[j][0], d1 = dg[j][1];
@@ -979,12 +993,11 @@ __global__ void __launch_bounds__(AR_THREADS, 1) net_adam_ring_kernel(NetAdamArg
         adam_one<double>(wp[j].x, wm[j].x, wv[j].x, d0, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
         adam_one<double>(wp[j].y, wm[j].y, wv[j].y, d1, a.lr, a.b1, a.b2, a.eps, ibc1, ibc2);
         if (!isfinite(wp[j].x) || !isfinite(wp[j].y)) errbits |= ERR_NONFINITE_PARAM;
-        const size_t o = L.w_off + (size_t)n * K + k0 + (j0 + j) * 8 + 2 * t;
+        const size_t o = L.w_off + (size_t)n * K + k0 + j * 8 + 2 * t;
         *reinterpret_cast<double2*>(th + o) = wp[j];
         *reinterpret_cast<double2*>(mm + o) = wm[j];
         *reinterpret_cast<double2*>(vv + o) = wv[j];
       }
-      ++ring_it;
     } else {
       // bias item: outputs 256 * (local - wc) + tid (network.py:213,217)
       const int bn = (local - wc) * 256 + tid;
