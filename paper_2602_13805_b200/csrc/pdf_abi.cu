@@ -980,12 +980,13 @@ static int adam_x_all(pdf_ctx* c, double* theta, double* m, double* v, cudaStrea
   void* args[] = {&a};
   const int MT = (c->rows + 7) / 8;
   cudaError_t e;
-  // many rows, one scene: the persistent warp-specialised form (bulk-copy ring)
+  // many rows, one large scene: the persistent warp-specialised form (shared-memory ring)
   static const int ring_env = env_int("PDF_ADAM_RING", 1);
   bool aligned = true;
   for (int l = 0; l < 3; ++l)
     if (a.L[l].items && (a.L[l].N % AX_NB || a.L[l].K % (AX_ST * 8))) aligned = false;
-  if (ring_env && c->d.S == 1 && MT >= 5 && aligned && items > 2 * 148) {
+  // (16+ items per CTA: at cfg3's 7 the pipeline's ramp loses to the one-shot kernel, 37 vs 25 us)
+  if (ring_env && c->d.S == 1 && MT >= 5 && aligned && items > 16 * 148) {
     const size_t rs = adam_ring_smem_bytes(MT);
     const dim3 rgrid(148);
     switch (MT) {
