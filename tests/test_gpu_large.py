@@ -259,3 +259,33 @@ def test_batch_of_600_views_takes_the_single_cta_path_and_matches_single_scenes(
         one.check_errors()
         assert rel(ga[i], g1[0].cpu().numpy()) < 1e-10
         np.testing.assert_allclose(bd[i], b1[0].cpu().numpy(), rtol=1e-10)
+
+
+def test_cfg5_fused_train_steps_match_gradient_plus_adam(cfg5):
+    """Two fused training steps at config 5 (the persistent ring g_W + Adam
+    kernel: 33.6 M parameters, 72 rows) against the library's own unfused
+    gradient (pdf_grad_loss, pinned to the reference by test_cfg5_single_step)
+    followed by Adam in torch float64 (network.py:248-264): every parameter,
+    first and second moment."""
+    from oracle import pdf_oracle as O
+    st, g = cfg5
+    dev = _dev(st, g["data"])
+    dev.net_setup(torch.as_tensor(g["alpha0"][None], device="cuda"))
+    flat = O.flat(O.init_net(g["alpha0"].shape[1], np.random.default_rng(5)))
+    flat = flat + 0.02 * np.random.default_rng(7).standard_normal(flat.size)
+    th, m, v = dev.alloc_state(torch.as_tensor(flat[None], device="cuda"))
+    ref_t, ref_m, ref_v = th.clone(), m.clone(), v.clone()
+    lr, b1, b2, eps = 1e-2, 0.9, 0.999, 1e-8
+    trace = torch.zeros(2, 1, 6, dtype=torch.float64, device="cuda")
+    for t in (1, 2):
+        grad, _ = dev.grad_loss(ref_t.contiguous())
+        gr = grad.clone()
+        ref_m = b1 * ref_m + (1 - b1) * gr
+        ref_v = b2 * ref_v + (1 - b2) * gr * gr
+        mh, vh = ref_m / (1 - b1 ** t), ref_v / (1 - b2 ** t)
+        ref_t = ref_t - lr * mh / (torch.sqrt(vh) + eps)
+        dev.train(th, m, v, t - 1, 1, trace[t - 1:t], use_graph=False)
+        dev.check_errors()
+        assert torch.max(torch.abs(m - ref_m)).item() <= 1e-14 * torch.max(torch.abs(ref_m)).item() + 1e-300
+        assert torch.max(torch.abs(v - ref_v)).item() <= 1e-14 * torch.max(torch.abs(ref_v)).item() + 1e-300
+        assert torch.max(torch.abs(th - ref_t)).item() < 1e-12
