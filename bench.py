@@ -127,7 +127,46 @@ class ClockSampler:
         self.stop = threading.Event()
         self.th = None
 
+    def _nvml(self):
+        """NVML handle for fast sampling (a query takes well under a millisecond, so the
+        ~0.2 s headline region gets tens of samples); None: fall back to nvidia-smi."""
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = self.index
+            if vis:
+                ids = [x.strip() for x in vis.split(",") if x.strip()]
+                if self.index < len(ids) and ids[self.index].isdigit():
+                    idx = int(ids[self.index])
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+        except Exception:
+            return None
+
     def _run(self):
+        nv = self._nvml()
+        if nv is not None:
+            pynvml, h = nv
+            bits = ((0x8, 3), (0x40, 4), (0x20, 5), (0x4, 6))   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            try:
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            except Exception:
+                mx = 0
+            while not self.stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    try:
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    row = [str(sm), str(mx), "", "", "", "", ""]
+                    for bit, pos in bits:
+                        row[pos] = "Active" if rs & bit else "Not Active"
+                    self.samples.append(row)
+                except Exception:
+                    pass
+                self.stop.wait(0.005)
+            return
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -736,14 +775,20 @@ def run_ours(args, d: Dist):
     h2d = data[0].nbytes + M * M * 16 + int(dev.n_params) * 8     # data, chi_true, the run's initial weights
     d2h = 3 * M * M * 16 + k * 6 * 8 + 6 * 8 + 8
 
-    batched = batched_leg(args, d, e_inc, fp64, hbm, notes) if args.batch else None
+    # the other legs' timed regions are sampled as well: `clocks` is the headline
+    # region, `clocks.by_leg` the batched and large legs (the 256-scene batch runs
+    # into the software power cap)
+    with ClockSampler(d.local) as clk_b:
+        batched = batched_leg(args, d, e_inc, fp64, hbm, notes) if args.batch else None
 
     large = None
-    if args.large_iters:
-        try:
-            large = large_leg(args, d, fp64, hbm, notes)
-        except Exception as ex:   # reported, never fatal for the headline line
-            large = {"error": f"{type(ex).__name__}: {ex}"}
+    with ClockSampler(d.local) as clk_l:
+        if args.large_iters:
+            try:
+                large = large_leg(args, d, fp64, hbm, notes)
+            except Exception as ex:   # reported, never fatal for the headline line
+                large = {"error": f"{type(ex).__name__}: {ex}"}
+    by_leg = {"batched": clk_b.summary(), "large": clk_l.summary()}
 
     cpu = None
     if d.rank == 0 and not args.no_cpu_baseline:
@@ -765,7 +810,8 @@ def run_ours(args, d: Dist):
             "roofline": roof, "kernels_in_graph": legroof.get("kernels") if legroof else None,
             "iteration_period_us": legroof.get("iteration_period_us") if legroof else None,
             "path_roofline": proof, "phases_ms_events": phases_ev, "fp64_peak_tflops_measured": fp64,
-            "cpu_baseline": cpu, "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "clocks": dict(clk.summary(), by_leg=by_leg),
             "gpu_launches": args.steps * (1 + launches_per_iter * k), "batched": batched, "large": large}
     if d.rank == 0:
         print(json.dumps(line), flush=True)
