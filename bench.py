@@ -788,7 +788,8 @@ def run_ours(args, d: Dist):
                 large = large_leg(args, d, fp64, hbm, notes)
             except Exception as ex:   # reported, never fatal for the headline line
                 large = {"error": f"{type(ex).__name__}: {ex}"}
-    by_leg = {"batched": clk_b.summary(), "large": clk_l.summary()}
+    by_leg = {"batched": clk_b.summary() if args.batch else None,
+              "large": clk_l.summary() if args.large_iters else None}
 
     cpu = None
     if d.rank == 0 and not args.no_cpu_baseline:
