@@ -478,7 +478,7 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
   // 1/4 142, 1/8 151, 2/4 150, 2/8 160 us; cfg2 8.2-8.9 us for all)
   const long long rows1 = (long long)(c->M / c->TX) * c->M * c->d.S;
   const bool batch = rows1 > 4 * 148;
-  // throughput regime: three streaming kernels (pdf_pixel_stream.cuh; cfg4 579 -> 367 us, cfg5 142 -> 86 us)
+  // throughput regime: three streaming kernels (pdf_pixel_stream.cuh; cfg4 579 -> 326 us, cfg5 142 -> 86 us)
   static const int stream_env = env_int("PDF_PIX_STREAM", 1);
   if (batch && stream_env) {
     PixStreamArgs<T> q = {};
@@ -491,10 +491,17 @@ static int phys_pixel(pdf_ctx* c, void* chi_out, cudaStream_t st) {
     // from it, measured slower: 372 us in one launch, 398 / 431 / 620 us in
     // chunks of 80 / 40 / 20 MiB -- the per-chunk launches' ramps and tails)
     cudaError_t e = plain_launch(pix_sums_kernel<T>, dim3((unsigned)(img / 32), c->d.S), dim3(256), 0, st, qargs);
-    q.p.tl = 0;
-    if (e == cudaSuccess)
-      e = plain_launch(pix_point_kernel<T, GRAD, 4>, dim3(c->M / c->TX, c->M / 4, c->d.S), dim3(128), 0, st, qargs);
-    if (GRAD && e == cudaSuccess) {
+    // gradient pass fused into the per-pixel kernel for <= 32 views (cfg4); many
+    // views (cfg5's 72) keep the separate pass, split over groups of views
+    static const int fuse_env = env_int("PDF_PIX_FUSE", 1);
+    const bool fuse = GRAD && fuse_env && c->d.n <= 32;
+    q.p.tl = fuse ? p.tl : 0;
+    if (e == cudaSuccess) {
+      const dim3 pg(c->M / c->TX, c->M / 4, c->d.S);
+      e = fuse ? plain_launch(pix_point_kernel<T, GRAD, 4, true>, pg, dim3(128), 0, st, qargs)
+               : plain_launch(pix_point_kernel<T, GRAD, 4, false>, pg, dim3(128), 0, st, qargs);
+    }
+    if (GRAD && !fuse && e == cudaSuccess) {
       q.p.tl = p.tl;
       e = plain_launch(pix_grad_kernel<T>, dim3((unsigned)((img + 255) / 256), (c->d.n + PG_VIEWS - 1) / PG_VIEWS, c->d.S),
                        dim3(256), 0, st, qargs);

@@ -93,7 +93,12 @@ __global__ void __launch_bounds__(256) pix_sums_kernel(PixStreamArgs<T> a) {
 
 // CTA = TY image rows x TX columns of a scene; everything per pixel.  The
 // stencil terms are the ones of pixel_kernel (same expressions, same order).
-template <typename T, bool GRAD, int TY>
+// FUSE (with GRAD): the gradient pass over the views runs in this kernel, thread
+// = pixel (a warp = 32 consecutive pixels of a row): the coefficients stay in
+// registers and the per-pixel arithmetic of one CTA hides behind the field
+// streaming of the others on its SM (pix_point + pix_grad as two launches:
+// 79 + 168 us at cfg4, the second with 16 % of its issue slots used).
+template <typename T, bool GRAD, int TY, bool FUSE>
 __global__ void __launch_bounds__(128) pix_point_kernel(PixStreamArgs<T> a) {
   constexpr int W = PIX_TX + 2, HR = TY + 2;
   __shared__ C<T> chis[HR][W];
@@ -153,6 +158,8 @@ __global__ void __launch_bounds__(128) pix_point_kernel(PixStreamArgs<T> a) {
   __syncthreads();
   // pixel (row pr, column pc): one warp per image row of the tile (TY <= 4 warps)
   double vs = 0.0, vb_ = 0.0, vt = 0.0, vr = 0.0;
+  C<T> fR = czero<T>(), fgn = czero<T>();   // the pixel's R and LS-quotient adjoint coefficients
+  T fgd = T(0);
   const int pr = warp, pc = lane;
   if (pr < TY && pc < TX) {
     const int x = x0 + pc, y = y0 + pr, c1 = pc + 1, hr = pr + 1;
@@ -209,15 +216,54 @@ __global__ void __launch_bounds__(128) pix_point_kernel(PixStreamArgs<T> a) {
       C<T> gchi = g;
       if (!a.p.rfixed) gchi = cadd<T>(gchi, cmul<T>(chn, gr));
       const T den = den0 + eps;
-      double* co = a.coef + ((size_t)scene * img + p) * 6;
-      co[0] = (double)R_.x;
-      co[1] = (double)R_.y;
-      co[2] = (double)(gchi.x / den);
-      co[3] = (double)(gchi.y / den);
-      co[4] = (double)(-(gchi.x * chi.x + gchi.y * chi.y) / den);   // -Re(conj(g_chi) chi) / den
+      fR = R_;
+      fgn = mk<T>(gchi.x / den, gchi.y / den);
+      fgd = -(gchi.x * chi.x + gchi.y * chi.y) / den;   // -Re(conj(g_chi) chi) / den
+      if constexpr (!FUSE) {
+        double* co = a.coef + ((size_t)scene * img + p) * 6;
+        co[0] = (double)fR.x;
+        co[1] = (double)fR.y;
+        co[2] = (double)fgn.x;
+        co[3] = (double)fgn.y;
+        co[4] = (double)fgd;
+      }
     }
   }
   pdl_trigger();
+  if constexpr (GRAD && FUSE) {
+    if (pr < TY && pc < TX) {
+      const size_t pix = (size_t)(y0 + pr) * M + x0 + pc;
+      const T beta = a.p.beta;
+      const T gsc = T(2.0 / a.p.c_inc[scene]);
+      auto one = [&](size_t o, C<T> j, C<T> e) {
+        const C<T> P = mk<T>(e.x + beta * j.x, e.y + beta * j.y);
+        const C<T> Sr = csub<T>(cmul<T>(fR, P), mk<T>(beta * j.x, beta * j.y));
+        const C<T> gS = cscale<T>(Sr, gsc);
+        const C<T> gP = cmul<T>(conj_<T>(fR), gS);
+        C<T> gj = cscale<T>(csub<T>(gP, gS), beta);
+        gj = cadd<T>(gj, cmul<T>(e, fgn));
+        C<T> ge = cadd<T>(gP, cmul<T>(conj_<T>(fgn), j));
+        ge = cadd<T>(ge, cscale<T>(e, T(2) * fgd));
+        a.p.gJ[o] = gj;
+        a.p.gE[o] = ge;
+      };
+      const size_t o0 = (size_t)scene * n * img + pix;
+      int i = 0;
+      for (; i + 3 < n; i += 4) {   // four views in flight per thread
+        const size_t oa = o0 + (size_t)i * img, ob = oa + img, oc = ob + img, od = oc + img;
+        const C<T> ja = a.p.J[oa], ea = a.p.E[oa], jb = a.p.J[ob], eb = a.p.E[ob];
+        const C<T> jc = a.p.J[oc], ec = a.p.E[oc], jd = a.p.J[od], ed = a.p.E[od];
+        one(oa, ja, ea);
+        one(ob, jb, eb);
+        one(oc, jc, ec);
+        one(od, jd, ed);
+      }
+      for (; i < n; ++i) {
+        const size_t oa = o0 + (size_t)i * img;
+        one(oa, a.p.J[oa], a.p.E[oa]);
+      }
+    }
+  }
   // loss partials per image row: a TX-lane tree over the row's pixels
   if (pr < TY) {
     for (int o = TX / 2; o >= 1; o >>= 1) {
@@ -232,6 +278,7 @@ __global__ void __launch_bounds__(128) pix_point_kernel(PixStreamArgs<T> a) {
       o4[0] = vs; o4[1] = vb_; o4[2] = vt; o4[3] = vr;
     }
   }
+  if constexpr (FUSE) tl_mark(a.p.tl, 2);
 }
 
 // thread = pixel, grid.y = group of up to PG_VIEWS views, grid.z = scene
